@@ -1,0 +1,186 @@
+/*
+ * sts_b200.h — C-ABI of the B200-native STS (Speculative Token Sparsity)
+ * sparse-attention hot path.  libsts_b200.so exports exactly these symbols.
+ *
+ * Conventions
+ *   - Every pointer argument named *_dev / listed as "device" is a CUDA device
+ *     pointer; every function is asynchronous on the given cudaStream_t
+ *     (passed as void* so this header needs no CUDA include).
+ *   - No function throws.  Return value: 0 ok, 1 input/config error
+ *     (reference ConfigError/InputError, src/errors.py:15,27), 2 contract
+ *     violation (reference ContractViolation, src/errors.py:19), 3 CUDA error.
+ *     The message of the last failure on the calling thread is returned by
+ *     sts_last_error().
+ *   - Re-entrant per stream; no global mutable device state; the caller owns
+ *     every buffer (outputs and workspace are caller-allocated, so nothing is
+ *     allocated on the hot path).
+ *
+ * The reference (pkg/src/specsparse, pure numpy) has no FFI.  Each entry point
+ * below replaces the reference Python function(s) named in its comment; the
+ * Python host package paper_2605_15508_b200 re-exports the reference names on
+ * top of these (see INTEGRATION.md for the ctypes binding).
+ */
+#ifndef STS_B200_H
+#define STS_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define STS_API __attribute__((visibility("default")))
+#else
+#define STS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STS_ABI_VERSION 1
+
+#define STS_OK 0
+#define STS_ERR_INPUT 1
+#define STS_ERR_CONTRACT 2
+#define STS_ERR_CUDA 3
+
+#define STS_DTYPE_F32 0
+#define STS_DTYPE_BF16 1
+
+/* selection extras (SparsityConfig.include_current / include_sink,
+ * src/sparsity.py:46-47) */
+#define STS_SEL_CURRENT 0x1u
+#define STS_SEL_SINK 0x2u
+
+/* device status word bits (written by kernels into *status_dev, never cleared
+ * by them; the host reads it after a sync when validation is wanted) */
+#define STS_DEV_IDX_CAPACITY 0x1 /* an index list exceeded idx_ld           */
+#define STS_DEV_EMPTY_ROW 0x2    /* a query row had no admissible key       */
+#define STS_DEV_BAD_INDEX 0x4    /* an index was outside the cached context */
+
+STS_API const char* sts_last_error(void);
+STS_API int sts_abi_version(void);
+
+/* ------------------------------------------------------------------------
+ * sts_select_topk — sparsity-mask construction.
+ * Replaces sparsity._select_row / draft_masks_decode / draft_masks_prefill
+ * (src/sparsity.py:86-130), numkit.topk_indices (src/numkit.py:74-86),
+ * sparsity.page_aggregate (src/sparsity.py:72-83) and, through row_src, the
+ * head remap of remap_masks (src/sparsity.py:133-149) and the mode-S
+ * reduction.
+ *
+ * Logical row r in [0, rows):
+ *   n_r   = row_len_dev ? row_len_dev[r] : n_common           (positions)
+ *   v_r[j]= fp32 sum, in s order, of scores[src(r,s)*ld + j], s < nsrc,
+ *           src(r,s) = row_src_dev ? row_src_dev[r*nsrc+s] : r (nsrc==1)
+ *   b_r   = budget_is_fraction ? max(1, ceil(budget*n_r)) : (int)budget
+ *   out   = sorted unique indices: dense [0,n_r) if b_r >= n_r, else the
+ *           top-b_r tokens (page_size==1) or the tokens of the top
+ *           ceil(b_r/page_size) pages by fp64 page sum in numpy reduceat
+ *           order; plus extras (n_r-1 if CURRENT, 0 if SINK, the last
+ *           recent_window positions); then the tail n_r .. n_r+tail_len-1.
+ *   Ranking: score descending, ties to the lower index, -0.0 == +0.0, NaN
+ *   below everything (identical to the stable argsort of src/numkit.py:84).
+ * idx_out_dev[r*idx_ld + i], i < cnt_out_dev[r]: int32 ascending.
+ * ---------------------------------------------------------------------- */
+STS_API size_t sts_select_workspace_bytes(int64_t rows, int32_t max_len, int32_t page_size);
+STS_API int sts_select_topk(const float* scores_dev, int64_t ld, const int32_t* row_src_dev,
+                    int32_t nsrc, int64_t rows, const int32_t* row_len_dev,
+                    int32_t n_common, double budget, int32_t budget_is_fraction,
+                    int32_t page_size, uint32_t flags, int32_t recent_window,
+                    int32_t tail_len, int32_t* idx_out_dev, int64_t idx_ld,
+                    int32_t* cnt_out_dev, int32_t* status_dev, void* workspace_dev,
+                    size_t workspace_bytes, void* stream);
+
+/* sts_page_aggregate — page scores alone (src/sparsity.py:72-83): out[r][pg]
+ * = fp64 sum of row r's tokens [pg*ps, min((pg+1)*ps, n_r)) in numpy
+ * add.reduceat order (x0 + pairwise(rest)); page_size 1 is the identity. */
+STS_API int sts_page_aggregate(const float* scores_dev, int64_t ld, int64_t rows, const int32_t* row_len_dev,
+                       int32_t n_common, int32_t page_size, double* out_dev, int64_t out_ld,
+                       void* stream);
+
+/* ------------------------------------------------------------------------
+ * sts_sparse_decode — gathered-KV sparse flash-decode of the gamma+1
+ * verification rows stacked with their GQA group (M = group*rows_per_head).
+ * Replaces the masked attention loop of toymodel._run_block
+ * (src/toymodel.py:315-348, rows via forward_block :430-455) and
+ * sparsity.sparse_attention (src/sparsity.py:152-173).
+ *
+ * unit u (e.g. (batch, layer, kv-head)): K/V rows at k_cache + u*kv_unit_stride
+ *   (elements), row p of d contiguous elements.  Queries q[u][M][d].
+ *   keys: idx_dev[u*idx_ld + j], j < cnt_dev[u]  (idx_dev NULL => dense
+ *   0..n_dense-1).  Row r attends key p iff
+ *     (causal_base < 0 || pos_offset + p - causal_base <= r % rows_per_head)
+ *     && (member_dev == NULL || bit r of member_dev[u*idx_ld + j]).
+ *   out[u][M][d] (dtype) = softmax_S(q.k*scale) V ; lse_dev[u][M] = natural
+ *   log-sum-exp of the scaled scores (nullable).  dtype F32 computes in fp32
+ *   on CUDA cores (parity path); BF16 uses tensor cores with fp32 accumulate.
+ * ---------------------------------------------------------------------- */
+STS_API size_t sts_sparse_decode_workspace_bytes(int64_t units, int32_t M, int32_t d, int32_t splits);
+/* split-K factor that fills 148 SMs x 2 CTAs in whole waves (>= 8 key tiles
+ * of 16 per CTA); what the host uses when it has no better knowledge. */
+STS_API int32_t sts_auto_splits(int64_t units, int64_t keys_per_unit);
+STS_API int sts_sparse_decode(int32_t dtype, const void* q_dev, const void* k_cache_dev,
+                      const void* v_cache_dev, int64_t kv_unit_stride, int64_t units,
+                      int32_t M, int32_t d, const int32_t* idx_dev, int64_t idx_ld,
+                      const int32_t* cnt_dev, int32_t n_dense, const uint32_t* member_dev,
+                      int32_t causal_base, int32_t rows_per_head, int32_t pos_offset,
+                      float scale, void* out_dev, float* lse_dev, int32_t splits,
+                      int32_t* status_dev, void* workspace_dev, size_t workspace_bytes,
+                      void* stream);
+
+/* ------------------------------------------------------------------------
+ * sts_draft_scores — draft-score capture (ForwardRecord.attention of the
+ * draft's decode, src/toymodel.py:349-350 via specdec.propose
+ * src/specdec.py:150-167), computed for the R speculative rows at once.
+ *
+ * unit u = (draft layer, draft kv-head); q[u][G*R][d] with row index
+ * hh*R + i (hh = q-head within the GQA group, i = speculative row); row i sits
+ * at global position base+i and sees keys with global position <= base+i.
+ * The unit's n_keys K rows hold global positions pos_offset .. .
+ *   lse_dev[u][G*R]: natural log-sum-exp of the scaled scores over the local
+ *                    keys (sts_draft_lse), or the global one (input to
+ *                    sts_draft_probs when the KV is sequence-sharded).
+ *   mode 0 (S): out[u][hh][j] = sum_i p_{hh,i}[j], fp32, i ascending, for
+ *               local j with global position < base (committed prefix).
+ *   mode 1 (R): out[(u*G+hh)*R + i][j] = p_{hh,i}[j] for pos <= base+i.
+ *   (row stride out_ld floats)
+ * ---------------------------------------------------------------------- */
+STS_API size_t sts_draft_workspace_bytes(int64_t units, int32_t GR, int32_t n_keys);
+STS_API int sts_draft_lse(int32_t dtype, const void* q_dev, const void* k_cache_dev,
+                  int64_t kv_unit_stride, int64_t units, int32_t G, int32_t R, int32_t d,
+                  int32_t n_keys, int32_t pos_offset, int32_t base, float scale,
+                  float* lse_dev, void* workspace_dev, size_t workspace_bytes, void* stream);
+STS_API int sts_draft_probs(int32_t dtype, const void* q_dev, const void* k_cache_dev,
+                    int64_t kv_unit_stride, int64_t units, int32_t G, int32_t R, int32_t d,
+                    int32_t n_keys, int32_t pos_offset, int32_t base, float scale,
+                    const float* lse_dev, int32_t mode, float* out_dev, int64_t out_ld,
+                    void* stream);
+
+/* ------------------------------------------------------------------------
+ * sts_lse_merge — merge P partial attention results (split-K or
+ * sequence shards): LSE = log sum_p exp(LSE_p), O = sum_p exp(LSE_p-LSE) O_p.
+ * o_part[p][rows][d] fp32 (nullable => only the LSE), lse_part[p][rows].
+ * out dtype F32 or BF16 [rows][d] (nullable), lse_out[rows] (nullable).
+ * ---------------------------------------------------------------------- */
+STS_API int sts_lse_merge(const float* o_part_dev, const float* lse_part_dev, int32_t nparts,
+                  int64_t rows, int32_t d, int32_t out_dtype, void* out_dev,
+                  float* lse_out_dev, void* stream);
+
+/* ------------------------------------------------------------------------
+ * sts_row_union — mode R (reference-exact per-row masks) under GQA: build,
+ * for each unit, the sorted union of the M per-row index lists together with
+ * a membership bit per (row, key) for sts_sparse_decode.
+ * lists: row m of unit u is list src_dev[u*M+m] of a selection output
+ * (idx_in_dev[list*in_ld + i], i < cnt_in_dev[list]) — the src table is the
+ * remap of remap_masks (src/sparsity.py:141).  M <= 32.
+ * bitmap_ws: units*n_max uint32 scratch (zeroed by this call).
+ * ---------------------------------------------------------------------- */
+STS_API int sts_row_union(const int32_t* idx_in_dev, int64_t in_ld, const int32_t* cnt_in_dev,
+                  const int32_t* src_dev, int64_t units, int32_t M, int32_t n_max,
+                  uint32_t* bitmap_ws_dev, int32_t* idx_out_dev, uint32_t* member_out_dev,
+                  int64_t out_ld, int32_t* cnt_out_dev, int32_t* status_dev, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STS_B200_H */

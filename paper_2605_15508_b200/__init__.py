@@ -1,0 +1,54 @@
+"""B200-native (sm_100a) STS sparse-attention hot path.
+
+Drop-in for the hot-path subset of the reference package ``specsparse``
+(src/__init__.py:55-102): the sparsity API (SparsityConfig, page_aggregate,
+draft_masks_decode, draft_masks_prefill, remap_masks, sparse_attention,
+dump_masks), the head-mapping tables (HeadMapping, MappingSet), the error
+classes, and the batched device pipeline (``verify.STSVerifyStep``) that
+replaces propose -> _verification_masks -> verify for gamma+1 stacked rows.
+
+All compute runs in libsts_b200.so (include/sts_b200.h); there is no CPU
+fallback.
+"""
+
+from .errors import (
+    CapacityError,
+    ConfigError,
+    ContractViolation,
+    DeviceError,
+    InputError,
+    SpecSparseError,
+)
+from .headmap import HeadMapping, MappingSet, load_mapping
+from .sparsity import (
+    SparsityConfig,
+    draft_masks_decode,
+    draft_masks_prefill,
+    dump_masks,
+    page_aggregate,
+    remap_masks,
+    sparse_attention,
+    verification_masks,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "CapacityError",
+    "ConfigError",
+    "ContractViolation",
+    "DeviceError",
+    "HeadMapping",
+    "InputError",
+    "MappingSet",
+    "SparsityConfig",
+    "SpecSparseError",
+    "draft_masks_decode",
+    "draft_masks_prefill",
+    "dump_masks",
+    "load_mapping",
+    "page_aggregate",
+    "remap_masks",
+    "sparse_attention",
+    "verification_masks",
+]

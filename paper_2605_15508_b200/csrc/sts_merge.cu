@@ -1,0 +1,142 @@
+// sts_merge.cu — log-sum-exp merge of partial attention results (split-K
+// partials inside one GPU, or per-rank partials of the sequence-sharded path),
+// and the mode-R row-union builder.
+#include "sts_common.cuh"
+
+namespace sts {
+namespace {
+
+constexpr int MERGE_WARPS = 8;
+
+__global__ void __launch_bounds__(MERGE_WARPS * 32) lse_merge_kernel(
+    const float* __restrict__ o_part, const float* __restrict__ lse_part, int nparts, int64_t rows,
+    int d, int out_dtype, void* out, float* lse_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * MERGE_WARPS + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  float m = -INFINITY;
+  for (int q = 0; q < nparts; ++q) m = fmaxf(m, lse_part[(int64_t)q * rows + row]);
+  float tot = 0.f;
+  if (m != -INFINITY)
+    for (int q = 0; q < nparts; ++q) tot += expf(lse_part[(int64_t)q * rows + row] - m);
+  if (lane == 0 && lse_out) lse_out[row] = tot > 0.f ? m + logf(tot) : -INFINITY;
+  if (!out || !o_part) return;
+  for (int e = lane; e < d; e += 32) {
+    float acc = 0.f;
+    if (tot > 0.f) {
+      for (int q = 0; q < nparts; ++q) {
+        const float l = lse_part[(int64_t)q * rows + row];
+        if (l == -INFINITY) continue;
+        acc += expf(l - m) * o_part[((int64_t)q * rows + row) * d + e];
+      }
+      acc /= tot;
+    }
+    if (out_dtype == STS_DTYPE_BF16)
+      static_cast<__nv_bfloat16*>(out)[row * d + e] = __float2bfloat16_rn(acc);
+    else
+      static_cast<float*>(out)[row * d + e] = acc;
+  }
+}
+
+// ---- mode-R union ----------------------------------------------------------
+__global__ void union_scatter_kernel(const int32_t* __restrict__ idx_in, int64_t in_ld,
+                                     const int32_t* __restrict__ cnt_in, const int32_t* __restrict__ src,
+                                     int M, int n_max, uint32_t* bitmap, int32_t* status) {
+  const int64_t u = blockIdx.y;
+  const int m = blockIdx.z;
+  const int list = src[u * M + m];
+  const int c = cnt_in[list];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x) {
+    const int j = idx_in[(int64_t)list * in_ld + i];
+    if (j < 0 || j >= n_max) {
+      set_status(status, STS_DEV_BAD_INDEX);
+      continue;
+    }
+    atomicOr(&bitmap[u * n_max + j], 1u << m);
+  }
+}
+
+constexpr int UNION_THREADS = 1024;
+
+__global__ void __launch_bounds__(UNION_THREADS) union_compact_kernel(
+    const uint32_t* __restrict__ bitmap, int n_max, int32_t* idx_out, uint32_t* member_out,
+    int64_t out_ld, int32_t* cnt_out, int32_t* status) {
+  __shared__ int warp_tot[UNION_THREADS / 32];
+  const int64_t u = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int run = 0;
+  for (int base = 0; base < n_max; base += UNION_THREADS) {
+    const int j = base + threadIdx.x;
+    const uint32_t bits = j < n_max ? bitmap[u * n_max + j] : 0u;
+    const bool f = bits != 0u;
+    const uint32_t bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) warp_tot[warp] = __popc(bal);
+    __syncthreads();
+    int before = 0, tot = 0;
+    for (int w = 0; w < UNION_THREADS / 32; ++w) {
+      before += w < warp ? warp_tot[w] : 0;
+      tot += warp_tot[w];
+    }
+    __syncthreads();
+    if (f) {
+      const int pos = run + before + __popc(bal & ((1u << lane) - 1u));
+      if (pos < out_ld) {
+        idx_out[u * out_ld + pos] = j;
+        member_out[u * out_ld + pos] = bits;
+      } else {
+        set_status(status, STS_DEV_IDX_CAPACITY);
+      }
+    }
+    run += tot;
+  }
+  if (threadIdx.x == 0) cnt_out[u] = run < out_ld ? run : (int)out_ld;
+}
+
+}  // namespace
+
+int lse_merge_launch(const float* o_part, const float* lse_part, int nparts, int64_t rows, int d,
+                     int out_dtype, void* out, float* lse_out, cudaStream_t st) {
+  if (rows == 0) return STS_OK;
+  const int64_t blocks = (rows + MERGE_WARPS - 1) / MERGE_WARPS;
+  lse_merge_kernel<<<(unsigned)blocks, MERGE_WARPS * 32, 0, st>>>(o_part, lse_part, nparts, rows, d,
+                                                                  out_dtype, out, lse_out);
+  STS_LAUNCH_CHECK();
+  return STS_OK;
+}
+
+}  // namespace sts
+
+using namespace sts;
+
+extern "C" int sts_lse_merge(const float* o_part_dev, const float* lse_part_dev, int32_t nparts,
+                             int64_t rows, int32_t d, int32_t out_dtype, void* out_dev,
+                             float* lse_out_dev, void* stream) {
+  STS_REQUIRE(nparts >= 1 && rows >= 0 && d >= 1, STS_ERR_CONTRACT, "bad merge shape");
+  STS_REQUIRE(lse_part_dev, STS_ERR_CONTRACT, "null lse_part");
+  STS_REQUIRE(out_dtype == STS_DTYPE_F32 || out_dtype == STS_DTYPE_BF16, STS_ERR_CONTRACT, "bad dtype");
+  return lse_merge_launch(o_part_dev, lse_part_dev, nparts, rows, d, out_dtype, out_dev, lse_out_dev,
+                          static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int sts_row_union(const int32_t* idx_in_dev, int64_t in_ld, const int32_t* cnt_in_dev,
+                             const int32_t* src_dev, int64_t units, int32_t M, int32_t n_max,
+                             uint32_t* bitmap_ws_dev, int32_t* idx_out_dev, uint32_t* member_out_dev,
+                             int64_t out_ld, int32_t* cnt_out_dev, int32_t* status_dev, void* stream) {
+  STS_REQUIRE(units >= 0 && M >= 1 && M <= 32 && n_max >= 1, STS_ERR_CONTRACT, "bad union shape");
+  STS_REQUIRE(units <= 65535, STS_ERR_CONTRACT, "units must be <= 65535");
+  STS_REQUIRE(idx_in_dev && cnt_in_dev && src_dev && bitmap_ws_dev && idx_out_dev && member_out_dev &&
+                  cnt_out_dev,
+              STS_ERR_CONTRACT, "null buffer");
+  if (units == 0) return STS_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  STS_CUDA_CHECK(cudaMemsetAsync(bitmap_ws_dev, 0, (size_t)units * n_max * sizeof(uint32_t), st));
+  dim3 g1(8, (unsigned)units, (unsigned)M);
+  union_scatter_kernel<<<g1, 256, 0, st>>>(idx_in_dev, in_ld, cnt_in_dev, src_dev, M, n_max,
+                                           bitmap_ws_dev, status_dev);
+  STS_LAUNCH_CHECK();
+  union_compact_kernel<<<(unsigned)units, UNION_THREADS, 0, st>>>(bitmap_ws_dev, n_max, idx_out_dev,
+                                                                  member_out_dev, out_ld, cnt_out_dev,
+                                                                  status_dev);
+  STS_LAUNCH_CHECK();
+  return STS_OK;
+}

@@ -1,0 +1,455 @@
+// sts_select.cu — sparsity-mask construction on sm_100a.
+//
+// One CTA (1024 threads) per logical row.  The row's values are formed on the
+// fly (fp32 sum of nsrc source rows: identity for mode R, head-group sum for
+// mode S), turned into order-preserving integer keys, and the k-th largest
+// key is found by an MSB-first radix select with 12-bit digits and 4096-bin
+// shared-memory histograms.  The emit pass walks indices in ascending order
+// with ballot-based block scans, so ties at the threshold go to the lowest
+// indices (the stable-argsort rule of src/numkit.py:84) and the output comes
+// out sorted without a sort.
+//
+// Page mode (page_size > 1) reproduces src/sparsity.py:94-101: fp64 page sums
+// in numpy add.reduceat order (x0 + pairwise(x[1:]), see pairwise_sum), a
+// 64-bit-key radix select over pages, then page expansion.
+//
+// Keys live in shared memory when the row fits (<= SEL_SMEM_MAX_LEN), else in
+// a per-CTA slot of the global workspace (persistent grid over rows).
+#include "sts_common.cuh"
+
+namespace sts {
+namespace {
+
+constexpr int SEL_THREADS = 1024;
+constexpr int SEL_WARPS = SEL_THREADS / 32;
+constexpr int DIGIT_BITS = 12;
+constexpr int NBINS = 1 << DIGIT_BITS;
+constexpr int SEL_SMEM_MAX_LEN = 49152;
+
+struct SelectParams {
+  const float* scores;
+  int64_t ld;
+  const int32_t* row_src;
+  int nsrc;
+  int64_t rows;
+  const int32_t* row_len;
+  int n_common;
+  double budget;
+  int budget_is_fraction;
+  int page_size;
+  uint32_t flags;
+  int recent_window;
+  int tail_len;
+  int32_t* idx_out;
+  int64_t idx_ld;
+  int32_t* cnt_out;
+  int32_t* status;
+  uint8_t* gbuf;          // global key buffers (nullptr => shared memory)
+  int64_t gbuf_stride;    // bytes per CTA slot
+  int64_t buf_bytes;      // bytes of one key buffer (smem or global)
+};
+
+struct SelShared {
+  uint32_t hist[NBINS];
+  int warp_tot[SEL_WARPS];
+  int bcast[8];
+};
+
+// value of logical-row element j: fp32 sum over sources in order
+__device__ __forceinline__ float row_value(const SelectParams& p, const int32_t* srcs, int j) {
+  const float* base = p.scores;
+  float acc = base[(int64_t)srcs[0] * p.ld + j];
+  for (int s = 1; s < p.nsrc; ++s) acc = __fadd_rn(acc, base[(int64_t)srcs[s] * p.ld + j]);
+  return acc;
+}
+
+// numpy pairwise_sum (float64) over row values [start, start+n)
+__device__ double pairwise_sum(const SelectParams& p, const int32_t* srcs, int start, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, (double)row_value(p, srcs, start + i));
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = (double)row_value(p, srcs, start + j);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], (double)row_value(p, srcs, start + i + j));
+    }
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, (double)row_value(p, srcs, start + i));
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pairwise_sum(p, srcs, start, n2), pairwise_sum(p, srcs, start + n2, n - n2));
+}
+
+__device__ __forceinline__ double page_sum(const SelectParams& p, const int32_t* srcs, int start, int len) {
+  // np.add.reduceat segment: x[start] + pairwise(x[start+1 : start+len])
+  double x0 = (double)row_value(p, srcs, start);
+  if (len == 1) return x0;
+  return __dadd_rn(x0, pairwise_sum(p, srcs, start + 1, len - 1));
+}
+
+// Block-wide exclusive scan of a 0/1 flag in thread order; returns the
+// exclusive prefix and writes the block total.  Contains two barriers.
+__device__ __forceinline__ int block_scan_flag(bool f, int* warp_tot, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t bal = __ballot_sync(0xffffffffu, f);
+  int in_warp = __popc(bal & ((1u << lane) - 1u));
+  if (lane == 0) warp_tot[warp] = __popc(bal);
+  __syncthreads();
+  int before = 0, tot = 0;
+#pragma unroll 8
+  for (int w = 0; w < SEL_WARPS; ++w) {
+    int t = warp_tot[w];
+    before += (w < warp) ? t : 0;
+    tot += t;
+  }
+  __syncthreads();
+  total = tot;
+  return before + in_warp;
+}
+
+// Block-wide exclusive scan of an int in thread order.
+__device__ __forceinline__ int block_scan_int(int v, int* warp_tot, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  int before = 0, tot = 0;
+#pragma unroll 8
+  for (int w = 0; w < SEL_WARPS; ++w) {
+    int t = warp_tot[w];
+    before += (w < warp) ? t : 0;
+    tot += t;
+  }
+  __syncthreads();
+  total = tot;
+  return before + incl - v;
+}
+
+// Radix select: k-th largest key (1-based k <= n) among keys[0..n).
+// On return T is that key and need = how many keys equal to T belong to the
+// top-k (the rest of the top-k are strictly greater than T).
+template <typename K>
+__device__ void radix_select(const K* keys, int n, int k, SelShared& sh, K& T, int& need) {
+  constexpr int KBITS = sizeof(K) * 8;
+  K prefix = 0, pmask = 0;
+  int krem = k;
+  for (int shift = KBITS - DIGIT_BITS;; shift -= DIGIT_BITS) {
+    const int s = shift < 0 ? 0 : shift;
+    const int width = shift < 0 ? DIGIT_BITS + shift : DIGIT_BITS;
+    const int nb = 1 << width;
+    for (int i = threadIdx.x; i < nb; i += SEL_THREADS) sh.hist[i] = 0;
+    __syncthreads();
+    for (int j = threadIdx.x; j < n; j += SEL_THREADS) {
+      K key = keys[j];
+      bool in = (key & pmask) == prefix;
+      uint32_t dig = (uint32_t)((key >> s) & (K)(nb - 1));
+      // warp-aggregate lanes hitting the same bin (probability rows are
+      // exponent-concentrated, so bins collide heavily)
+      uint32_t active = __ballot_sync(__activemask(), in);
+      if (in) {
+        uint32_t peers = __match_any_sync(active, dig);
+        int leader = __ffs(peers) - 1;
+        if ((int)(threadIdx.x & 31) == leader) atomicAdd(&sh.hist[dig], (uint32_t)__popc(peers));
+      }
+    }
+    __syncthreads();
+    // descending scan over bins: thread t owns bins nb-1-4t .. nb-4-4t
+    int local[4];
+    int lsum = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      int b = nb - 1 - 4 * (int)threadIdx.x - q;
+      local[q] = (b >= 0) ? (int)sh.hist[b] : 0;
+      lsum += local[q];
+    }
+    int total;
+    int excl = block_scan_int(lsum, sh.warp_tot, total);
+    if (excl < krem && krem <= excl + lsum) {
+      int acc = excl;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (acc < krem && krem <= acc + local[q]) {
+          sh.bcast[0] = nb - 1 - 4 * (int)threadIdx.x - q;
+          sh.bcast[1] = acc;
+        }
+        acc += local[q];
+      }
+    }
+    __syncthreads();
+    const int digit = sh.bcast[0];
+    const int above = sh.bcast[1];
+    __syncthreads();
+    prefix |= (K)digit << s;
+    pmask |= (K)(nb - 1) << s;
+    krem -= above;
+    if (s == 0) break;
+  }
+  T = prefix;
+  need = krem;
+}
+
+__device__ __forceinline__ bool is_extra(const SelectParams& p, int j, int n) {
+  if ((p.flags & STS_SEL_CURRENT) && j == n - 1) return true;
+  if ((p.flags & STS_SEL_SINK) && j == 0) return true;
+  if (p.recent_window > 0 && j >= n - p.recent_window) return true;
+  return false;
+}
+
+__device__ __forceinline__ void write_idx(const SelectParams& p, int32_t* out, int pos, int val) {
+  if (pos < p.idx_ld) out[pos] = val;
+  else set_status(p.status, STS_DEV_IDX_CAPACITY);
+}
+
+__global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(SelectParams p) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  SelShared& sh = *reinterpret_cast<SelShared*>(smem_raw);
+  uint8_t* buf = p.gbuf ? (p.gbuf + (int64_t)blockIdx.x * p.gbuf_stride)
+                        : (smem_raw + ((sizeof(SelShared) + 15) & ~size_t(15)));
+
+  for (int64_t r = blockIdx.x; r < p.rows; r += gridDim.x) {
+    const int n = p.row_len ? p.row_len[r] : p.n_common;
+    int32_t* out = p.idx_out + r * p.idx_ld;
+    int32_t srcs_local[8];
+    const int32_t* srcs;
+    int32_t ident = (int32_t)r;
+    if (p.row_src) {
+      for (int s = 0; s < p.nsrc && s < 8; ++s) srcs_local[s] = p.row_src[r * p.nsrc + s];
+      srcs = srcs_local;
+    } else {
+      srcs = &ident;
+    }
+    int b;
+    if (p.budget_is_fraction) {
+      double c = ceil(p.budget * (double)n);
+      b = c < 1.0 ? 1 : (int)c;
+    } else {
+      b = (int)p.budget;
+    }
+
+    int count = 0;
+    if (n <= 0) {
+      // empty committed range: only the tail
+    } else if (b >= n) {
+      // dense fallback (src/sparsity.py:90-91)
+      for (int j = threadIdx.x; j < n; j += SEL_THREADS) write_idx(p, out, j, j);
+      count = n;
+    } else if (p.page_size == 1) {
+      uint32_t* keys = reinterpret_cast<uint32_t*>(buf);
+      for (int j = threadIdx.x; j < n; j += SEL_THREADS) keys[j] = f32_key(row_value(p, srcs, j));
+      __syncthreads();
+      uint32_t T;
+      int need;
+      radix_select<uint32_t>(keys, n, b, sh, T, need);
+      int run_sel = 0, run_tie = 0;
+      for (int base = 0; base < n; base += SEL_THREADS) {
+        const int j = base + threadIdx.x;
+        const bool valid = j < n;
+        const uint32_t key = valid ? keys[j] : 0u;
+        const bool tie = valid && key == T;
+        int tie_tot;
+        const int tie_ex = block_scan_flag(tie, sh.warp_tot, tie_tot);
+        const bool sel = valid && (key > T || (tie && run_tie + tie_ex < need) || is_extra(p, j, n));
+        int sel_tot;
+        const int sel_ex = block_scan_flag(sel, sh.warp_tot, sel_tot);
+        if (sel) write_idx(p, out, run_sel + sel_ex, j);
+        run_sel += sel_tot;
+        run_tie += tie_tot;
+      }
+      count = run_sel;
+    } else {
+      const int ps = p.page_size;
+      const int P = (n + ps - 1) / ps;
+      const int kp = (b + ps - 1) / ps;
+      uint64_t* pkeys = reinterpret_cast<uint64_t*>(buf);
+      uint32_t* pbits = reinterpret_cast<uint32_t*>(buf + (((int64_t)P * 8 + 15) & ~int64_t(15)));
+      for (int w = threadIdx.x; w < (P + 31) / 32; w += SEL_THREADS) pbits[w] = 0u;
+      if (kp >= P) {
+        __syncthreads();
+        for (int w = threadIdx.x; w < (P + 31) / 32; w += SEL_THREADS) pbits[w] = 0xffffffffu;
+      } else {
+        for (int pg = threadIdx.x; pg < P; pg += SEL_THREADS) {
+          const int start = pg * ps;
+          const int len = min(ps, n - start);
+          pkeys[pg] = f64_key(page_sum(p, srcs, start, len));
+        }
+        __syncthreads();
+        uint64_t T;
+        int need;
+        radix_select<uint64_t>(pkeys, P, kp, sh, T, need);
+        int run_tie = 0;
+        for (int base = 0; base < P; base += SEL_THREADS) {
+          const int pg = base + threadIdx.x;
+          const bool valid = pg < P;
+          const uint64_t key = valid ? pkeys[pg] : 0ull;
+          const bool tie = valid && key == T;
+          int tie_tot;
+          const int tie_ex = block_scan_flag(tie, sh.warp_tot, tie_tot);
+          const bool sel = valid && (key > T || (tie && run_tie + tie_ex < need));
+          uint32_t bal = __ballot_sync(0xffffffffu, sel);
+          if ((threadIdx.x & 31) == 0 && base + (int)threadIdx.x < P) pbits[(base + threadIdx.x) >> 5] = bal;
+          run_tie += tie_tot;
+        }
+      }
+      __syncthreads();
+      int run_sel = 0;
+      for (int base = 0; base < n; base += SEL_THREADS) {
+        const int j = base + threadIdx.x;
+        const bool valid = j < n;
+        bool sel = false;
+        if (valid) {
+          const int pg = j / ps;
+          sel = ((pbits[pg >> 5] >> (pg & 31)) & 1u) || is_extra(p, j, n);
+        }
+        int sel_tot;
+        const int sel_ex = block_scan_flag(sel, sh.warp_tot, sel_tot);
+        if (sel) write_idx(p, out, run_sel + sel_ex, j);
+        run_sel += sel_tot;
+      }
+      count = run_sel;
+    }
+    // in-block tail (mode S: the verify block's own positions)
+    for (int t = threadIdx.x; t < p.tail_len; t += SEL_THREADS) write_idx(p, out, count + t, max(n, 0) + t);
+    count += p.tail_len;
+    if (threadIdx.x == 0) p.cnt_out[r] = count;
+    __syncthreads();
+  }
+}
+
+// page_aggregate as a standalone op (src/sparsity.py:72-83): one thread per page
+__global__ void page_aggregate_kernel(SelectParams p, double* out, int64_t out_ld) {
+  const int64_t r = blockIdx.y;
+  const int n = p.row_len ? p.row_len[r] : p.n_common;
+  const int ps = p.page_size;
+  const int P = (n + ps - 1) / ps;
+  const int32_t ident = (int32_t)r;
+  for (int pg = blockIdx.x * blockDim.x + threadIdx.x; pg < P; pg += gridDim.x * blockDim.x) {
+    const int start = pg * ps;
+    out[r * out_ld + pg] = ps == 1 ? (double)row_value(p, &ident, start)
+                                   : page_sum(p, &ident, start, min(ps, n - start));
+  }
+}
+
+int64_t key_buf_bytes(int32_t max_len, int32_t page_size) {
+  int64_t tok = (int64_t)max_len * 4;
+  int64_t pages = page_size > 1 ? ((int64_t)max_len + page_size - 1) / page_size : 0;
+  int64_t pg = ((pages * 8 + 15) & ~int64_t(15)) + ((pages + 31) / 32) * 4 + 16;
+  int64_t b = tok > pg ? tok : pg;
+  return (b + 127) & ~int64_t(127);
+}
+
+}  // namespace
+}  // namespace sts
+
+using namespace sts;
+
+extern "C" size_t sts_select_workspace_bytes(int64_t rows, int32_t max_len, int32_t page_size) {
+  if (max_len <= SEL_SMEM_MAX_LEN) return 0;
+  int64_t slots = rows < 4 * num_sms() ? rows : 4 * num_sms();
+  return (size_t)(slots * key_buf_bytes(max_len, page_size));
+}
+
+extern "C" int sts_select_topk(const float* scores_dev, int64_t ld, const int32_t* row_src_dev,
+                               int32_t nsrc, int64_t rows, const int32_t* row_len_dev,
+                               int32_t n_common, double budget, int32_t budget_is_fraction,
+                               int32_t page_size, uint32_t flags, int32_t recent_window,
+                               int32_t tail_len, int32_t* idx_out_dev, int64_t idx_ld,
+                               int32_t* cnt_out_dev, int32_t* status_dev, void* workspace_dev,
+                               size_t workspace_bytes, void* stream) {
+  STS_REQUIRE(rows >= 0, STS_ERR_CONTRACT, "rows must be >= 0");
+  if (rows == 0) return STS_OK;
+  STS_REQUIRE(scores_dev && idx_out_dev && cnt_out_dev, STS_ERR_CONTRACT, "null buffer");
+  STS_REQUIRE(nsrc >= 1 && nsrc <= 8, STS_ERR_CONTRACT, "nsrc must be in [1, 8], got %d", nsrc);
+  STS_REQUIRE(row_src_dev || nsrc == 1, STS_ERR_CONTRACT, "nsrc > 1 needs a row_src table");
+  STS_REQUIRE(page_size >= 1, STS_ERR_INPUT, "page_size must be >= 1");
+  STS_REQUIRE(recent_window >= 0, STS_ERR_INPUT, "recent_window must be >= 0");
+  STS_REQUIRE(tail_len >= 0, STS_ERR_CONTRACT, "tail_len must be >= 0");
+  if (budget_is_fraction) {
+    STS_REQUIRE(budget > 0.0 && budget <= 1.0, STS_ERR_INPUT,
+                "fractional budget must be in (0, 1], got %g", budget);
+  } else {
+    STS_REQUIRE(budget >= 1.0, STS_ERR_INPUT, "token budget must be >= 1, got %g", budget);
+  }
+  STS_REQUIRE(row_len_dev || n_common >= 0, STS_ERR_CONTRACT, "n_common must be >= 0");
+  STS_REQUIRE(ld >= 1, STS_ERR_CONTRACT, "ld must be >= 1");
+  const int32_t max_len = row_len_dev ? (int32_t)ld : n_common;
+
+  SelectParams p;
+  p.scores = scores_dev;
+  p.ld = ld;
+  p.row_src = row_src_dev;
+  p.nsrc = nsrc;
+  p.rows = rows;
+  p.row_len = row_len_dev;
+  p.n_common = n_common;
+  p.budget = budget;
+  p.budget_is_fraction = budget_is_fraction;
+  p.page_size = page_size;
+  p.flags = flags;
+  p.recent_window = recent_window;
+  p.tail_len = tail_len;
+  p.idx_out = idx_out_dev;
+  p.idx_ld = idx_ld;
+  p.cnt_out = cnt_out_dev;
+  p.status = status_dev;
+  p.buf_bytes = key_buf_bytes(max_len, page_size);
+
+  const size_t sh_bytes = (sizeof(SelShared) + 15) & ~size_t(15);
+  size_t smem = sh_bytes;
+  int grid;
+  if (max_len <= SEL_SMEM_MAX_LEN) {
+    p.gbuf = nullptr;
+    p.gbuf_stride = 0;
+    smem += (size_t)p.buf_bytes;
+    grid = (int)(rows < (int64_t)1 << 30 ? rows : (1 << 30));
+  } else {
+    int64_t slots = rows < 4 * num_sms() ? rows : 4 * num_sms();
+    size_t need = (size_t)(slots * p.buf_bytes);
+    STS_REQUIRE(workspace_dev && workspace_bytes >= need, STS_ERR_CONTRACT,
+                "select workspace too small: need %zu bytes, got %zu", need, workspace_bytes);
+    p.gbuf = static_cast<uint8_t*>(workspace_dev);
+    p.gbuf_stride = p.buf_bytes;
+    grid = (int)slots;
+  }
+  STS_CUDA_CHECK(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  select_kernel<<<grid, SEL_THREADS, smem, static_cast<cudaStream_t>(stream)>>>(p);
+  STS_LAUNCH_CHECK();
+  return STS_OK;
+}
+
+extern "C" int sts_page_aggregate(const float* scores_dev, int64_t ld, int64_t rows,
+                                  const int32_t* row_len_dev, int32_t n_common, int32_t page_size,
+                                  double* out_dev, int64_t out_ld, void* stream) {
+  STS_REQUIRE(page_size >= 1, STS_ERR_CONTRACT, "page_size must be >= 1");
+  STS_REQUIRE(rows >= 0 && rows <= 65535, STS_ERR_CONTRACT, "rows must be in [0, 65535]");
+  if (rows == 0) return STS_OK;
+  STS_REQUIRE(scores_dev && out_dev, STS_ERR_CONTRACT, "null buffer");
+  SelectParams p;
+  memset(&p, 0, sizeof(p));
+  p.scores = scores_dev;
+  p.ld = ld;
+  p.nsrc = 1;
+  p.rows = rows;
+  p.row_len = row_len_dev;
+  p.n_common = n_common;
+  p.page_size = page_size;
+  const int32_t max_len = row_len_dev ? (int32_t)ld : n_common;
+  const int pages = (max_len + page_size - 1) / page_size;
+  dim3 grid((pages + 255) / 256 > 0 ? (pages + 255) / 256 : 1, (unsigned)rows);
+  page_aggregate_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(p, out_dev, out_ld);
+  STS_LAUNCH_CHECK();
+  return STS_OK;
+}

@@ -1,0 +1,211 @@
+"""Reference-named sparsity API, computed on the B200.
+
+Drop-in for ``specsparse.sparsity`` (src/sparsity.py) on the hot path: the
+same names, arguments, return types (dicts of int64 numpy index arrays,
+fp32 / fp64 numpy results) and exceptions, but every mask / page sum /
+attention is produced by libsts_b200.so kernels.  Inputs may be numpy arrays
+or torch tensors (CUDA tensors avoid the host->device copy).  For batched
+device-resident work use ``kernels`` / ``verify`` directly.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import kernels
+from .errors import ConfigError, ContractViolation
+from .headmap import HeadKey, HeadMapping
+
+SCOPE_DECODE = "decode"
+SCOPE_PREFILL_DECODE = "prefill-decode"
+
+
+@dataclass(frozen=True)
+class SparsityConfig:
+    """Budget, granularity and scope of mask generation (src/sparsity.py:33-69)."""
+
+    budget: float
+    page_size: int = 1
+    scope: str = SCOPE_DECODE
+    include_current: bool = True
+    include_sink: bool = False
+    recent_window: int = 0
+
+    def __post_init__(self) -> None:
+        if isinstance(self.budget, float) and not 0.0 < self.budget <= 1.0:
+            raise ConfigError(f"fractional budget must be in (0, 1], got {self.budget}")
+        if isinstance(self.budget, int) and self.budget < 1:
+            raise ConfigError(f"token budget must be >= 1, got {self.budget}")
+        if self.page_size < 1:
+            raise ConfigError("page_size must be >= 1")
+        if self.scope not in (SCOPE_DECODE, SCOPE_PREFILL_DECODE):
+            raise ConfigError(f"unknown scope {self.scope!r}")
+        if self.recent_window < 0:
+            raise ConfigError("recent_window must be >= 0")
+
+    def tokens_for_context(self, n: int) -> int:
+        if isinstance(self.budget, int):
+            return self.budget
+        return max(1, math.ceil(self.budget * n))
+
+    def sparse_prefill(self) -> bool:
+        return self.scope == SCOPE_PREFILL_DECODE
+
+    def select_kwargs(self) -> dict:
+        return dict(budget=self.budget, page_size=self.page_size, include_current=self.include_current,
+                    include_sink=self.include_sink, recent_window=self.recent_window)
+
+
+def _device():
+    if not torch.cuda.is_available():
+        raise RuntimeError("the STS B200 path needs a CUDA device (there is no CPU fallback)")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _pack_rows(rows, dev):
+    """list of 1-D float rows -> (fp32 [R, maxlen] device tensor, int32 lengths)."""
+    lens = [int(r.shape[0]) for r in rows]
+    width = max(max(lens), 1)
+    width = -(-width // 4) * 4
+    buf = torch.zeros((len(rows), width), dtype=torch.float32, device=dev)
+    for i, r in enumerate(rows):
+        t = r if isinstance(r, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(r, dtype=np.float32))
+        buf[i, : lens[i]] = t.to(device=dev, dtype=torch.float32)
+    return buf, torch.tensor(lens, dtype=torch.int32, device=dev)
+
+
+def _unpack(idx, cnt):
+    idx = idx.cpu().numpy()
+    cnt = cnt.cpu().numpy()
+    return [idx[i, : cnt[i]].astype(np.int64) for i in range(idx.shape[0])]
+
+
+def select_rows(rows, cfg: SparsityConfig, tail_len: int = 0):
+    """GPU _select_row over a list of rows (one launch); list of int64 arrays."""
+    if not rows:
+        return []
+    dev = _device()
+    buf, lens = _pack_rows(rows, dev)
+    idx, cnt = kernels.select_topk(buf, row_len=lens, tail_len=tail_len, **cfg.select_kwargs())
+    return _unpack(idx, cnt)
+
+
+def page_aggregate(scores, page_size: int) -> np.ndarray:
+    """fp64 page sums in numpy reduceat order (src/sparsity.py:72-83), on the GPU."""
+    if page_size < 1:
+        raise ContractViolation("page_size must be >= 1")
+    from . import _lib
+
+    arr = scores if isinstance(scores, torch.Tensor) else torch.from_numpy(np.asarray(scores, dtype=np.float32).ravel().copy())
+    dev = _device()
+    x = arr.to(device=dev, dtype=torch.float32).reshape(1, -1).contiguous()
+    n = x.shape[1]
+    pages = -(-n // page_size)
+    out = torch.empty((1, max(pages, 1)), dtype=torch.float64, device=dev)
+    if n > 0:
+        _lib.call("sts_page_aggregate", x.data_ptr(), max(n, 1), 1, None, n, page_size, out.data_ptr(),
+                  out.stride(0), _lib.stream_handle())
+    return out[0, :pages].cpu().numpy()
+
+
+def draft_masks_decode(rows: dict, cfg: SparsityConfig) -> dict:
+    """One index set per draft head from its attention row (src/sparsity.py:115-119)."""
+    heads = list(rows.keys())
+    masks = select_rows([rows[h] for h in heads], cfg)
+    return dict(zip(heads, masks))
+
+
+def draft_masks_prefill(matrices: dict, cfg: SparsityConfig) -> dict:
+    """Per-row masks over each causal prefix (src/sparsity.py:122-130); all
+    rows of all heads in one launch."""
+    flat, owners = [], []
+    for head, mat in matrices.items():
+        m = mat if isinstance(mat, torch.Tensor) else np.asarray(mat)
+        for t in range(m.shape[0]):
+            flat.append(m[t, : t + 1])
+            owners.append(head)
+    masks = select_rows(flat, cfg)
+    out: dict = {h: [] for h in matrices}
+    for h, m in zip(owners, masks):
+        out[h].append(m)
+    return out
+
+
+def remap_masks(draft_masks: dict, mapping: HeadMapping) -> dict:
+    """Copy each mapped draft head's mask to its target heads (src/sparsity.py:133-149).
+
+    Host bookkeeping only (dict of copies); the device pipeline performs the
+    same remap as an int32 indirection table (HeadMapping.to_table).
+    """
+    out: dict = {}
+    for target, (draft, _) in mapping.entries.items():
+        if draft not in draft_masks:
+            raise ContractViolation(f"no draft mask for head {draft} (target {target})")
+        value = draft_masks[draft]
+        if isinstance(value, list):
+            out[target] = [np.array(v, dtype=np.int64, copy=True) for v in value]
+        else:
+            out[target] = np.array(value, dtype=np.int64, copy=True)
+    return out
+
+
+def sparse_attention(q, keys, values, mask) -> np.ndarray:
+    """Single-query attention over the masked subset (src/sparsity.py:152-173),
+    computed by the fp32 gather kernel."""
+    idx = np.asarray(mask, dtype=np.int64).ravel()
+    if idx.size == 0:
+        raise ContractViolation("sparse attention needs a non-empty mask")
+    n = keys.shape[0]
+    if idx.min() < 0 or idx.max() >= n:
+        raise ContractViolation("mask index outside the cached context")
+    dev = _device()
+
+    def dev32(x):
+        t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.asarray(x, dtype=np.float32))
+        return t.to(device=dev, dtype=torch.float32).contiguous()
+
+    qd = dev32(q).reshape(1, 1, -1)
+    kd = dev32(keys).reshape(1, n, -1)
+    vd = dev32(values).reshape(1, n, -1)
+    it = torch.from_numpy(idx.astype(np.int32)).to(dev).reshape(1, -1)
+    cnt = torch.tensor([idx.size], dtype=torch.int32, device=dev)
+    out, _ = kernels.sparse_decode(qd, kd, vd, idx=it, cnt=cnt, splits=1)
+    return out[0, 0].cpu().numpy()
+
+
+def dump_masks(fh, step: int, masks: dict) -> None:
+    """Append one JSON document describing a step's masks (src/sparsity.py:176-185)."""
+    heads = {}
+    for (layer, head), value in sorted(masks.items()):
+        key = f"{layer}.{head}"
+        if isinstance(value, list):
+            heads[key] = [[int(i) for i in row] for row in value]
+        else:
+            heads[key] = [int(i) for i in value]
+    fh.write(json.dumps({"step": step, "heads": heads}, sort_keys=True) + "\n")
+
+
+def _clamp_current(indices, pos: int) -> np.ndarray:
+    """src/specdec.py:212-216."""
+    arr = np.asarray(indices, dtype=np.int64)
+    arr = arr[arr <= pos]
+    return np.union1d(arr, np.asarray([pos], dtype=np.int64))
+
+
+def verification_masks(draft_rows: list, base: int, sparsity: SparsityConfig, mapping: HeadMapping) -> dict:
+    """``specdec._verification_masks`` (src/specdec.py:219-233): every
+    (speculative row, draft head) is selected in ONE kernel launch, then
+    remapped to target heads and clamped to its row's position."""
+    heads = list(draft_rows[0].keys())
+    flat = [draft_rows[i][h] for i in range(len(draft_rows)) for h in heads]
+    masks = select_rows(flat, sparsity)
+    per_row = []
+    for i in range(len(draft_rows)):
+        dm = dict(zip(heads, masks[i * len(heads) : (i + 1) * len(heads)]))
+        per_row.append({t: _clamp_current(m, base + i) for t, m in remap_masks(dm, mapping).items()})
+    return {head: [per_row[i][head] for i in range(len(draft_rows))] for head in per_row[0]}

@@ -1,0 +1,274 @@
+"""One STS verify step on the GPU: draft-score capture -> mask build -> sparse
+target attention for the gamma+1 verification rows of every (batch, layer,
+kv-head).
+
+This is the device-resident form of the reference round
+(src/specdec.py:324-352): ``propose`` records draft attention rows
+(:150-167), ``_verification_masks`` turns them into per-target-head masks
+(:219-233), ``verify`` runs the masked target block (:170-209) and the
+correction decode adds the (gamma+1)-th row (:345-352).  Here all gamma+1
+rows are stacked (the vLLM layout) and processed in four launches:
+
+  1. sts_draft_lse    draft rows' log-sum-exp           (draft K read once)
+  2. sts_draft_probs  p = exp(s - lse), reduced (mode S) or per row (mode R)
+  3. sts_select_topk  radix top-k per target (layer, kv-head) [mode S] or per
+                      draft row [mode R] (+ sts_row_union for GQA, mode R)
+  4. sts_sparse_decode gathered flash-decode over the selected keys
+
+Mode S (north-star design): one key set per (layer, kv-head),
+scores summed over the gamma+1 rows and the GQA group's mapped draft heads;
+every row also attends its own in-block causal prefix.  Mode R
+(reference-exact): every (target head, row) keeps its own reference mask;
+the kernel gathers the union per kv-head and applies per-row membership bits.
+
+All buffers are allocated once in ``__init__``; ``step`` allocates nothing.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import kernels
+from .kernels import Workspace
+from .sparsity import SparsityConfig
+
+
+@dataclass(frozen=True)
+class VerifyShape:
+    batch: int
+    context: int          # committed positions (base); rows sit at base .. base+gamma
+    gamma: int
+    target_layers: int
+    target_q_heads: int
+    target_kv_heads: int
+    head_dim: int
+    draft_layers: int
+    draft_q_heads: int
+    draft_kv_heads: int
+    draft_head_dim: int
+
+    @property
+    def rows(self) -> int:  # R = gamma + 1 stacked verification rows
+        return self.gamma + 1
+
+    @property
+    def n_kv(self) -> int:  # positions in the cache during verify
+        return self.context + self.rows
+
+    @property
+    def target_group(self) -> int:
+        return self.target_q_heads // self.target_kv_heads
+
+    @property
+    def draft_group(self) -> int:
+        return self.draft_q_heads // self.draft_kv_heads
+
+    @property
+    def target_units(self) -> int:
+        return self.batch * self.target_layers * self.target_kv_heads
+
+    @property
+    def draft_units(self) -> int:
+        return self.batch * self.draft_layers * self.draft_kv_heads
+
+
+def random_mapping_table(shape: VerifyShape, seed: int = 0) -> np.ndarray:
+    """Synthetic head mapping: target (layer, q-head) -> flattened draft q-head
+    (draft_layer * draft_q_heads + draft_head), drawn uniformly (one-to-many,
+    global search like src/headmap.py:83-125 would produce)."""
+    rng = np.random.default_rng(seed)
+    n_draft = shape.draft_layers * shape.draft_q_heads
+    return rng.integers(0, n_draft, size=(shape.target_layers, shape.target_q_heads)).astype(np.int32)
+
+
+class STSVerifyStep:
+    """Preallocated GPU pipeline for one verify step (see module docstring)."""
+
+    def __init__(self, shape: VerifyShape, sparsity: SparsityConfig, mapping_table, mode: str = "S",
+                 device=None, splits=None):
+        if mode not in ("S", "R"):
+            raise ValueError("mode must be 'S' or 'R'")
+        if shape.target_q_heads % shape.target_kv_heads or shape.draft_q_heads % shape.draft_kv_heads:
+            raise ValueError("q heads must be a multiple of kv heads")
+        self.shape = s = shape
+        self.cfg = sparsity
+        self.mode = mode
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        R, base = s.rows, s.context
+        table = np.asarray(mapping_table, dtype=np.int64)
+        if table.shape != (s.target_layers, s.target_q_heads):
+            raise ValueError(f"mapping table must be [{s.target_layers}, {s.target_q_heads}]")
+        Gt = s.target_group
+        nd = s.draft_layers * s.draft_q_heads
+        # per-round budget (src/specdec.py:331): b(base + 1)
+        self.budget = sparsity.tokens_for_context(base + 1)
+        self.n_draft_cols = -(-s.n_kv // 4) * 4
+        self.ws_draft, self.ws_sel, self.ws_dec = Workspace(dev), Workspace(dev), Workspace(dev)
+
+        # draft side
+        self.draft_lse = torch.empty((s.draft_units, s.draft_group * R), dtype=torch.float32, device=dev)
+        if mode == "S":
+            self.draft_rows = torch.zeros((s.batch * nd, self.n_draft_cols), dtype=torch.float32, device=dev)
+            # row_src[(b, l, g), hh] = b*nd + table[l, g*Gt + hh]
+            src = (np.arange(s.batch)[:, None, None, None] * nd
+                   + table.reshape(1, s.target_layers, s.target_kv_heads, Gt))
+            self.row_src = torch.from_numpy(src.reshape(-1, Gt).astype(np.int32)).to(dev)
+            self.idx_ld = kernels.index_capacity(base, self.budget, sparsity.page_size, False,
+                                                 sparsity.include_sink, sparsity.recent_window, R)
+            self.idx = torch.empty((s.target_units, self.idx_ld), dtype=torch.int32, device=dev)
+            self.cnt = torch.empty((s.target_units,), dtype=torch.int32, device=dev)
+            self.member = None
+        else:
+            rows_total = s.batch * nd * R
+            self.draft_rows = torch.zeros((rows_total, self.n_draft_cols), dtype=torch.float32, device=dev)
+            self.row_len = torch.from_numpy(np.tile(base + 1 + np.arange(R, dtype=np.int32), s.batch * nd)).to(dev)
+            self.sel_ld = kernels.index_capacity(s.n_kv, sparsity.budget, sparsity.page_size, True,
+                                                 sparsity.include_sink, sparsity.recent_window, 0)
+            self.sel_idx = torch.empty((rows_total, self.sel_ld), dtype=torch.int32, device=dev)
+            self.sel_cnt = torch.empty((rows_total,), dtype=torch.int32, device=dev)
+            # union lists: unit (b, l, g), row m = hh*R + i -> draft row ((b*nd + table)*R + i)
+            dr = (np.arange(s.batch)[:, None, None, None] * nd
+                  + table.reshape(1, s.target_layers, s.target_kv_heads, Gt))  # [B, L, Hkv, Gt]
+            src = dr[..., None] * R + np.arange(R)  # [B, L, Hkv, Gt, R]
+            self.union_src = torch.from_numpy(src.reshape(-1, Gt * R).astype(np.int32)).to(dev)
+            self.idx_ld = s.n_kv
+            self.bitmap = torch.empty((s.target_units, s.n_kv), dtype=torch.int32, device=dev)
+            self.idx = self.cnt = self.member = None
+        # target side
+        M = Gt * R
+        self.M = M
+        self.out = torch.empty((s.target_units, M, s.head_dim), dtype=torch.bfloat16, device=dev)
+        self.lse = torch.empty((s.target_units, M), dtype=torch.float32, device=dev)
+        self.status = torch.zeros((1,), dtype=torch.int32, device=dev)
+        keys = self.idx_ld
+        self.splits = splits if splits is not None else kernels._lib.load().sts_auto_splits(s.target_units, keys)
+        self.dense_splits = kernels._lib.load().sts_auto_splits(s.target_units, s.n_kv)
+
+    # -- the four stages ----------------------------------------------------------
+    def capture(self, draft_q, draft_k, stream=None):
+        """Stages 1-2: draft log-sum-exp and probability rows (score capture)."""
+        s, R = self.shape, self.shape.rows
+        kernels.draft_lse(draft_q, draft_k, G=s.draft_group, R=R, base=s.context, n_keys=s.n_kv,
+                          out=self.draft_lse, workspace=self.ws_draft, stream=stream)
+        kernels.draft_probs(draft_q, draft_k, self.draft_lse, G=s.draft_group, R=R, base=s.context,
+                            mode=self.mode, n_keys=s.n_kv, out=self.draft_rows, stream=stream)
+
+    def build_masks(self, stream=None):
+        """Stage 3: radix top-k selection (+ union for mode R)."""
+        s, cfg = self.shape, self.cfg
+        if self.mode == "S":
+            kernels.select_topk(self.draft_rows, row_src=self.row_src, n_common=s.context,
+                                budget=int(self.budget), page_size=cfg.page_size, include_current=False,
+                                include_sink=cfg.include_sink, recent_window=cfg.recent_window,
+                                tail_len=s.rows, out=self.idx, cnt=self.cnt, status=self.status,
+                                workspace=self.ws_sel, stream=stream)
+        else:
+            kernels.select_topk(self.draft_rows, row_len=self.row_len, budget=cfg.budget,
+                                page_size=cfg.page_size, include_current=True, include_sink=cfg.include_sink,
+                                recent_window=cfg.recent_window, out=self.sel_idx, cnt=self.sel_cnt,
+                                status=self.status, workspace=self.ws_sel, stream=stream)
+            self.idx, self.member, self.cnt = kernels.row_union(
+                self.sel_idx, self.sel_cnt, self.union_src, M=self.M, n_max=s.n_kv, bitmap=self.bitmap,
+                status=self.status, stream=stream)
+
+    def attend(self, target_q, target_k, target_v, stream=None):
+        """Stage 4: gathered sparse flash-decode of the stacked rows."""
+        s = self.shape
+        causal = s.context if self.mode == "S" else -1
+        return kernels.sparse_decode(target_q, target_k, target_v, idx=self.idx, cnt=self.cnt,
+                                     member=self.member, causal_base=causal, rows_per_head=s.rows,
+                                     splits=self.splits, out=self.out, lse=self.lse, status=self.status,
+                                     workspace=self.ws_dec, stream=stream)
+
+    def attend_dense(self, target_q, target_k, target_v, out=None, lse=None, stream=None):
+        """Dense baseline on the same kernel: every cached key, causal tail."""
+        s = self.shape
+        return kernels.sparse_decode(target_q, target_k, target_v, n_dense=s.n_kv, causal_base=s.context,
+                                     rows_per_head=s.rows, splits=self.dense_splits,
+                                     out=out if out is not None else self.out,
+                                     lse=lse if lse is not None else self.lse, status=self.status,
+                                     workspace=self.ws_dec, stream=stream)
+
+    def step(self, draft_q, draft_k, target_q, target_k, target_v, stream=None):
+        self.capture(draft_q, draft_k, stream)
+        self.build_masks(stream)
+        return self.attend(target_q, target_k, target_v, stream)
+
+    # -- layouts ------------------------------------------------------------------
+    def target_views(self, q, k, v):
+        """[B, L, Hq, R, d] q and [B, L, Hkv, N, d] caches -> kernel unit views."""
+        s = self.shape
+        U = s.target_units
+        return (q.reshape(U, self.M, s.head_dim), k.reshape(U, k.shape[-2], s.head_dim),
+                v.reshape(U, v.shape[-2], s.head_dim))
+
+    def draft_views(self, q, k):
+        s = self.shape
+        U = s.draft_units
+        return q.reshape(U, s.draft_group * s.rows, s.draft_head_dim), k.reshape(U, k.shape[-2], s.draft_head_dim)
+
+
+def synthetic_inputs(shape: VerifyShape, device, dtype=torch.bfloat16, seed: int = 0, n_max=None):
+    """Seeded synthetic inputs: Q, K, V ~ N(0,1); draft q/K too.
+
+    Returns draft_q [B, Ld, Hqd, R, dd], draft_k [B, Ld, Hkvd, N, dd],
+    target_q [B, L, Hq, R, d], target_k/v [B, L, Hkv, N, d]; N = n_kv.
+    Generated in chunks on the device to bound peak memory.
+    """
+    s = shape
+    n = s.n_kv if n_max is None else n_max
+    g = torch.Generator(device=device)
+
+    def randn(shape_, seed_):
+        g.manual_seed(seed_)
+        t = torch.empty(shape_, dtype=dtype, device=device)
+        flat = t.view(-1)
+        step = 1 << 28
+        for i in range(0, flat.numel(), step):
+            m = min(step, flat.numel() - i)
+            flat[i : i + m] = torch.randn(m, generator=g, device=device, dtype=torch.float32).to(dtype)
+        return t
+
+    tq = randn((s.batch, s.target_layers, s.target_q_heads, s.rows, s.head_dim), seed + 0)
+    tk = randn((s.batch, s.target_layers, s.target_kv_heads, n, s.head_dim), seed + 1)
+    tv = randn((s.batch, s.target_layers, s.target_kv_heads, n, s.head_dim), seed + 2)
+    dq = randn((s.batch, s.draft_layers, s.draft_q_heads, s.rows, s.draft_head_dim), seed + 3)
+    dk = randn((s.batch, s.draft_layers, s.draft_kv_heads, n, s.draft_head_dim), seed + 4)
+    return dq, dk, tq, tk, tv
+
+
+# BASELINE.json configs (SURVEY §8a model shapes)
+CONFIGS = {
+    "c1": dict(batch=1, context=4096, gamma=4, target_layers=4, target_q_heads=8, target_kv_heads=8, head_dim=64,
+               draft_layers=2, draft_q_heads=4, draft_kv_heads=4, draft_head_dim=64),
+    "c2": dict(batch=1, context=32768, gamma=4, target_layers=32, target_q_heads=32, target_kv_heads=8,
+               head_dim=128, draft_layers=16, draft_q_heads=32, draft_kv_heads=8, draft_head_dim=64),
+    "c3": dict(batch=8, context=131072, gamma=4, target_layers=28, target_q_heads=28, target_kv_heads=4,
+               head_dim=128, draft_layers=24, draft_q_heads=14, draft_kv_heads=2, draft_head_dim=64),
+    "c4": dict(batch=1, context=1048576, gamma=4, target_layers=32, target_q_heads=32, target_kv_heads=8,
+               head_dim=128, draft_layers=16, draft_q_heads=32, draft_kv_heads=8, draft_head_dim=64),
+    "c5": dict(batch=4, context=262144, gamma=4, target_layers=80, target_q_heads=64, target_kv_heads=8,
+               head_dim=128, draft_layers=16, draft_q_heads=32, draft_kv_heads=8, draft_head_dim=64),
+}
+
+
+def config_shape(name: str, **overrides) -> VerifyShape:
+    d = dict(CONFIGS[name])
+    d.update(overrides)
+    return VerifyShape(**d)
+
+
+def algorithmic_bytes(shape: VerifyShape, keys_per_unit: float, e: int = 2, dense: bool = False) -> float:
+    """bytes = U*|S|*d*2*e (K,V) + U*|S|*4 (idx) + 2*B*L*Hq*R*d*e (Q,O)
+    + B*L*Hq*R*4 (LSE)."""
+    s = shape
+    U = s.target_units
+    kv = U * keys_per_unit * s.head_dim * 2 * e
+    idx = 0 if dense else U * keys_per_unit * 4
+    rows = s.batch * s.target_layers * s.target_q_heads * s.rows
+    return kv + idx + 2 * rows * s.head_dim * e + rows * 4
