@@ -24,7 +24,6 @@ constexpr int SEL_THREADS = 1024;
 constexpr int SEL_WARPS = SEL_THREADS / 32;
 constexpr int DIGIT_BITS = 12;
 constexpr int NBINS = 1 << DIGIT_BITS;
-constexpr int SEL_SMEM_MAX_LEN = 49152;
 
 struct SelectParams {
   const float* scores;
@@ -94,26 +93,6 @@ __device__ __forceinline__ double page_sum(const SelectParams& p, const int32_t*
   double x0 = (double)row_value(p, srcs, start);
   if (len == 1) return x0;
   return __dadd_rn(x0, pairwise_sum(p, srcs, start + 1, len - 1));
-}
-
-// Block-wide exclusive scan of a 0/1 flag in thread order; returns the
-// exclusive prefix and writes the block total.  Contains two barriers.
-__device__ __forceinline__ int block_scan_flag(bool f, int* warp_tot, int& total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t bal = __ballot_sync(0xffffffffu, f);
-  int in_warp = __popc(bal & ((1u << lane) - 1u));
-  if (lane == 0) warp_tot[warp] = __popc(bal);
-  __syncthreads();
-  int before = 0, tot = 0;
-#pragma unroll 8
-  for (int w = 0; w < SEL_WARPS; ++w) {
-    int t = warp_tot[w];
-    before += (w < warp) ? t : 0;
-    tot += t;
-  }
-  __syncthreads();
-  total = tot;
-  return before + in_warp;
 }
 
 // Block-wide exclusive scan of an int in thread order.
@@ -214,6 +193,120 @@ __device__ __forceinline__ void write_idx(const SelectParams& p, int32_t* out, i
   else set_status(p.status, STS_DEV_IDX_CAPACITY);
 }
 
+// Form the logical row's fp32 values (sum of sources, in source order) for
+// j in [0, n) and hand each to `sink(j, value)`; 4 elements per thread per
+// step with 128-bit loads when rows are 16-byte aligned, two steps in flight.
+template <typename Sink>
+__device__ __forceinline__ void for_row_values(const SelectParams& p, const int32_t* srcs, int n, Sink sink) {
+  const bool vec = (p.ld % 4) == 0 && (reinterpret_cast<uintptr_t>(p.scores) % 16) == 0;
+  int j0 = 0;
+  if (vec) {
+    const int n4 = n / 4;
+    for (int v = threadIdx.x; v < n4; v += 2 * SEL_THREADS) {
+      const int v2 = v + SEL_THREADS;
+      const bool has2 = v2 < n4;
+      float4 a = *reinterpret_cast<const float4*>(p.scores + (int64_t)srcs[0] * p.ld + 4 * v);
+      float4 b = has2 ? *reinterpret_cast<const float4*>(p.scores + (int64_t)srcs[0] * p.ld + 4 * v2)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s = 1; s < p.nsrc; ++s) {
+        const float* base = p.scores + (int64_t)srcs[s] * p.ld;
+        const float4 x = *reinterpret_cast<const float4*>(base + 4 * v);
+        a.x = __fadd_rn(a.x, x.x); a.y = __fadd_rn(a.y, x.y); a.z = __fadd_rn(a.z, x.z); a.w = __fadd_rn(a.w, x.w);
+        if (has2) {
+          const float4 y = *reinterpret_cast<const float4*>(base + 4 * v2);
+          b.x = __fadd_rn(b.x, y.x); b.y = __fadd_rn(b.y, y.y); b.z = __fadd_rn(b.z, y.z); b.w = __fadd_rn(b.w, y.w);
+        }
+      }
+      sink(4 * v, a.x); sink(4 * v + 1, a.y); sink(4 * v + 2, a.z); sink(4 * v + 3, a.w);
+      if (has2) { sink(4 * v2, b.x); sink(4 * v2 + 1, b.y); sink(4 * v2 + 2, b.z); sink(4 * v2 + 3, b.w); }
+    }
+    j0 = 4 * n4;
+  }
+  for (int j = j0 + threadIdx.x; j < n; j += SEL_THREADS) sink(j, row_value(p, srcs, j));
+}
+
+// numpy pairwise_sum over values already staged in `vals` (see pairwise_sum)
+__device__ double pairwise_vals(const float* vals, int start, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = __dadd_rn(r, (double)vals[start + i]);
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = (double)vals[start + j];
+    int i = 8;
+    for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], (double)vals[start + i + j]);
+    }
+    double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                           __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+    for (; i < n; ++i) res = __dadd_rn(res, (double)vals[start + i]);
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return __dadd_rn(pairwise_vals(vals, start, n2), pairwise_vals(vals, start + n2, n - n2));
+}
+
+// Emit pass over `len` candidates in index order, 4 per thread per chunk.
+// sel(j, tie_rank_before_j_is_lt_need) decides membership; writes ascending.
+template <typename KeyAt, typename Extra>
+__device__ __forceinline__ int emit_sorted(const SelectParams& p, SelShared& sh, int32_t* out, int len,
+                                           KeyAt key_at, uint64_t T, int need, Extra extra, int out_base,
+                                           bool write_bits, uint32_t* bits) {
+  int run_sel = 0, run_tie = 0;
+  for (int base = 0; base < len; base += 4 * SEL_THREADS) {
+    const int j0 = base + 4 * threadIdx.x;
+    uint64_t k4[4];
+    int nt = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = j0 + q;
+      k4[q] = j < len ? key_at(j) : 0ull;
+      nt += (j < len && k4[q] == T) ? 1 : 0;
+    }
+    int tie_tot;
+    int tie_ex = block_scan_int(nt, sh.warp_tot, tie_tot);
+    bool f[4];
+    int ns = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = j0 + q;
+      bool sel = false;
+      if (j < len) {
+        const bool tie = k4[q] == T;
+        sel = k4[q] > T || (tie && run_tie + tie_ex < need) || extra(j);
+        tie_ex += tie ? 1 : 0;
+      }
+      f[q] = sel;
+      ns += sel ? 1 : 0;
+    }
+    if (write_bits) {
+      // page mode: record selected pages as a bitmap (4 bits per thread)
+      const uint32_t nib = (f[0] ? 1u : 0u) | (f[1] ? 2u : 0u) | (f[2] ? 4u : 0u) | (f[3] ? 8u : 0u);
+      const int lane = threadIdx.x & 31;
+      uint32_t w = nib << ((lane & 7) * 4);
+      w |= __shfl_xor_sync(0xffffffffu, w, 1);
+      w |= __shfl_xor_sync(0xffffffffu, w, 2);
+      w |= __shfl_xor_sync(0xffffffffu, w, 4);
+      if ((lane & 7) == 0 && j0 < len) bits[j0 >> 5] = w;
+      run_tie += tie_tot;
+      continue;
+    }
+    int sel_tot;
+    int sel_ex = block_scan_int(ns, sh.warp_tot, sel_tot);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (f[q]) write_idx(p, out, out_base + run_sel + sel_ex++, j0 + q);
+    run_sel += sel_tot;
+    run_tie += tie_tot;
+  }
+  return run_sel;
+}
+
 __global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(SelectParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   SelShared& sh = *reinterpret_cast<SelShared*>(smem_raw);
@@ -239,6 +332,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(SelectParams p) 
     } else {
       b = (int)p.budget;
     }
+    auto extra = [&](int j) { return is_extra(p, j, n); };
 
     int count = 0;
     if (n <= 0) {
@@ -249,77 +343,43 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(SelectParams p) 
       count = n;
     } else if (p.page_size == 1) {
       uint32_t* keys = reinterpret_cast<uint32_t*>(buf);
-      for (int j = threadIdx.x; j < n; j += SEL_THREADS) keys[j] = f32_key(row_value(p, srcs, j));
+      for_row_values(p, srcs, n, [&](int j, float v) { keys[j] = f32_key(v); });
       __syncthreads();
       uint32_t T;
       int need;
       radix_select<uint32_t>(keys, n, b, sh, T, need);
-      int run_sel = 0, run_tie = 0;
-      for (int base = 0; base < n; base += SEL_THREADS) {
-        const int j = base + threadIdx.x;
-        const bool valid = j < n;
-        const uint32_t key = valid ? keys[j] : 0u;
-        const bool tie = valid && key == T;
-        int tie_tot;
-        const int tie_ex = block_scan_flag(tie, sh.warp_tot, tie_tot);
-        const bool sel = valid && (key > T || (tie && run_tie + tie_ex < need) || is_extra(p, j, n));
-        int sel_tot;
-        const int sel_ex = block_scan_flag(sel, sh.warp_tot, sel_tot);
-        if (sel) write_idx(p, out, run_sel + sel_ex, j);
-        run_sel += sel_tot;
-        run_tie += tie_tot;
-      }
-      count = run_sel;
+      count = emit_sorted(p, sh, out, n, [&](int j) { return (uint64_t)keys[j]; }, (uint64_t)T, need, extra, 0,
+                          false, nullptr);
     } else {
       const int ps = p.page_size;
       const int P = (n + ps - 1) / ps;
       const int kp = (b + ps - 1) / ps;
-      uint64_t* pkeys = reinterpret_cast<uint64_t*>(buf);
-      uint32_t* pbits = reinterpret_cast<uint32_t*>(buf + (((int64_t)P * 8 + 15) & ~int64_t(15)));
-      for (int w = threadIdx.x; w < (P + 31) / 32; w += SEL_THREADS) pbits[w] = 0u;
+      float* vals = reinterpret_cast<float*>(buf);
+      uint64_t* pkeys = reinterpret_cast<uint64_t*>(buf + (((int64_t)n * 4 + 15) & ~int64_t(15)));
+      uint32_t* pbits = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(pkeys) + (((int64_t)P * 8 + 15) & ~int64_t(15)));
       if (kp >= P) {
-        __syncthreads();
         for (int w = threadIdx.x; w < (P + 31) / 32; w += SEL_THREADS) pbits[w] = 0xffffffffu;
       } else {
+        for_row_values(p, srcs, n, [&](int j, float v) { vals[j] = v; });
+        __syncthreads();
         for (int pg = threadIdx.x; pg < P; pg += SEL_THREADS) {
           const int start = pg * ps;
           const int len = min(ps, n - start);
-          pkeys[pg] = f64_key(page_sum(p, srcs, start, len));
+          // np.add.reduceat segment: x[start] + pairwise(x[start+1 : start+len])
+          const double x0 = (double)vals[start];
+          pkeys[pg] = f64_key(len == 1 ? x0 : __dadd_rn(x0, pairwise_vals(vals, start + 1, len - 1)));
         }
         __syncthreads();
         uint64_t T;
         int need;
         radix_select<uint64_t>(pkeys, P, kp, sh, T, need);
-        int run_tie = 0;
-        for (int base = 0; base < P; base += SEL_THREADS) {
-          const int pg = base + threadIdx.x;
-          const bool valid = pg < P;
-          const uint64_t key = valid ? pkeys[pg] : 0ull;
-          const bool tie = valid && key == T;
-          int tie_tot;
-          const int tie_ex = block_scan_flag(tie, sh.warp_tot, tie_tot);
-          const bool sel = valid && (key > T || (tie && run_tie + tie_ex < need));
-          uint32_t bal = __ballot_sync(0xffffffffu, sel);
-          if ((threadIdx.x & 31) == 0 && base + (int)threadIdx.x < P) pbits[(base + threadIdx.x) >> 5] = bal;
-          run_tie += tie_tot;
-        }
+        emit_sorted(p, sh, out, P, [&](int j) { return pkeys[j]; }, T, need, [](int) { return false; }, 0, true,
+                    pbits);
       }
       __syncthreads();
-      int run_sel = 0;
-      for (int base = 0; base < n; base += SEL_THREADS) {
-        const int j = base + threadIdx.x;
-        const bool valid = j < n;
-        bool sel = false;
-        if (valid) {
-          const int pg = j / ps;
-          sel = ((pbits[pg >> 5] >> (pg & 31)) & 1u) || is_extra(p, j, n);
-        }
-        int sel_tot;
-        const int sel_ex = block_scan_flag(sel, sh.warp_tot, sel_tot);
-        if (sel) write_idx(p, out, run_sel + sel_ex, j);
-        run_sel += sel_tot;
-      }
-      count = run_sel;
+      count = emit_sorted(p, sh, out, n,
+                          [&](int j) { return (uint64_t)((pbits[(j / ps) >> 5] >> ((j / ps) & 31)) & 1u); },
+                          0ull, 0, extra, 0, false, nullptr);  // selected iff page bit (key) > 0
     }
     // in-block tail (mode S: the verify block's own positions)
     for (int t = threadIdx.x; t < p.tail_len; t += SEL_THREADS) write_idx(p, out, count + t, max(n, 0) + t);
@@ -344,12 +404,14 @@ __global__ void page_aggregate_kernel(SelectParams p, double* out, int64_t out_l
 }
 
 int64_t key_buf_bytes(int32_t max_len, int32_t page_size) {
-  int64_t tok = (int64_t)max_len * 4;
-  int64_t pages = page_size > 1 ? ((int64_t)max_len + page_size - 1) / page_size : 0;
-  int64_t pg = ((pages * 8 + 15) & ~int64_t(15)) + ((pages + 31) / 32) * 4 + 16;
-  int64_t b = tok > pg ? tok : pg;
+  int64_t tok = ((int64_t)max_len * 4 + 15) & ~int64_t(15);
+  if (page_size == 1) return (tok + 127) & ~int64_t(127);
+  int64_t pages = ((int64_t)max_len + page_size - 1) / page_size;
+  int64_t b = tok + ((pages * 8 + 15) & ~int64_t(15)) + ((pages + 31) / 32 + 32) * 4;
   return (b + 127) & ~int64_t(127);
 }
+
+constexpr int64_t SEL_SMEM_BUDGET = 227 * 1024 - (int64_t)sizeof(SelShared) - 256;
 
 }  // namespace
 }  // namespace sts
@@ -357,7 +419,7 @@ int64_t key_buf_bytes(int32_t max_len, int32_t page_size) {
 using namespace sts;
 
 extern "C" size_t sts_select_workspace_bytes(int64_t rows, int32_t max_len, int32_t page_size) {
-  if (max_len <= SEL_SMEM_MAX_LEN) return 0;
+  if (key_buf_bytes(max_len, page_size) <= SEL_SMEM_BUDGET) return 0;
   int64_t slots = rows < 4 * num_sms() ? rows : 4 * num_sms();
   return (size_t)(slots * key_buf_bytes(max_len, page_size));
 }
@@ -410,7 +472,7 @@ extern "C" int sts_select_topk(const float* scores_dev, int64_t ld, const int32_
   const size_t sh_bytes = (sizeof(SelShared) + 15) & ~size_t(15);
   size_t smem = sh_bytes;
   int grid;
-  if (max_len <= SEL_SMEM_MAX_LEN) {
+  if (p.buf_bytes <= SEL_SMEM_BUDGET) {
     p.gbuf = nullptr;
     p.gbuf_stride = 0;
     smem += (size_t)p.buf_bytes;

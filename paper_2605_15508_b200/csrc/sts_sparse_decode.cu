@@ -52,26 +52,32 @@ struct DecodeParams {
   float* probs_out;
   int64_t out_ld;
   int probs_mode;       // 0: reduced over rows (mode S), 1: per row (mode R)
+  int idx_cap;          // keys of the CTA slice staged in shared memory
 };
 
 __device__ __forceinline__ int unit_count(const DecodeParams& p, int64_t u) {
   return p.idx ? p.cnt[u] : p.n_dense;
 }
 
-template <int D, int NT, int STAGES, int WARPS, bool K_ONLY>
+// Shared-memory plan of one CTA.  A warp's stage holds KT = 16*SUB keys
+// (K, plus V in MODE_DECODE).  The CTA's slice of the index list (and of the
+// membership bits) is preloaded once into shared memory so a gather never
+// waits on a dependent index load.
+template <int D, int NT, int STAGES, int WARPS, int MODE, int SUB>
 struct Bf16Layout {
+  static constexpr bool K_ONLY = MODE != 0;
+  static constexpr int KT = KEY_TILE * SUB;
   static constexpr int MP = 8 * NT;                        // padded rows
   static constexpr int ROW_BYTES = D * 2;
   static constexpr int Q_BYTES = MP * ROW_BYTES;
-  static constexpr int TILE_BYTES = KEY_TILE * ROW_BYTES;  // one K or V tile
-  static constexpr int STAGE_BYTES = (K_ONLY ? 1 : 2) * TILE_BYTES;
-  static constexpr int META_BYTES = KEY_TILE * 8;          // pos + member per key
-  static constexpr int PROB_BYTES = KEY_TILE * MP * 4;      // MODE_PROBS scratch
-  static constexpr int WARP_BYTES = STAGES * (STAGE_BYTES + META_BYTES) + PROB_BYTES;
-  static constexpr int MERGE_BYTES = WARPS * MP * D * 4 + WARPS * MP * 2 * 4;
+  static constexpr int SUB_BYTES = KEY_TILE * ROW_BYTES;   // one 16-key K (or V) sub-tile
+  static constexpr int STAGE_BYTES = (K_ONLY ? 1 : 2) * SUB * SUB_BYTES;
+  static constexpr int PROB_BYTES = MODE == 2 ? KEY_TILE * MP * 4 : 0;  // MODE_PROBS scratch
+  static constexpr int WARP_BYTES = STAGES * STAGE_BYTES + PROB_BYTES;
+  static constexpr int MERGE_BYTES = WARPS * MP * (K_ONLY ? 0 : D) * 4 + WARPS * MP * 2 * 4;
   static constexpr int PIPE_BYTES = WARPS * WARP_BYTES;
   static constexpr int BODY = PIPE_BYTES > MERGE_BYTES ? PIPE_BYTES : MERGE_BYTES;
-  static constexpr int SMEM = Q_BYTES + BODY;
+  static constexpr int FIXED = Q_BYTES + BODY;             // + idx slice (runtime)
 };
 
 __device__ __forceinline__ uint32_t swz(int row, int chunk) { return (uint32_t)((chunk ^ (row & 7)) << 4); }
@@ -82,10 +88,11 @@ __device__ __forceinline__ uint32_t swz(int row, int chunk) { return (uint32_t)(
 //              reduced over the speculative rows of each head (sts_draft_probs)
 constexpr int MODE_DECODE = 0, MODE_LSE = 1, MODE_PROBS = 2;
 
-template <int D, int NT, int STAGES, int WARPS, int MODE>
+template <int D, int NT, int STAGES, int WARPS, int MODE, int SUB>
 __global__ void __launch_bounds__(WARPS * 32, 2) sparse_decode_bf16_kernel(DecodeParams p) {
-  using L = Bf16Layout<D, NT, STAGES, WARPS, MODE != MODE_DECODE>;
+  using L = Bf16Layout<D, NT, STAGES, WARPS, MODE, SUB>;
   constexpr int CH = D / 8;  // 16-byte chunks per row
+  constexpr int KT = L::KT;
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -95,11 +102,13 @@ __global__ void __launch_bounds__(WARPS * 32, 2) sparse_decode_bf16_kernel(Decod
 
   // ---- key range of this CTA ----
   const int cnt = unit_count(p, u);
-  const int ntiles_all = (cnt + KEY_TILE - 1) / KEY_TILE;
+  const int ntiles_all = (cnt + KT - 1) / KT;
   const int t0 = (int)((int64_t)split * ntiles_all / p.splits);
   const int t1 = (int)((int64_t)(split + 1) * ntiles_all / p.splits);
+  const int key0 = t0 * KT;
+  const int key1 = min(t1 * KT, cnt);
 
-  // ---- Q -> smem (zero-padded rows) ----
+  // ---- Q -> smem (zero-padded rows); idx / member slice -> smem ----
   const __nv_bfloat16* qg = static_cast<const __nv_bfloat16*>(p.q) + u * (int64_t)M * D;
   for (int c = threadIdx.x; c < L::MP * CH; c += WARPS * 32) {
     const int r = c / CH, ch = c % CH;
@@ -107,18 +116,36 @@ __global__ void __launch_bounds__(WARPS * 32, 2) sparse_decode_bf16_kernel(Decod
     if (r < M) val = *reinterpret_cast<const uint4*>(qg + (int64_t)r * D + ch * 8);
     *reinterpret_cast<uint4*>(smem + r * L::ROW_BYTES + swz(r, ch)) = val;
   }
+  int* sidx = reinterpret_cast<int*>(smem + L::FIXED);
+  uint32_t* smem_bits = reinterpret_cast<uint32_t*>(sidx + p.idx_cap);
+  const int32_t* idxg = p.idx ? p.idx + u * p.idx_ld : nullptr;
+  const uint32_t* memg = p.member ? p.member + u * p.idx_ld : nullptr;
+  const bool idx_in_smem = idxg != nullptr && (key1 - key0) <= p.idx_cap;
+  if (idx_in_smem) {
+    for (int j = threadIdx.x; j < key1 - key0; j += WARPS * 32) {
+      sidx[j] = idxg[key0 + j];
+      if (memg) smem_bits[j] = memg[key0 + j];
+    }
+  }
   __syncthreads();
   const uint32_t q_base = smem_u32(smem);
   uint8_t* wbase = smem + L::Q_BYTES + warp * L::WARP_BYTES;
   const uint32_t wbase_u = smem_u32(wbase);
-  int* meta_pos = reinterpret_cast<int*>(wbase + STAGES * L::STAGE_BYTES);
-  uint32_t* meta_mem = reinterpret_cast<uint32_t*>(meta_pos + STAGES * KEY_TILE);
-  float* pscr = reinterpret_cast<float*>(meta_mem + STAGES * KEY_TILE);  // [16][MP]
+  float* pscr = reinterpret_cast<float*>(wbase + STAGES * L::STAGE_BYTES);  // [16][MP]
 
   const __nv_bfloat16* kg = static_cast<const __nv_bfloat16*>(p.k) + u * p.kv_stride;
   const __nv_bfloat16* vg = MODE == MODE_DECODE ? static_cast<const __nv_bfloat16*>(p.v) + u * p.kv_stride : nullptr;
-  const int32_t* idxg = p.idx ? p.idx + u * p.idx_ld : nullptr;
-  const uint32_t* memg = p.member ? p.member + u * p.idx_ld : nullptr;
+
+  // position of key j of the list (-1 if past the CTA range)
+  auto key_pos = [&](int j) -> int {
+    if (j >= key1) return -1;
+    if (!idxg) return j;
+    return idx_in_smem ? sidx[j - key0] : idxg[j];
+  };
+  auto key_mem = [&](int j) -> uint32_t {
+    if (!memg || j >= key1) return 0xffffffffu;
+    return idx_in_smem ? smem_bits[j - key0] : memg[j];
+  };
 
   // number of tiles this warp owns: t = t0 + warp + WARPS*i
   const int my_n = (t1 - t0 - warp + WARPS - 1) / WARPS > 0 ? (t1 - t0 - warp + WARPS - 1) / WARPS : 0;
@@ -126,44 +153,36 @@ __global__ void __launch_bounds__(WARPS * 32, 2) sparse_decode_bf16_kernel(Decod
   auto issue = [&](int i) {
     if (i < my_n) {
       const int stage = i % STAGES;
-      const int kbase = (t0 + warp + WARPS * i) * KEY_TILE;
-      int pos = -1;
-      uint32_t mem = 0xffffffffu;
-      if (lane < KEY_TILE) {
-        const int j = kbase + lane;
-        if (j < cnt) {
-          pos = idxg ? idxg[j] : j;
-          if (memg) mem = memg[j];
-        }
-        meta_pos[stage * KEY_TILE + lane] = pos;
-        meta_mem[stage * KEY_TILE + lane] = mem;
-      }
-      const uint32_t sk = wbase_u + stage * L::STAGE_BYTES;
-      const uint32_t sv = sk + L::TILE_BYTES;
+      const int kbase = (t0 + warp + WARPS * i) * KT;
+      const uint32_t st_k = wbase_u + stage * L::STAGE_BYTES;
       constexpr int ROWS_PER_IT = 32 / CH;
 #pragma unroll
-      for (int it = 0; it < KEY_TILE / ROWS_PER_IT; ++it) {
-        const int r = it * ROWS_PER_IT + lane / CH;
+      for (int it = 0; it < KT / ROWS_PER_IT; ++it) {
+        const int r = it * ROWS_PER_IT + lane / CH;  // row within the stage (0..KT)
         const int ch = lane % CH;
-        const int pr = __shfl_sync(0xffffffffu, pos, r);
+        const int pr = key_pos(kbase + r);
         const bool ok = pr >= 0;
         const int64_t off = (int64_t)(ok ? pr : 0) * D + ch * 8;
-        cp_async_16_zfill(sk + r * L::ROW_BYTES + swz(r, ch), kg + off, ok);
-        if constexpr (MODE == MODE_DECODE) cp_async_16_zfill(sv + r * L::ROW_BYTES + swz(r, ch), vg + off, ok);
+        const uint32_t sk = st_k + (r >> 4) * L::SUB_BYTES;
+        const int rr = r & 15;
+        cp_async_16_zfill(sk + rr * L::ROW_BYTES + swz(rr, ch), kg + off, ok);
+        if constexpr (MODE == MODE_DECODE)
+          cp_async_16_zfill(sk + SUB * L::SUB_BYTES + rr * L::ROW_BYTES + swz(rr, ch), vg + off, ok);
       }
     }
     cp_async_commit();
   };
 
-  float o[D / 16][NT][4];
+  float o[MODE == MODE_DECODE ? D / 16 : 1][NT][4];
 #pragma unroll
-  for (int a = 0; a < D / 16; ++a)
+  for (int a = 0; a < (MODE == MODE_DECODE ? D / 16 : 1); ++a)
 #pragma unroll
     for (int b = 0; b < NT; ++b)
 #pragma unroll
       for (int c = 0; c < 4; ++c) o[a][b][c] = 0.f;
   float m_run[NT][2], l_run[NT][2];
   int rmod[NT][2];
+  float lse2[NT][2];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -172,19 +191,12 @@ __global__ void __launch_bounds__(WARPS * 32, 2) sparse_decode_bf16_kernel(Decod
       l_run[nt][c] = 0.f;
       const int r = nt * 8 + 2 * (lane & 3) + c;
       rmod[nt][c] = r % p.rows_per_head;
+      lse2[nt][c] = (MODE == MODE_PROBS && r < M) ? p.lse_in[u * M + r] * LOG2E : 0.f;
     }
   const float sl2 = p.scale * LOG2E;
   const int causal_shift = p.pos_offset - p.causal_base;  // pos_rel = pos + shift
   const bool causal = p.causal_base >= 0;
-
-  float lse2[NT][2];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      const int r = nt * 8 + 2 * (lane & 3) + c;
-      lse2[nt][c] = (MODE == MODE_PROBS && r < M) ? p.lse_in[u * M + r] * LOG2E : 0.f;
-    }
+  const int mi = lane >> 3, ri = lane & 7;
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) issue(s);
@@ -194,148 +206,150 @@ __global__ void __launch_bounds__(WARPS * 32, 2) sparse_decode_bf16_kernel(Decod
     cp_async_wait<STAGES - 1>();
     __syncwarp();
     const int stage = i % STAGES;
-    const uint32_t sk = wbase_u + stage * L::STAGE_BYTES;
-    const uint32_t sv = sk + L::TILE_BYTES;
+    const int kbase = (t0 + warp + WARPS * i) * KT;
 
-    // ---- S^T = K . Q^T  (16 keys x 8NT rows) ----
-    float s[NT][4];
+#pragma unroll 1
+    for (int sub = 0; sub < SUB; ++sub) {
+      const uint32_t sk = wbase_u + stage * L::STAGE_BYTES + sub * L::SUB_BYTES;
+      const uint32_t sv = sk + SUB * L::SUB_BYTES;
+      const int kb = kbase + sub * KEY_TILE;
+      if (kb >= key1) break;
+
+      // ---- S^T = K . Q^T  (16 keys x 8NT rows) ----
+      float s[NT][4];
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) s[nt][c] = 0.f;
-    const int mi = lane >> 3, ri = lane & 7;
+        for (int c = 0; c < 4; ++c) s[nt][c] = 0.f;
 #pragma unroll
-    for (int kk = 0; kk < D / 16; kk += 2) {
-      uint32_t a0[4], a1[4];
-      {
+      for (int kk = 0; kk < D / 16; kk += 2) {
+        uint32_t a0[4], a1[4];
         const int key = (mi & 1) * 8 + ri;
         ldmatrix_x4(a0[0], a0[1], a0[2], a0[3], sk + key * L::ROW_BYTES + swz(key, 2 * kk + (mi >> 1)));
         ldmatrix_x4(a1[0], a1[1], a1[2], a1[3], sk + key * L::ROW_BYTES + swz(key, 2 * kk + 2 + (mi >> 1)));
-      }
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int row = nt * 8 + ri;
-        uint32_t b[4];
-        ldmatrix_x4(b[0], b[1], b[2], b[3], q_base + row * L::ROW_BYTES + swz(row, 2 * kk + mi));
-        const uint32_t b0[2] = {b[0], b[1]};
-        const uint32_t b1[2] = {b[2], b[3]};
-        mma_bf16_16816(s[nt], a0, b0);
-        mma_bf16_16816(s[nt], a1, b1);
-      }
-    }
-
-    // ---- masking ----
-    const int kA = lane >> 2, kB = kA + 8;
-    const int posA = meta_pos[stage * KEY_TILE + kA];
-    const int posB = meta_pos[stage * KEY_TILE + kB];
-    const uint32_t memA = meta_mem[stage * KEY_TILE + kA];
-    const uint32_t memB = meta_mem[stage * KEY_TILE + kB];
-    bool okA[NT][2], okB[NT][2];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int r = nt * 8 + 2 * (lane & 3) + c;
-        bool a_ = posA >= 0, b_ = posB >= 0;
-        if (causal) {
-          a_ = a_ && (posA + causal_shift <= rmod[nt][c]);
-          b_ = b_ && (posB + causal_shift <= rmod[nt][c]);
+        for (int nt = 0; nt < NT; ++nt) {
+          const int row = nt * 8 + ri;
+          uint32_t b[4];
+          ldmatrix_x4(b[0], b[1], b[2], b[3], q_base + row * L::ROW_BYTES + swz(row, 2 * kk + mi));
+          const uint32_t b0[2] = {b[0], b[1]};
+          const uint32_t b1[2] = {b[2], b[3]};
+          mma_bf16_16816(s[nt], a0, b0);
+          mma_bf16_16816(s[nt], a1, b1);
         }
-        okA[nt][c] = a_ && ((memA >> (r & 31)) & 1u);
-        okB[nt][c] = b_ && ((memB >> (r & 31)) & 1u);
       }
 
-    if constexpr (MODE == MODE_PROBS) {
-      // p = exp2(s*sl2 - lse2[row]) -> scratch [key][row]
+      // ---- masking ----
+      const int kA = lane >> 2, kB = kA + 8;
+      const int posA = key_pos(kb + kA);
+      const int posB = key_pos(kb + kB);
+      const uint32_t memA = key_mem(kb + kA);
+      const uint32_t memB = key_mem(kb + kB);
+      bool okA[NT][2], okB[NT][2];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
           const int r = nt * 8 + 2 * (lane & 3) + c;
-          const float l2 = r < M ? lse2[nt][c] : 0.f;
-          pscr[kA * L::MP + r] = okA[nt][c] ? fast_exp2(s[nt][c] * sl2 - l2) : 0.f;
-          pscr[kB * L::MP + r] = okB[nt][c] ? fast_exp2(s[nt][2 + c] * sl2 - l2) : 0.f;
-        }
-      __syncwarp();
-      const int R = p.rows_per_head;
-      const int G = M / R;
-      const int kbase = (t0 + warp + WARPS * i) * KEY_TILE;
-      if (p.probs_mode == 0) {
-        // mode S: D[u][hh][j] = sum_i p_{hh,i}[j] (i ascending), committed keys only
-        for (int e = lane; e < KEY_TILE * G; e += 32) {
-          const int key = e % KEY_TILE, hh = e / KEY_TILE;
-          const int pos = meta_pos[stage * KEY_TILE + key];
-          if (pos >= 0 && pos + p.pos_offset < p.causal_base) {
-            float acc = pscr[key * L::MP + hh * R];
-            for (int ii = 1; ii < R; ++ii) acc = __fadd_rn(acc, pscr[key * L::MP + hh * R + ii]);
-            p.probs_out[(u * G + hh) * p.out_ld + kbase + key] = acc;
+          bool a_ = posA >= 0, b_ = posB >= 0;
+          if (causal) {
+            a_ = a_ && (posA + causal_shift <= rmod[nt][c]);
+            b_ = b_ && (posB + causal_shift <= rmod[nt][c]);
           }
+          okA[nt][c] = a_ && ((memA >> (r & 31)) & 1u);
+          okB[nt][c] = b_ && ((memB >> (r & 31)) & 1u);
         }
-      } else {
-        // mode R: one probability row per (head, speculative row)
-        for (int e = lane; e < KEY_TILE * M; e += 32) {
-          const int key = e % KEY_TILE, r = e / KEY_TILE;
-          const int pos = meta_pos[stage * KEY_TILE + key];
-          if (pos >= 0 && pos + p.pos_offset <= p.causal_base + r % R)
-            p.probs_out[(u * M + r) * p.out_ld + kbase + key] = pscr[key * L::MP + r];
-        }
-      }
-      __syncwarp();
-    } else {
-      // ---- online softmax (log2 domain) ----
-      uint32_t pb[NT][2];
+
+      if constexpr (MODE == MODE_PROBS) {
+        // p = exp2(s*sl2 - lse2[row]) -> scratch [key][row]
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        float pv[4];
+        for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const float vA = okA[nt][c] ? s[nt][c] * sl2 : -INFINITY;
-          const float vB = okB[nt][c] ? s[nt][2 + c] * sl2 : -INFINITY;
-          float tmax = fmaxf(vA, vB);
-          tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
-          tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
-          tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
-          const float m_old = m_run[nt][c];
-          const float m_new = fmaxf(m_old, tmax);
-          float alpha, pA, pB;
-          if (m_new == -INFINITY) {
-            alpha = 1.f;
-            pA = 0.f;
-            pB = 0.f;
-          } else {
-            alpha = fast_exp2(m_old - m_new);
-            pA = fast_exp2(vA - m_new);
-            pB = fast_exp2(vB - m_new);
+          for (int c = 0; c < 2; ++c) {
+            const int r = nt * 8 + 2 * (lane & 3) + c;
+            pscr[kA * L::MP + r] = okA[nt][c] ? fast_exp2(s[nt][c] * sl2 - lse2[nt][c]) : 0.f;
+            pscr[kB * L::MP + r] = okB[nt][c] ? fast_exp2(s[nt][2 + c] * sl2 - lse2[nt][c]) : 0.f;
           }
-          m_run[nt][c] = m_new;
-          l_run[nt][c] = l_run[nt][c] * alpha + pA + pB;
-          if constexpr (MODE == MODE_DECODE) {
-#pragma unroll
-            for (int mt = 0; mt < D / 16; ++mt) {
-              o[mt][nt][c] *= alpha;
-              o[mt][nt][2 + c] *= alpha;
+        __syncwarp();
+        const int R = p.rows_per_head;
+        const int G = M / R;
+        if (p.probs_mode == 0) {
+          // mode S: D[u][hh][j] = sum_i p_{hh,i}[j] (i ascending), committed keys only
+          for (int e = lane; e < KEY_TILE * G; e += 32) {
+            const int key = e % KEY_TILE, hh = e / KEY_TILE;
+            const int pos = key_pos(kb + key);
+            if (pos >= 0 && pos + p.pos_offset < p.causal_base) {
+              float acc = pscr[key * L::MP + hh * R];
+              for (int ii = 1; ii < R; ++ii) acc = __fadd_rn(acc, pscr[key * L::MP + hh * R + ii]);
+              p.probs_out[(u * G + hh) * p.out_ld + kb + key] = acc;
             }
           }
-          pv[c] = pA;
-          pv[2 + c] = pB;
+        } else {
+          // mode R: one probability row per (head, speculative row)
+          for (int e = lane; e < KEY_TILE * M; e += 32) {
+            const int key = e % KEY_TILE, r = e / KEY_TILE;
+            const int pos = key_pos(kb + key);
+            if (pos >= 0 && pos + p.pos_offset <= p.causal_base + r % R)
+              p.probs_out[(u * M + r) * p.out_ld + kb + key] = pscr[key * L::MP + r];
+          }
         }
-        if constexpr (MODE == MODE_DECODE) {
-          pb[nt][0] = movmatrix_trans(pack_bf16(pv[0], pv[1]));
-          pb[nt][1] = movmatrix_trans(pack_bf16(pv[2], pv[3]));
+        __syncwarp();
+      } else {
+        // ---- online softmax (log2 domain) ----
+        uint32_t pb[NT][2];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          float pv[4];
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            const float vA = okA[nt][c] ? s[nt][c] * sl2 : -INFINITY;
+            const float vB = okB[nt][c] ? s[nt][2 + c] * sl2 : -INFINITY;
+            float tmax = fmaxf(vA, vB);
+            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
+            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
+            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
+            const float m_old = m_run[nt][c];
+            const float m_new = fmaxf(m_old, tmax);
+            float alpha, pA, pB;
+            if (m_new == -INFINITY) {
+              alpha = 1.f;
+              pA = 0.f;
+              pB = 0.f;
+            } else {
+              alpha = fast_exp2(m_old - m_new);
+              pA = fast_exp2(vA - m_new);
+              pB = fast_exp2(vB - m_new);
+            }
+            m_run[nt][c] = m_new;
+            l_run[nt][c] = l_run[nt][c] * alpha + pA + pB;
+            if constexpr (MODE == MODE_DECODE) {
+#pragma unroll
+              for (int mt = 0; mt < D / 16; ++mt) {
+                o[mt][nt][c] *= alpha;
+                o[mt][nt][2 + c] *= alpha;
+              }
+            }
+            pv[c] = pA;
+            pv[2 + c] = pB;
+          }
+          if constexpr (MODE == MODE_DECODE) {
+            pb[nt][0] = movmatrix_trans(pack_bf16(pv[0], pv[1]));
+            pb[nt][1] = movmatrix_trans(pack_bf16(pv[2], pv[3]));
+          }
         }
-      }
 
-      // ---- O^T += V^T . P^T ----
-      if constexpr (MODE == MODE_DECODE) {
+        // ---- O^T += V^T . P^T ----
+        if constexpr (MODE == MODE_DECODE) {
 #pragma unroll
-        for (int mt = 0; mt < D / 16; ++mt) {
-          uint32_t a[4];
-          const int key = (mi >> 1) * 8 + ri;
-          ldmatrix_x4_trans(a[0], a[1], a[2], a[3], sv + key * L::ROW_BYTES + swz(key, 2 * mt + (mi & 1)));
+          for (int mt = 0; mt < D / 16; ++mt) {
+            uint32_t a[4];
+            const int key = (mi >> 1) * 8 + ri;
+            ldmatrix_x4_trans(a[0], a[1], a[2], a[3], sv + key * L::ROW_BYTES + swz(key, 2 * mt + (mi & 1)));
 #pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            const uint32_t b[2] = {pb[nt][0], pb[nt][1]};
-            mma_bf16_16816(o[mt][nt], a, b);
+            for (int nt = 0; nt < NT; ++nt) {
+              const uint32_t b[2] = {pb[nt][0], pb[nt][1]};
+              mma_bf16_16816(o[mt][nt], a, b);
+            }
           }
         }
       }
@@ -343,78 +357,79 @@ __global__ void __launch_bounds__(WARPS * 32, 2) sparse_decode_bf16_kernel(Decod
     __syncwarp();
   }
   cp_async_wait<0>();
-  if constexpr (MODE == MODE_PROBS) return;
 
-  // ---- finish per-warp row sums ----
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      float l = l_run[nt][c];
-      l += __shfl_xor_sync(0xffffffffu, l, 4);
-      l += __shfl_xor_sync(0xffffffffu, l, 8);
-      l += __shfl_xor_sync(0xffffffffu, l, 16);
-      l_run[nt][c] = l;
-    }
-  __syncthreads();  // all warps done with their rings: reuse as merge buffer
-
-  float* mo = reinterpret_cast<float*>(smem + L::Q_BYTES);   // [WARPS][MP][D]
-  float* mml = mo + (MODE == MODE_DECODE ? WARPS * L::MP * D : 0);  // [WARPS][MP][2]
-  if (lane < 4) {
+  if constexpr (MODE != MODE_PROBS) {
+    // ---- finish per-warp row sums ----
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
-        const int r = nt * 8 + 2 * lane + c;
-        mml[(warp * L::MP + r) * 2 + 0] = m_run[nt][c];
-        mml[(warp * L::MP + r) * 2 + 1] = l_run[nt][c];
+        float l = l_run[nt][c];
+        l += __shfl_xor_sync(0xffffffffu, l, 4);
+        l += __shfl_xor_sync(0xffffffffu, l, 8);
+        l += __shfl_xor_sync(0xffffffffu, l, 16);
+        l_run[nt][c] = l;
       }
-  }
-  if constexpr (MODE == MODE_DECODE) {
-#pragma unroll
-    for (int mt = 0; mt < D / 16; ++mt)
+    __syncthreads();  // all warps done with their rings: reuse as merge buffer
+
+    float* mo = reinterpret_cast<float*>(smem + L::Q_BYTES);          // [WARPS][MP][D]
+    float* mml = mo + (MODE == MODE_DECODE ? WARPS * L::MP * D : 0);  // [WARPS][MP][2]
+    if (lane < 4) {
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int dd = mt * 16 + (lane >> 2) + (c >= 2 ? 8 : 0);
-          const int r = nt * 8 + 2 * (lane & 3) + (c & 1);
-          mo[(warp * L::MP + r) * D + dd] = o[mt][nt][c];
+        for (int c = 0; c < 2; ++c) {
+          const int r = nt * 8 + 2 * lane + c;
+          mml[(warp * L::MP + r) * 2 + 0] = m_run[nt][c];
+          mml[(warp * L::MP + r) * 2 + 1] = l_run[nt][c];
         }
-  }
-  __syncthreads();
-
-  constexpr int DO = MODE == MODE_DECODE ? D : 1;
-  for (int e = threadIdx.x; e < M * DO; e += WARPS * 32) {
-    const int r = e / DO, dd = e % DO;
-    float mstar = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < WARPS; ++w) mstar = fmaxf(mstar, mml[(w * L::MP + r) * 2]);
-    float acc = 0.f, lsum = 0.f;
-    if (mstar != -INFINITY) {
-#pragma unroll
-      for (int w = 0; w < WARPS; ++w) {
-        const float mw = mml[(w * L::MP + r) * 2];
-        const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - mstar);
-        if constexpr (MODE == MODE_DECODE) acc += f * mo[(w * L::MP + r) * D + dd];
-        lsum += f * mml[(w * L::MP + r) * 2 + 1];
-      }
     }
-    const float val = lsum > 0.f ? acc / lsum : 0.f;
-    const float lse = lsum > 0.f ? (mstar + __log2f(lsum)) * LN2 : -INFINITY;
-    if (p.splits == 1) {
-      if constexpr (MODE == MODE_DECODE) {
-        __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + (u * M + r) * (int64_t)D;
-        og[dd] = __float2bfloat16_rn(val);
+    if constexpr (MODE == MODE_DECODE) {
+#pragma unroll
+      for (int mt = 0; mt < D / 16; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int dd = mt * 16 + (lane >> 2) + (c >= 2 ? 8 : 0);
+            const int r = nt * 8 + 2 * (lane & 3) + (c & 1);
+            mo[(warp * L::MP + r) * D + dd] = o[mt][nt][c];
+          }
+    }
+    __syncthreads();
+
+    constexpr int DO = MODE == MODE_DECODE ? D : 1;
+    for (int e = threadIdx.x; e < M * DO; e += WARPS * 32) {
+      const int r = e / DO, dd = e % DO;
+      float mstar = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < WARPS; ++w) mstar = fmaxf(mstar, mml[(w * L::MP + r) * 2]);
+      float acc = 0.f, lsum = 0.f;
+      if (mstar != -INFINITY) {
+#pragma unroll
+        for (int w = 0; w < WARPS; ++w) {
+          const float mw = mml[(w * L::MP + r) * 2];
+          const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - mstar);
+          if constexpr (MODE == MODE_DECODE) acc += f * mo[(w * L::MP + r) * D + dd];
+          lsum += f * mml[(w * L::MP + r) * 2 + 1];
+        }
       }
-      if (dd == 0) {
-        if (p.lse) p.lse[u * M + r] = lse;
-        if (MODE == MODE_DECODE && lsum <= 0.f) set_status(p.status, STS_DEV_EMPTY_ROW);
+      const float val = lsum > 0.f ? acc / lsum : 0.f;
+      const float lse = lsum > 0.f ? (mstar + __log2f(lsum)) * LN2 : -INFINITY;
+      if (p.splits == 1) {
+        if constexpr (MODE == MODE_DECODE) {
+          __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + (u * M + r) * (int64_t)D;
+          og[dd] = __float2bfloat16_rn(val);
+        }
+        if (dd == 0) {
+          if (p.lse) p.lse[u * M + r] = lse;
+          if (MODE == MODE_DECODE && lsum <= 0.f) set_status(p.status, STS_DEV_EMPTY_ROW);
+        }
+      } else {
+        const int64_t base = ((int64_t)split * p.units + u) * M + r;
+        if constexpr (MODE == MODE_DECODE) p.o_part[base * D + dd] = val;
+        if (dd == 0) p.l_part[base] = lse;
       }
-    } else {
-      const int64_t base = ((int64_t)split * p.units + u) * M + r;
-      if constexpr (MODE == MODE_DECODE) p.o_part[base * D + dd] = val;
-      if (dd == 0) p.l_part[base] = lse;
     }
   }
 }
@@ -513,13 +528,25 @@ __global__ void __launch_bounds__(F32_WARPS * 32) sparse_decode_f32_kernel(Decod
 }
 
 template <int D, int NT, int MODE>
-int launch_bf16(const DecodeParams& p, cudaStream_t st) {
-  constexpr int STAGES = MODE == MODE_DECODE ? 3 : 4, WARPS = 4;
-  using L = Bf16Layout<D, NT, STAGES, WARPS, MODE != MODE_DECODE>;
-  auto kern = sparse_decode_bf16_kernel<D, NT, STAGES, WARPS, MODE>;
-  STS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM));
+int launch_bf16(DecodeParams p, cudaStream_t st) {
+  constexpr int WARPS = 4;
+  // K-only draft passes move 16*SUB keys per stage so one stage is ~8 KB.
+  constexpr int SUB = MODE == MODE_DECODE ? (D == 64 ? 2 : 1) : (D == 64 ? 4 : 2);
+  constexpr int STAGES = 3;
+  using L = Bf16Layout<D, NT, STAGES, WARPS, MODE, SUB>;
+  auto kern = sparse_decode_bf16_kernel<D, NT, STAGES, WARPS, MODE, SUB>;
+  // index slice per CTA (+ membership bits): sized from the largest CTA range
+  int64_t max_keys = 0;
+  if (p.idx) {
+    const int64_t tiles = (p.idx_ld + L::KT - 1) / L::KT;
+    max_keys = ((tiles + p.splits - 1) / p.splits + 1) * L::KT;
+    if (max_keys > 8192) max_keys = 8192;  // larger slices read the list from global
+  }
+  p.idx_cap = (int)max_keys;
+  const int smem = L::FIXED + (int)max_keys * (p.member ? 8 : 4);
+  STS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   dim3 grid(p.splits, (unsigned)p.units);
-  kern<<<grid, WARPS * 32, L::SMEM, st>>>(p);
+  kern<<<grid, WARPS * 32, smem, st>>>(p);
   STS_LAUNCH_CHECK();
   return STS_OK;
 }
