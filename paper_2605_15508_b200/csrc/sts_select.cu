@@ -48,10 +48,13 @@ struct SelectParams {
   int64_t buf_bytes;      // bytes of one key buffer (smem or global)
 };
 
+constexpr int CAND_BYTES = 16384;  // candidate keys after the first digit
+
 struct SelShared {
   uint32_t hist[NBINS];
   int warp_tot[SEL_WARPS];
   int bcast[8];
+  uint8_t cand[CAND_BYTES];
 };
 
 // value of logical-row element j: fp32 sum over sources in order
@@ -95,7 +98,7 @@ __device__ __forceinline__ double page_sum(const SelectParams& p, const int32_t*
   return __dadd_rn(x0, pairwise_sum(p, srcs, start + 1, len - 1));
 }
 
-// Block-wide exclusive scan of an int in thread order.
+// Block-wide exclusive scan of an int in thread order (3 barriers).
 __device__ __forceinline__ int block_scan_int(int v, int* warp_tot, int& total) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int incl = v;
@@ -106,44 +109,45 @@ __device__ __forceinline__ int block_scan_int(int v, int* warp_tot, int& total) 
   }
   if (lane == 31) warp_tot[warp] = incl;
   __syncthreads();
-  int before = 0, tot = 0;
-#pragma unroll 8
-  for (int w = 0; w < SEL_WARPS; ++w) {
-    int t = warp_tot[w];
-    before += (w < warp) ? t : 0;
-    tot += t;
+  if (warp == 0) {
+    int x = warp_tot[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    warp_tot[lane] = x;  // inclusive prefix over warps
   }
   __syncthreads();
-  total = tot;
+  const int before = warp > 0 ? warp_tot[warp - 1] : 0;
+  total = warp_tot[SEL_WARPS - 1];
+  __syncthreads();
   return before + incl - v;
 }
 
 // Radix select: k-th largest key (1-based k <= n) among keys[0..n).
-// On return T is that key and need = how many keys equal to T belong to the
-// top-k (the rest of the top-k are strictly greater than T).
+// On return T is that key, need = how many keys equal to T belong to the
+// top-k (the rest are strictly greater), ties = how many keys equal T.
+// After the first digit the surviving keys are compacted into `cand` (when
+// they fit) so later digits only touch the candidates.
 template <typename K>
-__device__ void radix_select(const K* keys, int n, int k, SelShared& sh, K& T, int& need) {
+__device__ void radix_select(const K* keys, int n, int k, SelShared& sh, K* cand, int cand_cap, K& T,
+                             int& need, int& ties) {
   constexpr int KBITS = sizeof(K) * 8;
   K prefix = 0, pmask = 0;
   int krem = k;
+  const K* src = keys;
+  int len = n;
+  bool compacted = false;
   for (int shift = KBITS - DIGIT_BITS;; shift -= DIGIT_BITS) {
     const int s = shift < 0 ? 0 : shift;
     const int width = shift < 0 ? DIGIT_BITS + shift : DIGIT_BITS;
     const int nb = 1 << width;
     for (int i = threadIdx.x; i < nb; i += SEL_THREADS) sh.hist[i] = 0;
     __syncthreads();
-    for (int j = threadIdx.x; j < n; j += SEL_THREADS) {
-      K key = keys[j];
-      bool in = (key & pmask) == prefix;
-      uint32_t dig = (uint32_t)((key >> s) & (K)(nb - 1));
-      // warp-aggregate lanes hitting the same bin (probability rows are
-      // exponent-concentrated, so bins collide heavily)
-      uint32_t active = __ballot_sync(__activemask(), in);
-      if (in) {
-        uint32_t peers = __match_any_sync(active, dig);
-        int leader = __ffs(peers) - 1;
-        if ((int)(threadIdx.x & 31) == leader) atomicAdd(&sh.hist[dig], (uint32_t)__popc(peers));
-      }
+    for (int j = threadIdx.x; j < len; j += SEL_THREADS) {
+      const K key = src[j];
+      if ((key & pmask) == prefix) atomicAdd(&sh.hist[(uint32_t)((key >> s) & (K)(nb - 1))], 1u);
     }
     __syncthreads();
     // descending scan over bins: thread t owns bins nb-1-4t .. nb-4-4t
@@ -164,6 +168,7 @@ __device__ void radix_select(const K* keys, int n, int k, SelShared& sh, K& T, i
         if (acc < krem && krem <= acc + local[q]) {
           sh.bcast[0] = nb - 1 - 4 * (int)threadIdx.x - q;
           sh.bcast[1] = acc;
+          sh.bcast[2] = local[q];
         }
         acc += local[q];
       }
@@ -171,11 +176,34 @@ __device__ void radix_select(const K* keys, int n, int k, SelShared& sh, K& T, i
     __syncthreads();
     const int digit = sh.bcast[0];
     const int above = sh.bcast[1];
+    const int inbin = sh.bcast[2];
     __syncthreads();
     prefix |= (K)digit << s;
     pmask |= (K)(nb - 1) << s;
     krem -= above;
-    if (s == 0) break;
+    if (s == 0) {
+      ties = inbin;
+      break;
+    }
+    if (!compacted && inbin <= cand_cap && inbin < len) {
+      if (threadIdx.x == 0) sh.bcast[3] = 0;
+      __syncthreads();
+      const int lane = threadIdx.x & 31;
+      for (int j0 = 0; j0 < len; j0 += SEL_THREADS) {
+        const int j = j0 + threadIdx.x;
+        const K key = j < len ? src[j] : (K)0;
+        const bool m = j < len && (key & pmask) == prefix;
+        const uint32_t bal = __ballot_sync(0xffffffffu, m);
+        int base = 0;
+        if (lane == 0 && bal) base = atomicAdd(&sh.bcast[3], __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (m) cand[base + __popc(bal & ((1u << lane) - 1u))] = key;
+      }
+      __syncthreads();
+      src = cand;
+      len = inbin;
+      compacted = true;
+    }
   }
   T = prefix;
   need = krem;
@@ -256,7 +284,7 @@ __device__ double pairwise_vals(const float* vals, int start, int n) {
 template <typename KeyAt, typename Extra>
 __device__ __forceinline__ int emit_sorted(const SelectParams& p, SelShared& sh, int32_t* out, int len,
                                            KeyAt key_at, uint64_t T, int need, Extra extra, int out_base,
-                                           bool write_bits, uint32_t* bits) {
+                                           bool write_bits, uint32_t* bits, bool all_ties = false) {
   int run_sel = 0, run_tie = 0;
   for (int base = 0; base < len; base += 4 * SEL_THREADS) {
     const int j0 = base + 4 * threadIdx.x;
@@ -268,8 +296,8 @@ __device__ __forceinline__ int emit_sorted(const SelectParams& p, SelShared& sh,
       k4[q] = j < len ? key_at(j) : 0ull;
       nt += (j < len && k4[q] == T) ? 1 : 0;
     }
-    int tie_tot;
-    int tie_ex = block_scan_int(nt, sh.warp_tot, tie_tot);
+    int tie_tot = 0, tie_ex = 0;
+    if (!all_ties && need > 0) tie_ex = block_scan_int(nt, sh.warp_tot, tie_tot);
     bool f[4];
     int ns = 0;
 #pragma unroll
@@ -278,7 +306,7 @@ __device__ __forceinline__ int emit_sorted(const SelectParams& p, SelShared& sh,
       bool sel = false;
       if (j < len) {
         const bool tie = k4[q] == T;
-        sel = k4[q] > T || (tie && run_tie + tie_ex < need) || extra(j);
+        sel = k4[q] > T || (tie && need > 0 && (all_ties || run_tie + tie_ex < need)) || extra(j);
         tie_ex += tie ? 1 : 0;
       }
       f[q] = sel;
@@ -346,10 +374,10 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(SelectParams p) 
       for_row_values(p, srcs, n, [&](int j, float v) { keys[j] = f32_key(v); });
       __syncthreads();
       uint32_t T;
-      int need;
-      radix_select<uint32_t>(keys, n, b, sh, T, need);
+      int need, ties;
+      radix_select<uint32_t>(keys, n, b, sh, reinterpret_cast<uint32_t*>(sh.cand), CAND_BYTES / 4, T, need, ties);
       count = emit_sorted(p, sh, out, n, [&](int j) { return (uint64_t)keys[j]; }, (uint64_t)T, need, extra, 0,
-                          false, nullptr);
+                          false, nullptr, need == ties);
     } else {
       const int ps = p.page_size;
       const int P = (n + ps - 1) / ps;
@@ -371,10 +399,11 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(SelectParams p) 
         }
         __syncthreads();
         uint64_t T;
-        int need;
-        radix_select<uint64_t>(pkeys, P, kp, sh, T, need);
+        int need, ties;
+        radix_select<uint64_t>(pkeys, P, kp, sh, reinterpret_cast<uint64_t*>(sh.cand), CAND_BYTES / 8, T, need,
+                               ties);
         emit_sorted(p, sh, out, P, [&](int j) { return pkeys[j]; }, T, need, [](int) { return false; }, 0, true,
-                    pbits);
+                    pbits, need == ties);
       }
       __syncthreads();
       count = emit_sorted(p, sh, out, n,
