@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--mode", default="S", choices=["S", "R"])
     ap.add_argument("--sparsity", type=float, default=0.9)
+    ap.add_argument("--page-size", type=int, default=1)
+    ap.add_argument("--layout", default="separate", choices=["separate", "interleaved"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bound of the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -222,10 +224,10 @@ def main():
 
     shape = config_shape(args.config)
     budget = round(1.0 - args.sparsity, 10)
-    cfg = SparsityConfig(budget=budget)
+    cfg = SparsityConfig(budget=budget, page_size=args.page_size)
     table = random_mapping_table(shape, seed=5 + rank)
     step = STSVerifyStep(shape, cfg, table, mode=args.mode, device=dev)
-    dq, dk, tq, tk, tv = synthetic_inputs(shape, dev, seed=100 * rank)
+    dq, dk, tq, tk, tv = synthetic_inputs(shape, dev, seed=100 * rank, layout=args.layout)
     q, k, v = step.target_views(tq, tk, tv)
     dqv, dkv = step.draft_views(dq, dk)
     dense_out = torch.empty_like(step.out)
@@ -338,8 +340,10 @@ def main():
         "data": "synthetic (seeded N(0,1) bf16 Q/K/V, random head mapping)",
         "config": {"workload": f"{args.config}: Llama-3.2-1B draft -> Llama-3.1-8B target shapes, "
                                f"{shape.context} context, batch {shape.batch}, gamma {shape.gamma}, "
-                               f"sparsity {args.sparsity}, mode {args.mode}",
+                               f"sparsity {args.sparsity}, mode {args.mode}, page_size {args.page_size}, "
+                               f"kv layout {args.layout}",
                    "context": shape.context, "batch": shape.batch, "gamma": shape.gamma, "mode": args.mode,
+                   "page_size": args.page_size, "kv_layout": args.layout,
                    "keys_per_kv_head": round(cnt, 1), "l2": "flushed (256 MB write) before every timed stage",
                    "parallelism": "replicas" if world > 1 else "single"},
         "dense_us": round(den, 2), "speedup_vs_dense": round(den / att, 3),

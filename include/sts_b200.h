@@ -106,7 +106,10 @@ STS_API int sts_page_aggregate(const float* scores_dev, int64_t ld, int64_t rows
  * sparsity.sparse_attention (src/sparsity.py:152-173).
  *
  * unit u (e.g. (batch, layer, kv-head)): K/V rows at k_cache + u*kv_unit_stride
- *   (elements), row p of d contiguous elements.  Queries q[u][M][d].
+ *   (elements); row p of d contiguous elements starts kv_row_stride elements
+ *   after row p-1 (0 => d).  kv_row_stride = 2d with v = k + d is the
+ *   interleaved K|V token layout (one 4d-byte run per gathered bf16 token).
+ *   Queries q[u][M][d].
  *   keys: idx_dev[u*idx_ld + j], j < cnt_dev[u]  (idx_dev NULL => dense
  *   0..n_dense-1).  Row r attends key p iff
  *     (causal_base < 0 || pos_offset + p - causal_base <= r % rows_per_head)
@@ -120,7 +123,7 @@ STS_API size_t sts_sparse_decode_workspace_bytes(int64_t units, int32_t M, int32
  * of 16 per CTA); what the host uses when it has no better knowledge. */
 STS_API int32_t sts_auto_splits(int64_t units, int64_t keys_per_unit);
 STS_API int sts_sparse_decode(int32_t dtype, const void* q_dev, const void* k_cache_dev,
-                      const void* v_cache_dev, int64_t kv_unit_stride, int64_t units,
+                      const void* v_cache_dev, int64_t kv_unit_stride, int64_t kv_row_stride, int64_t units,
                       int32_t M, int32_t d, const int32_t* idx_dev, int64_t idx_ld,
                       const int32_t* cnt_dev, int32_t n_dense, const uint32_t* member_dev,
                       int32_t causal_base, int32_t rows_per_head, int32_t pos_offset,

@@ -29,6 +29,7 @@ struct DecodeParams {
   const void* k;
   const void* v;
   int64_t kv_stride;
+  int64_t row_stride;  // elements between consecutive K (V) rows
   int64_t units;
   int M;
   int d;
@@ -162,7 +163,7 @@ __global__ void __launch_bounds__(WARPS * 32, 2) sparse_decode_bf16_kernel(Decod
         const int ch = lane % CH;
         const int pr = key_pos(kbase + r);
         const bool ok = pr >= 0;
-        const int64_t off = (int64_t)(ok ? pr : 0) * D + ch * 8;
+        const int64_t off = (int64_t)(ok ? pr : 0) * p.row_stride + ch * 8;
         const uint32_t sk = st_k + (r >> 4) * L::SUB_BYTES;
         const int rr = r & 15;
         cp_async_16_zfill(sk + rr * L::ROW_BYTES + swz(rr, ch), kg + off, ok);
@@ -472,7 +473,7 @@ __global__ void __launch_bounds__(F32_WARPS * 32) sparse_decode_f32_kernel(Decod
         if (memg) ok = ok && ((memg[j] >> (r & 31)) & 1u);
       }
       if (ok) {
-        const float* kr = kg + (int64_t)pos * D;
+        const float* kr = kg + (int64_t)pos * p.row_stride;
         float dot = 0.f;
         for (int e = 0; e < D; ++e) dot = fmaf(q[e], kr[e], dot);
         s = dot * p.scale;
@@ -495,7 +496,7 @@ __global__ void __launch_bounds__(F32_WARPS * 32) sparse_decode_f32_kernel(Decod
         const float pk = __shfl_sync(0xffffffffu, pj, src);
         const int posk = __shfl_sync(0xffffffffu, pos, src);
         if (pk == 0.f) continue;
-        const float* vr = vg + (int64_t)posk * D;
+        const float* vr = vg + (int64_t)posk * p.row_stride;
 #pragma unroll
         for (int t = 0; t < 8; ++t) {
           const int e = lane + 32 * t;
@@ -607,7 +608,8 @@ extern "C" size_t sts_sparse_decode_workspace_bytes(int64_t units, int32_t M, in
 }
 
 extern "C" int sts_sparse_decode(int32_t dtype, const void* q_dev, const void* k_cache_dev,
-                                 const void* v_cache_dev, int64_t kv_unit_stride, int64_t units,
+                                 const void* v_cache_dev, int64_t kv_unit_stride, int64_t kv_row_stride,
+                                 int64_t units,
                                  int32_t M, int32_t d, const int32_t* idx_dev, int64_t idx_ld,
                                  const int32_t* cnt_dev, int32_t n_dense,
                                  const uint32_t* member_dev, int32_t causal_base,
@@ -632,6 +634,8 @@ extern "C" int sts_sparse_decode(int32_t dtype, const void* q_dev, const void* k
   p.k = k_cache_dev;
   p.v = v_cache_dev;
   p.kv_stride = kv_unit_stride;
+  p.row_stride = kv_row_stride > 0 ? kv_row_stride : d;
+  STS_REQUIRE(p.row_stride >= d, STS_ERR_CONTRACT, "kv_row_stride must be >= d");
   p.units = units;
   p.M = M;
   p.d = d;
@@ -694,6 +698,7 @@ static void draft_params(DecodeParams& p, const void* q_dev, const void* k_cache
   p.k = k_cache_dev;
   p.v = nullptr;
   p.kv_stride = kv_unit_stride;
+  p.row_stride = d;
   p.units = units;
   p.M = G * R;
   p.d = d;

@@ -121,8 +121,9 @@ def sparse_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
                   lse=None, status=None, workspace: Workspace | None = None, stream=None):
     """Gathered-KV sparse flash-decode.
 
-    q: [U, M, d] (bf16 or fp32); k_cache/v_cache: [U, N, d] same dtype (any
-    unit stride, rows contiguous).  idx/cnt: int32 [U, ld] / [U] key lists
+    q: [U, M, d] (bf16 or fp32); k_cache/v_cache: [U, N, d] views of the same
+    dtype with unit inner stride (row stride >= d: an interleaved K|V cache
+    [U, N, 2, d] passes kv[..., 0, :] and kv[..., 1, :]).  idx/cnt: int32 [U, ld] / [U] key lists
     (None => dense keys 0..n_dense-1).  Returns (out [U, M, d] q.dtype,
     lse fp32 [U, M]).  Semantics: include/sts_b200.h sts_sparse_decode.
     """
@@ -131,9 +132,10 @@ def sparse_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
         raise ValueError("q, k_cache, v_cache must share dtype float32 or bfloat16")
     U, M, d = q.shape
     q = q.contiguous()
-    if k_cache.stride(-1) != 1 or k_cache.stride(-2) != d or v_cache.stride() != k_cache.stride():
-        raise ValueError("k_cache/v_cache must be [U, N, d] with contiguous rows and equal strides")
+    if k_cache.stride(-1) != 1 or k_cache.stride(-2) < d or v_cache.stride() != k_cache.stride():
+        raise ValueError("k_cache/v_cache must be [U, N, d] views with unit inner stride and equal strides")
     kv_stride = k_cache.stride(0)
+    row_stride = k_cache.stride(1)
     scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
     idx_ld = idx.stride(0) if idx is not None else 0
     if member is not None and (member.stride(0) != idx_ld or member.dtype != torch.int32 and member.dtype != torch.uint32):
@@ -150,7 +152,7 @@ def sparse_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
     wbytes = lib.sts_sparse_decode_workspace_bytes(U, M, d, splits)
     ws = workspace or _ws("decode", dev)
     wbuf, wlen = ws.get(wbytes)
-    call("sts_sparse_decode", STS_DTYPE[q.dtype], ptr(q), ptr(k_cache), ptr(v_cache), kv_stride, U, M,
+    call("sts_sparse_decode", STS_DTYPE[q.dtype], ptr(q), ptr(k_cache), ptr(v_cache), kv_stride, row_stride, U, M,
          d, ptr(idx), idx_ld, ptr(cnt), int(n_dense), ptr(member), int(causal_base), int(rows_per_head),
          int(pos_offset), scale, ptr(out), ptr(lse), int(splits), ptr(status), ptr(wbuf), wlen,
          stream_handle(stream))

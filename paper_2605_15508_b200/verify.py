@@ -204,8 +204,9 @@ class STSVerifyStep:
         """[B, L, Hq, R, d] q and [B, L, Hkv, N, d] caches -> kernel unit views."""
         s = self.shape
         U = s.target_units
-        return (q.reshape(U, self.M, s.head_dim), k.reshape(U, k.shape[-2], s.head_dim),
-                v.reshape(U, v.shape[-2], s.head_dim))
+        def units(x):  # keep the row stride (interleaved K|V views are not contiguous)
+            return x.flatten(0, 2) if x.dim() == 5 else x
+        return q.reshape(U, self.M, s.head_dim), units(k), units(v)
 
     def draft_views(self, q, k):
         s = self.shape
@@ -213,11 +214,14 @@ class STSVerifyStep:
         return q.reshape(U, s.draft_group * s.rows, s.draft_head_dim), k.reshape(U, k.shape[-2], s.draft_head_dim)
 
 
-def synthetic_inputs(shape: VerifyShape, device, dtype=torch.bfloat16, seed: int = 0, n_max=None):
+def synthetic_inputs(shape: VerifyShape, device, dtype=torch.bfloat16, seed: int = 0, n_max=None,
+                     layout: str = "separate"):
     """Seeded synthetic inputs: Q, K, V ~ N(0,1); draft q/K too.
 
     Returns draft_q [B, Ld, Hqd, R, dd], draft_k [B, Ld, Hkvd, N, dd],
     target_q [B, L, Hq, R, d], target_k/v [B, L, Hkv, N, d]; N = n_kv.
+    layout "interleaved" stores the target cache as [B, L, Hkv, N, 2, d]
+    (K|V of one token adjacent) and returns k/v as strided views of it.
     Generated in chunks on the device to bound peak memory.
     """
     s = shape
@@ -235,8 +239,12 @@ def synthetic_inputs(shape: VerifyShape, device, dtype=torch.bfloat16, seed: int
         return t
 
     tq = randn((s.batch, s.target_layers, s.target_q_heads, s.rows, s.head_dim), seed + 0)
-    tk = randn((s.batch, s.target_layers, s.target_kv_heads, n, s.head_dim), seed + 1)
-    tv = randn((s.batch, s.target_layers, s.target_kv_heads, n, s.head_dim), seed + 2)
+    if layout == "interleaved":
+        kv = randn((s.batch, s.target_layers, s.target_kv_heads, n, 2, s.head_dim), seed + 1)
+        tk, tv = kv[..., 0, :], kv[..., 1, :]
+    else:
+        tk = randn((s.batch, s.target_layers, s.target_kv_heads, n, s.head_dim), seed + 1)
+        tv = randn((s.batch, s.target_layers, s.target_kv_heads, n, s.head_dim), seed + 2)
     dq = randn((s.batch, s.draft_layers, s.draft_q_heads, s.rows, s.draft_head_dim), seed + 3)
     dk = randn((s.batch, s.draft_layers, s.draft_kv_heads, n, s.draft_head_dim), seed + 4)
     return dq, dk, tq, tk, tv

@@ -62,7 +62,7 @@ def test_host_validation_without_gpu():
         _lib.call("sts_select_topk", 8, 4, None, 3, 1, None, 4, 2.0, 0, 1, 0, 0, 0, 8, 4, 8, None,
                   None, 0, None)
     with pytest.raises(ContractViolation, match="membership"):
-        _lib.call("sts_sparse_decode", 1, 8, 8, 8, 64, 1, 40, 64, 8, 4, 8, 0, 8, -1, 1, 0, 0.125, 8,
+        _lib.call("sts_sparse_decode", 1, 8, 8, 8, 64, 0, 1, 40, 64, 8, 4, 8, 0, 8, -1, 1, 0, 0.125, 8,
                   None, 1, None, None, 0, None)
 
 

@@ -214,3 +214,25 @@ def test_row_union(cuda_ok):
         for r in range(20):
             have = u_idx[u, : u_cnt[u]][(mem[u, : u_cnt[u]] >> r) & 1 == 1]
             np.testing.assert_array_equal(have, lists[src[u, r]])
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_interleaved_kv_row_stride(cuda_ok, dtype):
+    """K|V interleaved per token ([U, N, 2, d]) through the row-stride views."""
+    import torch
+
+    from paper_2605_15508_b200 import kernels
+
+    rng = np.random.default_rng(21)
+    U, G, R, d, base = 3, 4, 5, 128, 900
+    M, N = G * R, base + R
+    q, k, v, lists, idx, cnt = _case(rng, U, M, N, d, R, base, (10, 300), dtype)
+    kv = np.stack([k, v], axis=2)  # [U, N, 2, d]
+    kvd = _to_dev(kv, dtype)
+    out, _ = kernels.sparse_decode(_to_dev(q, dtype), kvd[:, :, 0, :], kvd[:, :, 1, :], idx=_to_dev(idx, dtype),
+                                   cnt=_to_dev(cnt, dtype), causal_base=base, rows_per_head=R, splits=2)
+    out = out.float().cpu().numpy()
+    tol = (RTOL32, ATOL32) if dtype == "f32" else (TOL16, TOL16)
+    for u in range(U):
+        want, _ = O.block_attention(q[u], k[u], v[u], lists[u], causal_base=base, rows_per_head=R)
+        np.testing.assert_allclose(out[u], want, rtol=tol[0], atol=tol[1])
