@@ -1,0 +1,57 @@
+// Parameters shared by the gather kernels (sparse decode, draft capture) and
+// the launch helpers implemented in sts_stream.cu.
+#pragma once
+
+#include "sts_common.cuh"
+
+namespace sts {
+
+constexpr int KEY_TILE = 16;
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr int MODE_DECODE = 0, MODE_LSE = 1, MODE_PROBS = 2;
+
+struct DecodeParams {
+  const void* q;
+  const void* k;
+  const void* v;
+  int64_t kv_stride;
+  int64_t row_stride;  // elements between consecutive K (V) rows
+  int64_t units;
+  int M;
+  int d;
+  const int32_t* idx;
+  int64_t idx_ld;
+  const int32_t* cnt;
+  int n_dense;
+  const uint32_t* member;
+  int causal_base;
+  int rows_per_head;
+  int pos_offset;
+  float scale;
+  void* out;      // final output
+  float* lse;     // final lse (nullable)
+  float* o_part;  // partials
+  float* l_part;
+  int splits;
+  int32_t* status;
+  // MODE_PROBS
+  const float* lse_in;  // [units][M] natural-log LSE
+  float* probs_out;
+  int64_t out_ld;
+  int probs_mode;       // 0: reduced over rows (mode S), 1: per row (mode R)
+  int idx_cap;
+  // stream-K bookkeeping (sts_stream.cu)
+  int* counters;        // [units], zeroed before each launch
+};
+
+// Persistent stream-K launch of the bf16 gather kernel in `mode`.
+// Workspace layout: counters [units] int32, then partial (O, lse) slots.
+size_t stream_workspace_bytes(int mode, int64_t units, int M, int d);
+int stream_launch(int mode, DecodeParams& p, void* ws, size_t ws_bytes, cudaStream_t st);
+
+int lse_merge_launch(const float* o_part, const float* lse_part, int nparts, int64_t rows, int d,
+                     int out_dtype, void* out, float* lse_out, cudaStream_t st);
+
+int auto_splits(int64_t units, int64_t keys_per_unit);
+
+}  // namespace sts
