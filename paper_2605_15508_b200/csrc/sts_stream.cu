@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(32, 1) stream_kernel(DecodeParams p) {
   constexpr int KT = L::KT, CH = L::CH, MP = L::MP;
   extern __shared__ __align__(128) uint8_t smem[];
   const int lane = threadIdx.x;
-  const int W = gridDim.x, w = blockIdx.x;
+  const int w = blockIdx.x;
   const int M = p.M;
   const int64_t U = p.units;
 
@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(32, 1) stream_kernel(DecodeParams p) {
   const uint32_t mem_base = smem_u32(s_mem);
 
   // ---- units with no keys: striped over warps (output zeros / LSE -inf) ----
-  for (int64_t u = w; u < U; u += W) {
+  for (int64_t u = w; u < U; u += gridDim.x) {
     if (unit_tiles<KT>(p, u) != 0) continue;
     if constexpr (MODE == MODE_DECODE) {
       __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + u * (int64_t)M * D;
@@ -100,6 +100,10 @@ __global__ void __launch_bounds__(32, 1) stream_kernel(DecodeParams p) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) T += __shfl_xor_sync(0xffffffffu, T, o);
   if (T == 0) return;
+  // never more warps than tiles: every active warp owns >= 1 tile, so the
+  // warps touching a unit are exactly warp_of(first)..warp_of(last)
+  const int W = (int)(T < (int64_t)gridDim.x ? T : (int64_t)gridDim.x);
+  if (w >= W) return;
   const int64_t s_w = (int64_t)w * T / W;
   const int64_t e_w = (int64_t)(w + 1) * T / W;
   if (s_w >= e_w) return;
@@ -297,10 +301,10 @@ __global__ void __launch_bounds__(32, 1) stream_kernel(DecodeParams p) {
         }
       }
     if (single) return;
+    __threadfence();
     __syncwarp();
     int last = 0;
     if (lane == 0) {
-      __threadfence();
       const int old = atomicAdd(p.counters + u, 1);
       last = old == wl - wf;
       if (last) __threadfence();
@@ -526,7 +530,7 @@ __global__ void __launch_bounds__(32, 1) stream_kernel(DecodeParams p) {
 
 template <int D, int NT, int MODE>
 struct Cfg {
-  static constexpr int STAGES = MODE == MODE_DECODE ? 4 : 3;
+  static constexpr int STAGES = 3;
   static constexpr int SUB = MODE == MODE_DECODE ? (D == 64 ? 2 : 1) : (D == 64 ? 4 : 2);
   using L = SL<D, NT, STAGES, MODE, SUB>;
 };
