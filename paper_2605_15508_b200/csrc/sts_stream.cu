@@ -176,6 +176,7 @@ __global__ void __launch_bounds__(32, 1) stream_kernel(DecodeParams p) {
       const int slot = (int)(i % L::RING);
       const int stage = (int)(i % STAGES);
       const int64_t u = s_meta[slot * 4 + 0];
+      const int jb = s_meta[slot * 4 + 1], cu = s_meta[slot * 4 + 2];
       const __nv_bfloat16* kg = static_cast<const __nv_bfloat16*>(p.k) + u * p.kv_stride;
       const __nv_bfloat16* vg = static_cast<const __nv_bfloat16*>(p.v) + u * p.kv_stride;
       const uint32_t st_k = stage_base + stage * L::STAGE_BYTES;
@@ -184,9 +185,9 @@ __global__ void __launch_bounds__(32, 1) stream_kernel(DecodeParams p) {
       for (int it = 0; it < KT / ROWS_PER_IT; ++it) {
         const int r = it * ROWS_PER_IT + lane / CH;
         const int ch = lane % CH;
-        const int pr = slot_pos(slot, r);
-        const bool ok = pr >= 0;
-        const int64_t off = (int64_t)(ok ? pr : 0) * p.row_stride + ch * 8;
+        const bool ok = jb + r < cu;
+        const int pr = ok ? (p.idx ? s_idx[slot * KT + r] : jb + r) : 0;
+        const int64_t off = (int64_t)pr * p.row_stride + ch * 8;
         const uint32_t sk = st_k + (r >> 4) * L::SUB_BYTES;
         const int rr = r & 15;
         cp_async_16_zfill(sk + rr * L::ROW_BYTES + swz(rr, ch), kg + off, ok);
@@ -311,41 +312,62 @@ __global__ void __launch_bounds__(32, 1) stream_kernel(DecodeParams p) {
     }
     last = __shfl_sync(0xffffffffu, last, 0);
     if (!last) return;
-    // merge contributors wf..wl (slots w' + u) in warp order
-    for (int r = 0; r < M; ++r) {
+    // merge contributors wf..wl (slots w' + u) in warp order.  Per-row max and
+    // weights are computed once (lanes over rows, independent loads) into the
+    // Q buffer, then lanes stream the float4 partials with no dependent loads.
+    const int n = wl - wf + 1;
+    float* s_w8 = reinterpret_cast<float*>(s_q);  // [n][M] weights, then [M] lse
+    const bool fits = (n + 1) * M * 4 <= L::Q_BYTES;
+    for (int r = lane; r < M; r += 32) {
       float mstar = -INFINITY;
-      for (int ww = wf; ww <= wl; ++ww) mstar = fmaxf(mstar, __ldcg(p.l_part + ((int64_t)ww + u) * M + r));
+      for (int ww = 0; ww < n; ++ww) mstar = fmaxf(mstar, __ldcg(p.l_part + ((int64_t)wf + ww + u) * M + r));
       float tot = 0.f;
       if (mstar != -INFINITY)
-        for (int ww = wf; ww <= wl; ++ww) {
-          const float l = __ldcg(p.l_part + ((int64_t)ww + u) * M + r);
+        for (int ww = 0; ww < n; ++ww) {
+          const float l = __ldcg(p.l_part + ((int64_t)wf + ww + u) * M + r);
           tot += l == -INFINITY ? 0.f : expf(l - mstar);
         }
-      if (lane == 0) {
-        if (p.lse) p.lse[u * M + r] = tot > 0.f ? mstar + logf(tot) : -INFINITY;
-        if (MODE == MODE_DECODE && !(tot > 0.f)) set_status(p.status, STS_DEV_EMPTY_ROW);
-      }
+      if (p.lse) p.lse[u * M + r] = tot > 0.f ? mstar + logf(tot) : -INFINITY;
+      if (MODE == MODE_DECODE && !(tot > 0.f)) set_status(p.status, STS_DEV_EMPTY_ROW);
       if constexpr (MODE == MODE_DECODE) {
-        for (int d4 = lane; d4 < D / 4; d4 += 32) {
-          float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (tot > 0.f) {
-            for (int ww = wf; ww <= wl; ++ww) {
-              const int64_t sl = (int64_t)ww + u;
-              const float l = __ldcg(p.l_part + sl * M + r);
-              if (l == -INFINITY) continue;
-              const float f = expf(l - mstar) / tot;
-              const float4 x = __ldcg(reinterpret_cast<const float4*>(p.o_part + (sl * M + r) * D) + d4);
-              acc.x += f * x.x;
-              acc.y += f * x.y;
-              acc.z += f * x.z;
-              acc.w += f * x.w;
-            }
+        if (fits) {
+          for (int ww = 0; ww < n; ++ww) {
+            const float l = __ldcg(p.l_part + ((int64_t)wf + ww + u) * M + r);
+            s_w8[ww * M + r] = (tot > 0.f && l != -INFINITY) ? expf(l - mstar) / tot : 0.f;
           }
-          __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + (u * M + r) * (int64_t)D + 4 * d4;
-          *reinterpret_cast<__nv_bfloat162*>(og) = __floats2bfloat162_rn(acc.x, acc.y);
-          *reinterpret_cast<__nv_bfloat162*>(og + 2) = __floats2bfloat162_rn(acc.z, acc.w);
+        } else {
+          s_w8[r] = mstar;  // slow path: recompute weights per element
+          s_w8[M + r] = tot;
         }
       }
+    }
+    if constexpr (MODE == MODE_DECODE) {
+      __syncwarp();
+      constexpr int D4 = D / 4;
+      for (int e = lane; e < M * D4; e += 32) {
+        const int r = e / D4, d4 = e % D4;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+        for (int ww = 0; ww < n; ++ww) {
+          const int64_t sl = (int64_t)wf + ww + u;
+          float f;
+          if (fits) {
+            f = s_w8[ww * M + r];
+          } else {
+            const float l = __ldcg(p.l_part + sl * M + r);
+            f = (s_w8[M + r] > 0.f && l != -INFINITY) ? expf(l - s_w8[r]) / s_w8[M + r] : 0.f;
+          }
+          const float4 x = __ldcg(reinterpret_cast<const float4*>(p.o_part + (sl * M + r) * D) + d4);
+          acc.x += f * x.x;
+          acc.y += f * x.y;
+          acc.z += f * x.z;
+          acc.w += f * x.w;
+        }
+        __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + (u * M + r) * (int64_t)D + 4 * d4;
+        *reinterpret_cast<__nv_bfloat162*>(og) = __floats2bfloat162_rn(acc.x, acc.y);
+        *reinterpret_cast<__nv_bfloat162*>(og + 2) = __floats2bfloat162_rn(acc.z, acc.w);
+      }
+      __syncwarp();
     }
     }
   };
@@ -383,41 +405,42 @@ __global__ void __launch_bounds__(32, 1) stream_kernel(DecodeParams p) {
     }
     const int j0 = s_meta[slot * 4 + 1];
 
-#pragma unroll 1
+    // ---- S^T = K . Q^T for every 16-key sub-tile of the stage ----
+    float s[SUB][NT][4];
+    bool okA[SUB][NT][2], okB[SUB][NT][2];
+#pragma unroll
     for (int sub = 0; sub < SUB; ++sub) {
-      if (j0 + sub * KEY_TILE >= cur_cnt) break;
+      const bool live = j0 + sub * KEY_TILE < cur_cnt;
       const uint32_t sk = stage_base + stage * L::STAGE_BYTES + sub * L::SUB_BYTES;
-      const uint32_t sv = sk + SUB * L::SUB_BYTES;
-
-      float s[NT][4];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) s[nt][c] = 0.f;
+        for (int c = 0; c < 4; ++c) s[sub][nt][c] = 0.f;
+      if (live) {
 #pragma unroll
-      for (int kk = 0; kk < D / 16; kk += 2) {
-        uint32_t a0[4], a1[4];
-        const int key = (mi & 1) * 8 + ri;
-        ldmatrix_x4(a0[0], a0[1], a0[2], a0[3], sk + key * L::ROW_BYTES + swz(key, 2 * kk + (mi >> 1)));
-        ldmatrix_x4(a1[0], a1[1], a1[2], a1[3], sk + key * L::ROW_BYTES + swz(key, 2 * kk + 2 + (mi >> 1)));
+        for (int kk = 0; kk < D / 16; kk += 2) {
+          uint32_t a0[4], a1[4];
+          const int key = (mi & 1) * 8 + ri;
+          ldmatrix_x4(a0[0], a0[1], a0[2], a0[3], sk + key * L::ROW_BYTES + swz(key, 2 * kk + (mi >> 1)));
+          ldmatrix_x4(a1[0], a1[1], a1[2], a1[3], sk + key * L::ROW_BYTES + swz(key, 2 * kk + 2 + (mi >> 1)));
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const int row = nt * 8 + ri;
-          uint32_t b[4];
-          ldmatrix_x4(b[0], b[1], b[2], b[3], q_base + row * L::ROW_BYTES + swz(row, 2 * kk + mi));
-          const uint32_t b0[2] = {b[0], b[1]};
-          const uint32_t b1[2] = {b[2], b[3]};
-          mma_bf16_16816(s[nt], a0, b0);
-          mma_bf16_16816(s[nt], a1, b1);
+          for (int nt = 0; nt < NT; ++nt) {
+            const int row = nt * 8 + ri;
+            uint32_t b[4];
+            ldmatrix_x4(b[0], b[1], b[2], b[3], q_base + row * L::ROW_BYTES + swz(row, 2 * kk + mi));
+            const uint32_t b0[2] = {b[0], b[1]};
+            const uint32_t b1[2] = {b[2], b[3]};
+            mma_bf16_16816(s[sub][nt], a0, b0);
+            mma_bf16_16816(s[sub][nt], a1, b1);
+          }
         }
       }
-
+      // masking (keys past the list, causal tail, mode-R membership)
       const int kA = (lane >> 2) + sub * KEY_TILE, kB = kA + 8;
-      const int posA = slot_pos(slot, kA);
-      const int posB = slot_pos(slot, kB);
+      const int posA = live ? slot_pos(slot, kA) : -1;
+      const int posB = live ? slot_pos(slot, kB) : -1;
       const uint32_t memA = slot_mem(slot, kA);
       const uint32_t memB = slot_mem(slot, kB);
-      bool okA[NT][2], okB[NT][2];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
@@ -428,23 +451,27 @@ __global__ void __launch_bounds__(32, 1) stream_kernel(DecodeParams p) {
             a_ = a_ && (posA + causal_shift <= rmod[nt][c]);
             b_ = b_ && (posB + causal_shift <= rmod[nt][c]);
           }
-          okA[nt][c] = a_ && ((memA >> (r & 31)) & 1u);
-          okB[nt][c] = b_ && ((memB >> (r & 31)) & 1u);
+          okA[sub][nt][c] = a_ && ((memA >> (r & 31)) & 1u);
+          okB[sub][nt][c] = b_ && ((memB >> (r & 31)) & 1u);
         }
+    }
 
-      if constexpr (MODE == MODE_PROBS) {
-        const int lk = lane >> 2;
+    if constexpr (MODE == MODE_PROBS) {
+      const int lk = lane >> 2;
+      const int R = p.rows_per_head;
+      const int G = M / R;
+#pragma unroll
+      for (int sub = 0; sub < SUB; ++sub) {
+        if (j0 + sub * KEY_TILE >= cur_cnt) break;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
             const int r = nt * 8 + 2 * (lane & 3) + c;
-            s_prob[lk * MP + r] = okA[nt][c] ? fast_exp2(s[nt][c] * sl2 - lse2[nt][c]) : 0.f;
-            s_prob[(lk + 8) * MP + r] = okB[nt][c] ? fast_exp2(s[nt][2 + c] * sl2 - lse2[nt][c]) : 0.f;
+            s_prob[lk * MP + r] = okA[sub][nt][c] ? fast_exp2(s[sub][nt][c] * sl2 - lse2[nt][c]) : 0.f;
+            s_prob[(lk + 8) * MP + r] = okB[sub][nt][c] ? fast_exp2(s[sub][nt][2 + c] * sl2 - lse2[nt][c]) : 0.f;
           }
         __syncwarp();
-        const int R = p.rows_per_head;
-        const int G = M / R;
         const int jb = j0 + sub * KEY_TILE;
         if (p.probs_mode == 0) {
           for (int e = lane; e < KEY_TILE * G; e += 32) {
@@ -465,49 +492,68 @@ __global__ void __launch_bounds__(32, 1) stream_kernel(DecodeParams p) {
           }
         }
         __syncwarp();
-      } else {
-        uint32_t pb[NT][2];
+      }
+    } else {
+      // ---- one online-softmax step over all SUB*16 keys (log2 domain) ----
+      float pv[SUB][NT][4];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          float pv[4];
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const float vA = okA[nt][c] ? s[nt][c] * sl2 : -INFINITY;
-            const float vB = okB[nt][c] ? s[nt][2 + c] * sl2 : -INFINITY;
-            float tmax = fmaxf(vA, vB);
-            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
-            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
-            tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
-            const float m_old = m_run[nt][c];
-            const float m_new = fmaxf(m_old, tmax);
-            float alpha, pA, pB;
-            if (m_new == -INFINITY) {
-              alpha = 1.f;
-              pA = 0.f;
-              pB = 0.f;
-            } else {
-              alpha = fast_exp2(m_old - m_new);
-              pA = fast_exp2(vA - m_new);
-              pB = fast_exp2(vB - m_new);
+        for (int c = 0; c < 2; ++c) {
+          float tmax = -INFINITY;
+#pragma unroll
+          for (int sub = 0; sub < SUB; ++sub) {
+            const float vA = okA[sub][nt][c] ? s[sub][nt][c] * sl2 : -INFINITY;
+            const float vB = okB[sub][nt][c] ? s[sub][nt][2 + c] * sl2 : -INFINITY;
+            s[sub][nt][c] = vA;
+            s[sub][nt][2 + c] = vB;
+            tmax = fmaxf(tmax, fmaxf(vA, vB));
+          }
+          tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
+          tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
+          tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
+          const float m_old = m_run[nt][c];
+          const float m_new = fmaxf(m_old, tmax);
+          float alpha = 1.f, psum = 0.f;
+          if (m_new != -INFINITY) {
+            alpha = fast_exp2(m_old - m_new);
+#pragma unroll
+            for (int sub = 0; sub < SUB; ++sub) {
+              pv[sub][nt][c] = fast_exp2(s[sub][nt][c] - m_new);
+              pv[sub][nt][2 + c] = fast_exp2(s[sub][nt][2 + c] - m_new);
+              psum += pv[sub][nt][c] + pv[sub][nt][2 + c];
             }
-            m_run[nt][c] = m_new;
-            l_run[nt][c] = l_run[nt][c] * alpha + pA + pB;
-            if constexpr (MODE == MODE_DECODE) {
+          } else {
+#pragma unroll
+            for (int sub = 0; sub < SUB; ++sub) {
+              pv[sub][nt][c] = 0.f;
+              pv[sub][nt][2 + c] = 0.f;
+            }
+          }
+          m_run[nt][c] = m_new;
+          l_run[nt][c] = l_run[nt][c] * alpha + psum;
+          if constexpr (MODE == MODE_DECODE) {
+            if (alpha != 1.f) {
 #pragma unroll
               for (int mt = 0; mt < D / 16; ++mt) {
                 o[mt][nt][c] *= alpha;
                 o[mt][nt][2 + c] *= alpha;
               }
             }
-            pv[c] = pA;
-            pv[2 + c] = pB;
-          }
-          if constexpr (MODE == MODE_DECODE) {
-            pb[nt][0] = movmatrix_trans(pack_bf16(pv[0], pv[1]));
-            pb[nt][1] = movmatrix_trans(pack_bf16(pv[2], pv[3]));
           }
         }
-        if constexpr (MODE == MODE_DECODE) {
+      // ---- O^T += V^T . P^T ----
+      if constexpr (MODE == MODE_DECODE) {
+#pragma unroll
+        for (int sub = 0; sub < SUB; ++sub) {
+          if (j0 + sub * KEY_TILE >= cur_cnt) break;
+          const uint32_t sv = stage_base + stage * L::STAGE_BYTES + (SUB + sub) * L::SUB_BYTES;
+          uint32_t pb[NT][2];
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt) {
+            pb[nt][0] = movmatrix_trans(pack_bf16(pv[sub][nt][0], pv[sub][nt][1]));
+            pb[nt][1] = movmatrix_trans(pack_bf16(pv[sub][nt][2], pv[sub][nt][3]));
+          }
 #pragma unroll
           for (int mt = 0; mt < D / 16; ++mt) {
             uint32_t a[4];

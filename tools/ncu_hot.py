@@ -20,6 +20,8 @@ def main():
     ap.add_argument("--launch", type=int, default=None, help="--print-details launch index filter (ncu -l)")
     a = ap.parse_args()
     cmd = ["ncu", "-i", a.report, "--page", "source", "--csv", "--print-source", "cuda,sass"]
+    if a.launch is not None:
+        cmd += ["--launch-skip", str(a.launch), "--launch-count", "1"]
     out = subprocess.run(cmd, capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     agg = {}
