@@ -53,5 +53,6 @@ int lse_merge_launch(const float* o_part, const float* lse_part, int nparts, int
                      int out_dtype, void* out, float* lse_out, cudaStream_t st);
 
 int auto_splits(int64_t units, int64_t keys_per_unit);
+int gather_launch(int mode, DecodeParams& p, cudaStream_t st);
 
 }  // namespace sts

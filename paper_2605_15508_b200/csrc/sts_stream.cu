@@ -18,6 +18,8 @@
 // MODE_LSE drops V and P.V (draft-row log-sum-exp); MODE_PROBS turns scores
 // into probabilities with a known LSE and writes them (per row, or summed
 // over the speculative rows of each head).
+#include <stdlib.h>
+
 #include "sts_decode.cuh"
 
 namespace sts {
@@ -647,6 +649,13 @@ int stream_launch(int mode, DecodeParams& p, void* ws, size_t ws_bytes, cudaStre
     p.o_part = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(p.o_part) + 15) & ~uintptr_t(15));
     STS_CUDA_CHECK(cudaMemsetAsync(p.counters, 0, (size_t)p.units * 4, st));
   }
+  // warp-specialised TMA gather (sts_gather.cu) unless STS_GATHER=stream
+  static int use_stream = -1;
+  if (use_stream < 0) {
+    const char* e = getenv("STS_GATHER");
+    use_stream = (e && strcmp(e, "stream") == 0) ? 1 : 0;
+  }
+  if (!use_stream) return gather_launch(mode, p, st);
   if (mode == MODE_DECODE) return dispatch_d<MODE_DECODE>(p, st);
   if (mode == MODE_LSE) return dispatch_d<MODE_LSE>(p, st);
   return dispatch_d<MODE_PROBS>(p, st);
