@@ -1,23 +1,27 @@
-// sts_gather.cu — warp-specialised persistent gather kernel (bf16, sm_100a).
+// sts_gather.cu — persistent row-split gather kernel (bf16, sm_100a tensor cores).
 //
-// One CTA per SM: warp 0 is a TMA producer, warps 1..NC are math consumers.
+// Work decomposition
+//  * Unit = (batch, layer, kv-head).  The key tiles of all units (KT keys per
+//    tile) form one global tile space, cut into equal contiguous ranges, one
+//    per CTA (stream-K): every CTA streams the same number of gathered bytes no
+//    matter how ragged the per-unit key lists are (mode-R unions, page mode).
+//  * A CTA has one warp per 8-row n-tile of the stacked query block
+//    (M = GQA group x (gamma+1) rows; M = 20 -> 3 warps).  All warps consume
+//    the SAME gathered K/V tile, each for its own 8 query rows, so the tile is
+//    fetched once, no math is duplicated, and a warp carries only its rows'
+//    accumulators (32 fp32 registers at d = 128).  That keeps registers low
+//    enough for 5+ CTAs (15+ warps) per SM — the latency hiding a 256-byte
+//    random-row gather needs.
+//  * One cp.async pipeline per CTA, STAGES deep, continuous across unit
+//    boundaries: index slices are prefetched STAGES tiles ahead into a ring,
+//    K/V rows (16-byte cp.async, XOR-swizzled) STAGES-1 tiles ahead of the
+//    math, one CTA barrier per tile.  Entering a new unit flushes each warp's
+//    softmax state and reloads Q; units spanning several CTAs are merged by the
+//    last CTA to arrive (per-unit counter), in CTA order (deterministic).
 //
-//  * The key tiles of all units (unit = (batch, layer, kv-head); KT keys per
-//    tile) form one global tile space cut into equal contiguous ranges, one
-//    per consumer warp (stream-K), so every consumer streams the same bytes
-//    however ragged the per-unit key lists are.
-//  * The producer walks the consumers round-robin.  For each tile it waits for
-//    a free slot in that consumer's SPC-deep ring (mbarrier `empty`), writes
-//    the tile's key positions into the slot, arms the slot's `full` mbarrier
-//    with the byte count and issues one cp.async.bulk (TMA) copy per gathered
-//    K / V row (D*2 bytes each) straight into padded shared-memory rows.  The
-//    index slice of a consumer's next tile is loaded one round ahead, so the
-//    gather never waits on a dependent index load.  Up to NC*SPC tiles
-//    (~160 KB at D=128) are in flight per SM.
-//  * Consumers issue no loads at all: wait `full`, run the tile math on the
-//    tensor cores (mma.sync m16n8k16, stacked query rows as N), release the
-//    slot.  Crossing into a new unit flushes the softmax state (final rows, or
-//    an fp32 partial merged in warp order by the last consumer to arrive).
+// (A warp-specialised variant — one producer warp issuing one cp.async.bulk
+// per gathered row into mbarrier rings — was measured 3-4x slower: 256-byte
+// bulk copies saturate the per-SM TMA unit.  See DESIGN.md §4.)
 //
 // Modes: DECODE (K+V, online softmax, O = P.V), LSE (K only, draft-row
 // log-sum-exp), PROBS (K only, probabilities from a known LSE, per row or
@@ -29,49 +33,30 @@ namespace {
 
 constexpr float LN2f = 0.6931471805599453f;
 
-template <int D, int NT, int MODE, int SUB, int NC, int SPC>
+template <int D, int NT, int MODE, int SUB, int STAGES>
 struct GL {
   static constexpr bool K_ONLY = MODE != MODE_DECODE;
   static constexpr int KT = KEY_TILE * SUB;
   static constexpr int MP = 8 * NT;
   static constexpr int CH = D / 8;
-  static constexpr int PITCH = D * 2 + 16;  // padded rows: ldmatrix conflict-free
-  static constexpr int ROWS_BYTES = KT * PITCH;
-  static constexpr int DATA = (K_ONLY ? 1 : 2) * ROWS_BYTES;
-  static constexpr int META = KT * 8 + 16;  // pos[KT], mem[KT], info[4]
-  static constexpr int STAGE = (DATA + META + 15) & ~15;
-  static constexpr int Q_BYTES = MP * D * 2;
-  static constexpr int PROB = MODE == MODE_PROBS ? KEY_TILE * MP * 4 : 0;
-  static constexpr int PER_C = SPC * STAGE + Q_BYTES + PROB;
-  static constexpr int BAR = ((NC * SPC * 2 * 8) + 127) & ~127;
-  static constexpr int SMEM = BAR + NC * PER_C;
-  static constexpr int THREADS = (NC + 1) * 32;
+  static constexpr int ROW = D * 2;
+  static constexpr int SUBB = KEY_TILE * ROW;  // one 16-key K (or V) block
+  static constexpr int STAGE = (K_ONLY ? 1 : 2) * SUB * SUBB;
+  static constexpr int RING = 2 * STAGES;
+  static constexpr int Q_BYTES = MP * ROW;
+  static constexpr int IDX_BYTES = RING * KT * 4;
+  static constexpr int META_BYTES = RING * 16;
+  static constexpr int PROB = MODE == MODE_PROBS ? KT * MP * 4 : 0;
+  static constexpr int MERGE = MP * 2 * 4;
+  static constexpr int SMEM = Q_BYTES + STAGES * STAGE + 2 * IDX_BYTES + META_BYTES + PROB + MERGE + 16;
+  static constexpr int THREADS = NT * 32;
 };
 
 __device__ __forceinline__ uint32_t swz(int row, int chunk) { return (uint32_t)((chunk ^ (row & 7)) << 4); }
 
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@!P1 bra WAIT_%=;\n\t}\n" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(bar)
-               : "memory");
+__device__ __forceinline__ void cp_async_4_zfill(uint32_t dst, const void* src, bool valid) {
+  int sz = valid ? 4 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(sz));
 }
 
 __device__ __forceinline__ int tiles_of(const DecodeParams& p, int64_t u, int KT) {
@@ -81,208 +66,147 @@ __device__ __forceinline__ int tiles_of(const DecodeParams& p, int64_t u, int KT
 
 __device__ __forceinline__ int owner_of(int64_t t, int64_t T, int W) { return (int)(((t + 1) * W - 1) / T); }
 
-// Warp-cooperative: total tiles T and the unit containing tile `t0`
-// (returns unit index and the unit's first tile).
-__device__ void locate(const DecodeParams& p, int KT, int64_t t0, int64_t& u_out, int64_t& P_out) {
-  const int lane = threadIdx.x & 31;
-  int64_t base = 0;
-  u_out = 0;
-  P_out = 0;
-  for (int64_t u0 = 0; u0 < p.units; u0 += 32) {
-    const int64_t u = u0 + lane;
-    const int t_u = u < p.units ? tiles_of(p, u, KT) : 0;
-    int64_t incl = t_u;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int64_t x = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += x;
-    }
-    const int64_t tot = __shfl_sync(0xffffffffu, incl, 31);
-    if (base + tot > t0) {
-      const uint32_t hit = __ballot_sync(0xffffffffu, base + incl > t0);
-      const int src = __ffs(hit) - 1;
-      u_out = u0 + src;
-      P_out = base + __shfl_sync(0xffffffffu, incl - t_u, src);
-      return;
-    }
-    base += tot;
-  }
-}
-
-template <int D, int NT, int MODE, int SUB, int NC, int SPC>
-__global__ void __launch_bounds__((NC + 1) * 32, 1) gather_kernel(DecodeParams p) {
-  using L = GL<D, NT, MODE, SUB, NC, SPC>;
-  constexpr int KT = L::KT, MP = L::MP, CH = L::CH, PITCH = L::PITCH;
+template <int D, int NT, int MODE, int SUB, int STAGES>
+__global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p) {
+  using L = GL<D, NT, MODE, SUB, STAGES>;
+  constexpr int KT = L::KT, MP = L::MP, CH = L::CH, NTH = L::THREADS;
   extern __shared__ __align__(128) uint8_t smem[];
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;  // this warp's n-tile: query rows 8*warp .. 8*warp+7
   const int M = p.M;
   const int64_t U = p.units;
-  const uint32_t bar_base = smem_u32(smem);  // full[k][s] then empty[k][s]
-  auto full_bar = [&](int k, int s) { return bar_base + (uint32_t)((k * SPC + s) * 8); };
-  auto empty_bar = [&](int k, int s) { return bar_base + (uint32_t)((NC * SPC + k * SPC + s) * 8); };
-  uint8_t* cbase = smem + L::BAR;
 
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < NC * SPC; ++i) {
-      mbar_init(bar_base + i * 8, 1);
-      mbar_init(bar_base + (NC * SPC + i) * 8, 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
+  uint8_t* s_q = smem;
+  uint8_t* s_stage = s_q + L::Q_BYTES;
+  int* s_idx = reinterpret_cast<int*>(s_stage + STAGES * L::STAGE);
+  uint32_t* s_mem = reinterpret_cast<uint32_t*>(s_idx + L::RING * KT);
+  int* s_meta = reinterpret_cast<int*>(s_mem + L::RING * KT);
+  float* s_prob = reinterpret_cast<float*>(s_meta + L::RING * 4);
+  float* s_merge = s_prob + (L::PROB / 4);
+  int* s_flag = reinterpret_cast<int*>(s_merge + L::MERGE / 4);
+  const uint32_t q_base = smem_u32(s_q);
+  const uint32_t stage_base = smem_u32(s_stage);
+  const uint32_t idx_base = smem_u32(s_idx);
+  const uint32_t mem_base = smem_u32(s_mem);
 
   // ---- units with no keys (striped over CTAs): zero rows, LSE -inf ----
-  if (warp == 0) {
-    for (int64_t u = blockIdx.x; u < U; u += gridDim.x) {
-      if (tiles_of(p, u, KT) != 0) continue;
-      if constexpr (MODE == MODE_DECODE) {
-        __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + u * (int64_t)M * D;
-        for (int e = lane; e < M * D; e += 32) og[e] = __float2bfloat16_rn(0.f);
-        if (lane == 0 && M > 0) set_status(p.status, STS_DEV_EMPTY_ROW);
-      }
-      if constexpr (MODE != MODE_PROBS)
-        if (p.lse)
-          for (int r = lane; r < M; r += 32) p.lse[u * M + r] = -INFINITY;
+  for (int64_t u = blockIdx.x; u < U; u += gridDim.x) {
+    if (tiles_of(p, u, KT) != 0) continue;
+    if constexpr (MODE == MODE_DECODE) {
+      __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + u * (int64_t)M * D;
+      for (int e = tid; e < M * D; e += NTH) og[e] = __float2bfloat16_rn(0.f);
+      if (tid == 0 && M > 0) set_status(p.status, STS_DEV_EMPTY_ROW);
     }
+    if constexpr (MODE != MODE_PROBS)
+      if (p.lse)
+        for (int r = tid; r < M; r += NTH) p.lse[u * M + r] = -INFINITY;
   }
 
-  // ---- tile space and consumer ranges ----
+  // ---- tile space and this CTA's range (every warp computes the same) ----
   int64_t T = 0;
   for (int64_t u = lane; u < U; u += 32) T += tiles_of(p, u, KT);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) T += __shfl_xor_sync(0xffffffffu, T, o);
   if (T == 0) return;
-  const int W = (int)(T < (int64_t)gridDim.x * NC ? T : (int64_t)gridDim.x * NC);
-  auto range_of = [&](int gw, int64_t& s, int64_t& e) {
-    if (gw >= W) {
-      s = e = 0;
-      return;
+  const int W = (int)(T < (int64_t)gridDim.x ? T : (int64_t)gridDim.x);
+  const int w = blockIdx.x;
+  if (w >= W) return;
+  const int64_t s_w = (int64_t)w * T / W;
+  const int64_t e_w = (int64_t)(w + 1) * T / W;
+  const int64_t ntile = e_w - s_w;
+
+  // unit holding tile s_w (warp-cooperative prefix scan over unit tile counts)
+  int64_t iu = 0, iP = 0;
+  {
+    int64_t base = 0;
+    for (int64_t u0 = 0; u0 < U; u0 += 32) {
+      const int64_t u = u0 + lane;
+      const int t_u = u < U ? tiles_of(p, u, KT) : 0;
+      int64_t incl = t_u;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int64_t x = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += x;
+      }
+      const int64_t tot = __shfl_sync(0xffffffffu, incl, 31);
+      if (base + tot > s_w) {
+        const uint32_t hit = __ballot_sync(0xffffffffu, base + incl > s_w);
+        const int src = __ffs(hit) - 1;
+        iu = u0 + src;
+        iP = base + __shfl_sync(0xffffffffu, incl - t_u, src);
+        break;
+      }
+      base += tot;
     }
-    s = (int64_t)gw * T / W;
-    e = (int64_t)(gw + 1) * T / W;
+  }
+  int icnt = p.idx ? p.cnt[iu] : p.n_dense;
+  int64_t iPn = iP + (icnt + KT - 1) / KT;
+
+  // index cursor: slice of relative tile i -> ring slot i % RING (+ meta)
+  auto issue_idx = [&](int64_t i) {
+    if (i >= ntile) return;
+    const int64_t t = s_w + i;
+    while (t >= iPn) {
+      ++iu;
+      iP = iPn;
+      icnt = p.idx ? p.cnt[iu] : p.n_dense;
+      iPn = iP + (icnt + KT - 1) / KT;
+    }
+    const int slot = (int)(i % L::RING);
+    const int j0 = (int)(t - iP) * KT;
+    if (tid == 0) {
+      s_meta[slot * 4 + 0] = (int)iu;
+      s_meta[slot * 4 + 1] = j0;
+      s_meta[slot * 4 + 2] = icnt;
+      s_meta[slot * 4 + 3] = (int)iP;
+    }
+    if (p.idx) {
+      for (int e = tid; e < KT; e += NTH) {
+        const bool ok = j0 + e < icnt;
+        cp_async_4_zfill(idx_base + (slot * KT + e) * 4, p.idx + iu * p.idx_ld + (ok ? j0 + e : 0), ok);
+        if (p.member)
+          cp_async_4_zfill(mem_base + (slot * KT + e) * 4, p.member + iu * p.idx_ld + (ok ? j0 + e : 0), ok);
+      }
+    }
+  };
+  auto slot_pos = [&](int slot, int r) -> int {
+    const int j = s_meta[slot * 4 + 1] + r;
+    if (j >= s_meta[slot * 4 + 2]) return -1;
+    return p.idx ? s_idx[slot * KT + r] : j;
   };
 
-  if (warp == 0) {
-    // =========================== PRODUCER ===========================
-    int64_t t[NC], e[NC], cu[NC], cP[NC], cPn[NC];
-    int ccnt[NC], n_used[NC];
-    int pos_n[NC];
-    uint32_t mem_n[NC];
-    int nu[NC], nj0[NC], ncnt[NC], nP[NC];  // info of the prefetched tile t[k]
-#pragma unroll
-    for (int k = 0; k < NC; ++k) {
-      range_of(blockIdx.x * NC + k, t[k], e[k]);
-      n_used[k] = 0;
-      cu[k] = 0;
-      cP[k] = 0;
-      if (t[k] < e[k]) {
-        int64_t uu, PP;
-        locate(p, KT, t[k], uu, PP);
-        cu[k] = uu;
-        cP[k] = PP;
-      }
-      ccnt[k] = t[k] < e[k] ? (p.idx ? p.cnt[cu[k]] : p.n_dense) : 0;
-      cPn[k] = cP[k] + (ccnt[k] + KT - 1) / KT;
+  // K/V gather of relative tile i (its indices are already in the ring)
+  auto issue_data = [&](int64_t i) {
+    if (i >= ntile) return;
+    const int slot = (int)(i % L::RING);
+    const int stage = (int)(i % STAGES);
+    const int64_t u = s_meta[slot * 4 + 0];
+    const int jb = s_meta[slot * 4 + 1], cu = s_meta[slot * 4 + 2];
+    const __nv_bfloat16* kg = static_cast<const __nv_bfloat16*>(p.k) + u * p.kv_stride;
+    const __nv_bfloat16* vg = static_cast<const __nv_bfloat16*>(p.v) + u * p.kv_stride;
+    const uint32_t st = stage_base + stage * L::STAGE;
+    constexpr int CHUNKS = KT * CH;
+#pragma unroll 4
+    for (int c = tid; c < CHUNKS; c += NTH) {
+      const int r = c / CH, ch = c % CH;
+      const bool ok = jb + r < cu;
+      const int pr = ok ? (p.idx ? s_idx[slot * KT + r] : jb + r) : 0;
+      const int64_t off = (int64_t)pr * p.row_stride + ch * 8;
+      const uint32_t sk = st + (r >> 4) * L::SUBB;
+      const int rr = r & 15;
+      cp_async_16_zfill(sk + rr * L::ROW + swz(rr, ch), kg + off, ok);
+      if constexpr (MODE == MODE_DECODE)
+        cp_async_16_zfill(sk + SUB * L::SUBB + rr * L::ROW + swz(rr, ch), vg + off, ok);
     }
-    // prefetch the positions of tile t[k] into registers (lane = row)
-    auto prefetch = [&](int k) {
-      if (t[k] >= e[k]) return;
-      while (t[k] >= cPn[k]) {
-        ++cu[k];
-        cP[k] = cPn[k];
-        ccnt[k] = p.idx ? p.cnt[cu[k]] : p.n_dense;
-        cPn[k] = cP[k] + (ccnt[k] + KT - 1) / KT;
-      }
-      nu[k] = (int)cu[k];
-      nj0[k] = (int)(t[k] - cP[k]) * KT;
-      ncnt[k] = ccnt[k];
-      nP[k] = (int)cP[k];
-      const int j = nj0[k] + lane;
-      pos_n[k] = -1;
-      mem_n[k] = 0xffffffffu;
-      if (lane < KT && j < ncnt[k]) {
-        pos_n[k] = p.idx ? __ldg(p.idx + cu[k] * p.idx_ld + j) : j;
-        if (p.member) mem_n[k] = __ldg(p.member + cu[k] * p.idx_ld + j);
-      }
-    };
-#pragma unroll
-    for (int k = 0; k < NC; ++k) prefetch(k);
+  };
 
-    const int row_bytes = D * 2;
-    bool more = true;
-    while (more) {
-      more = false;
+  // ---- per-warp running state (its 8 rows) ----
+  float o[MODE == MODE_DECODE ? D / 16 : 1][4];
+  float m_run[2], l_run[2], lse2[2];
+  int rmod[2];
 #pragma unroll
-      for (int k = 0; k < NC; ++k) {
-        if (t[k] >= e[k]) continue;
-        more = true;
-        const int s = n_used[k] % SPC;
-        const uint32_t ph = (uint32_t)((n_used[k] / SPC) & 1);
-        mbar_wait(empty_bar(k, s), ph ^ 1u);
-        uint8_t* st = cbase + k * L::PER_C + s * L::STAGE;
-        int* m_pos = reinterpret_cast<int*>(st + L::DATA);
-        uint32_t* m_mem = reinterpret_cast<uint32_t*>(m_pos + KT);
-        int* m_info = reinterpret_cast<int*>(m_mem + KT);
-        const int valid = min(KT, ncnt[k] - nj0[k]);
-        const int pos = pos_n[k];
-        if (lane < KT) {
-          m_pos[lane] = pos;
-          m_mem[lane] = mem_n[k];
-        }
-        if (lane == 0) {
-          m_info[0] = nu[k];
-          m_info[1] = nj0[k];
-          m_info[2] = ncnt[k];
-          m_info[3] = nP[k];
-        }
-        __syncwarp();
-        const uint32_t fb = full_bar(k, s);
-        if (lane == 0) mbar_arrive_expect_tx(fb, (uint32_t)(valid * row_bytes * (L::K_ONLY ? 1 : 2)));
-        __syncwarp();
-        const int64_t u = nu[k];
-        const __nv_bfloat16* kg = static_cast<const __nv_bfloat16*>(p.k) + u * p.kv_stride;
-        const __nv_bfloat16* vg = static_cast<const __nv_bfloat16*>(p.v) + u * p.kv_stride;
-        const uint32_t dst = smem_u32(st);
-        constexpr int COPIES = (L::K_ONLY ? 1 : 2) * KT;
-#pragma unroll
-        for (int c0 = 0; c0 < COPIES; c0 += 32) {
-          const int c = c0 + lane;
-          const int r = c % KT;
-          const int isv = c / KT;
-          const int pr = __shfl_sync(0xffffffffu, pos, r & 31);
-          if (c < COPIES && r < valid) {
-            const __nv_bfloat16* src = (isv ? vg : kg) + (int64_t)pr * p.row_stride;
-            bulk_g2s(dst + isv * L::ROWS_BYTES + r * PITCH, src, row_bytes, fb);
-          }
-        }
-        // next tile of consumer k: its index slice lands during the next round
-        ++t[k];
-        ++n_used[k];
-        prefetch(k);
-      }
-    }
-    return;
-  }
-
-  // =========================== CONSUMERS ===========================
-  const int k = warp - 1;
-  const int gw = blockIdx.x * NC + k;
-  int64_t s_w, e_w;
-  range_of(gw, s_w, e_w);
-  if (s_w >= e_w) return;
-  uint8_t* my = cbase + k * L::PER_C;
-  uint8_t* s_q = my + SPC * L::STAGE;
-  float* s_prob = reinterpret_cast<float*>(s_q + L::Q_BYTES);
-  const uint32_t q_base = smem_u32(s_q);
-
-  float o[MODE == MODE_DECODE ? D / 16 : 1][NT][4];
-  float m_run[NT][2], l_run[NT][2], lse2[NT][2];
-  int rmod[NT][2];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-    for (int c = 0; c < 2; ++c) rmod[nt][c] = (nt * 8 + 2 * (lane & 3) + c) % p.rows_per_head;
+  for (int c = 0; c < 2; ++c) rmod[c] = (warp * 8 + 2 * (lane & 3) + c) % p.rows_per_head;
   const float sl2 = p.scale * LOG2E;
   const int causal_shift = p.pos_offset - p.causal_base;
   const bool causal = p.causal_base >= 0;
@@ -294,359 +218,324 @@ __global__ void __launch_bounds__((NC + 1) * 32, 1) gather_kernel(DecodeParams p
 #pragma unroll
     for (int a = 0; a < (MODE == MODE_DECODE ? D / 16 : 1); ++a)
 #pragma unroll
-      for (int b = 0; b < NT; ++b)
+      for (int c = 0; c < 4; ++c) o[a][c] = 0.f;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) o[a][b][c] = 0.f;
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        m_run[nt][c] = -INFINITY;
-        l_run[nt][c] = 0.f;
-      }
+    for (int c = 0; c < 2; ++c) {
+      m_run[c] = -INFINITY;
+      l_run[c] = 0.f;
+    }
   };
 
+  // Q of unit u: each warp loads its own 8 rows (only it reads them)
   auto load_q = [&](int64_t u) {
     const __nv_bfloat16* qg = static_cast<const __nv_bfloat16*>(p.q) + u * (int64_t)M * D;
-    for (int c = lane; c < MP * CH; c += 32) {
-      const int r = c / CH, ch = c % CH;
+    for (int c = lane; c < 8 * CH; c += 32) {
+      const int r = warp * 8 + c / CH, ch = c % CH;
       uint4 val = make_uint4(0, 0, 0, 0);
       if (r < M) val = *reinterpret_cast<const uint4*>(qg + (int64_t)r * D + ch * 8);
-      *reinterpret_cast<uint4*>(s_q + r * (D * 2) + swz(r, ch)) = val;
+      *reinterpret_cast<uint4*>(s_q + r * L::ROW + swz(r, ch)) = val;
     }
     if constexpr (MODE == MODE_PROBS) {
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int r = nt * 8 + 2 * (lane & 3) + c;
-          lse2[nt][c] = r < M ? p.lse_in[u * M + r] * LOG2E : 0.f;
-        }
+      for (int c = 0; c < 2; ++c) {
+        const int r = warp * 8 + 2 * (lane & 3) + c;
+        lse2[c] = r < M ? p.lse_in[u * M + r] * LOG2E : 0.f;
+      }
     }
     __syncwarp();
   };
 
+  // finish unit u for this CTA: final rows, or partial + (last CTA) merge
   auto flush = [&](int64_t u, int P_u, int cnt_u) {
     if constexpr (MODE != MODE_PROBS) {
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          float l = l_run[nt][c];
-          l += __shfl_xor_sync(0xffffffffu, l, 4);
-          l += __shfl_xor_sync(0xffffffffu, l, 8);
-          l += __shfl_xor_sync(0xffffffffu, l, 16);
-          l_run[nt][c] = l;
-        }
+      for (int c = 0; c < 2; ++c) {
+        float l = l_run[c];
+        l += __shfl_xor_sync(0xffffffffu, l, 4);
+        l += __shfl_xor_sync(0xffffffffu, l, 8);
+        l += __shfl_xor_sync(0xffffffffu, l, 16);
+        l_run[c] = l;
+      }
       const int64_t tiles = (cnt_u + KT - 1) / KT;
       const int wf = owner_of(P_u, T, W);
       const int wl = owner_of(P_u + tiles - 1, T, W);
       const bool single = wf == wl;
-      const int64_t slot = (int64_t)gw + u;
+      const int64_t slot = (int64_t)w + u;
       float* part_o = p.o_part + slot * (int64_t)M * D;
       float* part_l = p.l_part + slot * (int64_t)M;
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
+      for (int c = 0; c < 2; ++c) {
+        const int r = warp * 8 + 2 * (lane & 3) + c;
+        if (r >= M) continue;
+        const float l = l_run[c];
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        const float lse = l > 0.f ? (m_run[c] + __log2f(l)) * LN2f : -INFINITY;
+        if constexpr (MODE == MODE_DECODE) {
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int r = nt * 8 + 2 * (lane & 3) + c;
-          if (r >= M) continue;
-          const float l = l_run[nt][c];
-          const float inv = l > 0.f ? 1.f / l : 0.f;
-          const float lse = l > 0.f ? (m_run[nt][c] + __log2f(l)) * LN2f : -INFINITY;
-          if constexpr (MODE == MODE_DECODE) {
-#pragma unroll
-            for (int mt = 0; mt < D / 16; ++mt) {
-              const int d0 = mt * 16 + (lane >> 2);
-              if (single) {
-                __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + (u * M + r) * (int64_t)D;
-                og[d0] = __float2bfloat16_rn(o[mt][nt][c] * inv);
-                og[d0 + 8] = __float2bfloat16_rn(o[mt][nt][2 + c] * inv);
-              } else {
-                part_o[r * D + d0] = o[mt][nt][c] * inv;
-                part_o[r * D + d0 + 8] = o[mt][nt][2 + c] * inv;
-              }
-            }
-          }
-          if (lane < 4) {
+          for (int mt = 0; mt < D / 16; ++mt) {
+            const int d0 = mt * 16 + (lane >> 2);
             if (single) {
-              if (p.lse) p.lse[u * M + r] = lse;
-              if (MODE == MODE_DECODE && !(l > 0.f)) set_status(p.status, STS_DEV_EMPTY_ROW);
+              __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + (u * M + r) * (int64_t)D;
+              og[d0] = __float2bfloat16_rn(o[mt][c] * inv);
+              og[d0 + 8] = __float2bfloat16_rn(o[mt][2 + c] * inv);
             } else {
-              part_l[r] = lse;
+              part_o[r * D + d0] = o[mt][c] * inv;
+              part_o[r * D + d0 + 8] = o[mt][2 + c] * inv;
             }
           }
         }
-      if (single) return;
-      __threadfence();
-      __syncwarp();
-      int last = 0;
-      if (lane == 0) {
-        const int old = atomicAdd(p.counters + u, 1);
-        last = old == wl - wf;
-        if (last) __threadfence();
-      }
-      last = __shfl_sync(0xffffffffu, last, 0);
-      if (!last) return;
-      const int n = wl - wf + 1;
-      float* s_w8 = reinterpret_cast<float*>(s_q);
-      const bool fits = (n + 1) * M * 4 <= L::Q_BYTES;
-      for (int r = lane; r < M; r += 32) {
-        float mstar = -INFINITY;
-        for (int ww = 0; ww < n; ++ww) mstar = fmaxf(mstar, __ldcg(p.l_part + ((int64_t)wf + ww + u) * M + r));
-        float tot = 0.f;
-        if (mstar != -INFINITY)
-          for (int ww = 0; ww < n; ++ww) {
-            const float l = __ldcg(p.l_part + ((int64_t)wf + ww + u) * M + r);
-            tot += l == -INFINITY ? 0.f : expf(l - mstar);
+        if (lane < 4) {
+          if (single) {
+            if (p.lse) p.lse[u * M + r] = lse;
+            if (MODE == MODE_DECODE && !(l > 0.f)) set_status(p.status, STS_DEV_EMPTY_ROW);
+          } else {
+            part_l[r] = lse;
           }
-        if (p.lse) p.lse[u * M + r] = tot > 0.f ? mstar + logf(tot) : -INFINITY;
-        if (MODE == MODE_DECODE && !(tot > 0.f)) set_status(p.status, STS_DEV_EMPTY_ROW);
-        if constexpr (MODE == MODE_DECODE) {
-          if (fits) {
+        }
+      }
+      if (single) return;  // uniform across the CTA
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) {
+        const int old = atomicAdd(p.counters + u, 1);
+        const int last = old == wl - wf;
+        if (last) __threadfence();
+        *s_flag = last;
+      }
+      __syncthreads();
+      const int last = *s_flag;
+      if (!last) return;
+      // merge CTAs wf..wl in order; each warp merges its own 8 rows
+      const int n = wl - wf + 1;
+      if (lane < 8) {
+        const int r = warp * 8 + lane;
+        float mstar = -INFINITY, tot = 0.f;
+        if (r < M) {
+          for (int ww = 0; ww < n; ++ww) mstar = fmaxf(mstar, __ldcg(p.l_part + ((int64_t)wf + ww + u) * M + r));
+          if (mstar != -INFINITY)
             for (int ww = 0; ww < n; ++ww) {
               const float l = __ldcg(p.l_part + ((int64_t)wf + ww + u) * M + r);
-              s_w8[ww * M + r] = (tot > 0.f && l != -INFINITY) ? expf(l - mstar) / tot : 0.f;
+              tot += l == -INFINITY ? 0.f : expf(l - mstar);
             }
-          } else {
-            s_w8[r] = mstar;
-            s_w8[M + r] = tot;
-          }
+          if (p.lse) p.lse[u * M + r] = tot > 0.f ? mstar + logf(tot) : -INFINITY;
+          if (MODE == MODE_DECODE && !(tot > 0.f)) set_status(p.status, STS_DEV_EMPTY_ROW);
         }
+        s_merge[r * 2 + 0] = mstar;
+        s_merge[r * 2 + 1] = tot;
       }
+      __syncwarp();
       if constexpr (MODE == MODE_DECODE) {
-        __syncwarp();
         constexpr int D4 = D / 4;
-        for (int e = lane; e < M * D4; e += 32) {
-          const int r = e / D4, d4 = e % D4;
+        for (int e = lane; e < 8 * D4; e += 32) {
+          const int r = warp * 8 + e / D4, d4 = e % D4;
+          if (r >= M) continue;
+          const float mstar = s_merge[r * 2], tot = s_merge[r * 2 + 1];
           float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (tot > 0.f) {
 #pragma unroll 4
-          for (int ww = 0; ww < n; ++ww) {
-            const int64_t sl = (int64_t)wf + ww + u;
-            float f;
-            if (fits) {
-              f = s_w8[ww * M + r];
-            } else {
+            for (int ww = 0; ww < n; ++ww) {
+              const int64_t sl = (int64_t)wf + ww + u;
               const float l = __ldcg(p.l_part + sl * M + r);
-              f = (s_w8[M + r] > 0.f && l != -INFINITY) ? expf(l - s_w8[r]) / s_w8[M + r] : 0.f;
+              const float f = l == -INFINITY ? 0.f : expf(l - mstar) / tot;
+              const float4 x = __ldcg(reinterpret_cast<const float4*>(p.o_part + (sl * M + r) * D) + d4);
+              acc.x += f * x.x;
+              acc.y += f * x.y;
+              acc.z += f * x.z;
+              acc.w += f * x.w;
             }
-            const float4 x = __ldcg(reinterpret_cast<const float4*>(p.o_part + (sl * M + r) * D) + d4);
-            acc.x += f * x.x;
-            acc.y += f * x.y;
-            acc.z += f * x.z;
-            acc.w += f * x.w;
           }
           __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + (u * M + r) * (int64_t)D + 4 * d4;
           *reinterpret_cast<__nv_bfloat162*>(og) = __floats2bfloat162_rn(acc.x, acc.y);
           *reinterpret_cast<__nv_bfloat162*>(og + 2) = __floats2bfloat162_rn(acc.z, acc.w);
         }
-        __syncwarp();
       }
+      __syncwarp();
     }
   };
 
-  int n_used = 0;
-  for (int64_t i = 0; i < e_w - s_w; ++i) {
-    const int slot = n_used % SPC;
-    mbar_wait(full_bar(k, slot), (uint32_t)((n_used / SPC) & 1));
-    const uint8_t* st = my + slot * L::STAGE;
-    const int* m_pos = reinterpret_cast<const int*>(st + L::DATA);
-    const uint32_t* m_mem = reinterpret_cast<const uint32_t*>(m_pos + KT);
-    const int* m_info = reinterpret_cast<const int*>(m_mem + KT);
-    const int64_t u = m_info[0];
-    const int j0 = m_info[1];
+  // ---- pipeline: idx slices STAGES tiles ahead, K/V STAGES-1 tiles ahead ----
+  for (int kk = 0; kk < STAGES; ++kk) issue_idx(kk);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+#pragma unroll
+  for (int s0 = 0; s0 < STAGES - 1; ++s0) {
+    issue_data(s0);
+    issue_idx(s0 + STAGES);
+    cp_async_commit();
+  }
+
+  for (int64_t i = 0; i < ntile; ++i) {
+    cp_async_wait<STAGES - 2>();  // this thread's gathers of tile i landed (and idx of tile i+STAGES-1)
+    __syncthreads();              // ... everyone's; everyone is done with tile i-1
+    issue_data(i + STAGES - 1);   // refill the stage tile i-1 used
+    issue_idx(i + 2 * STAGES - 1);
+    cp_async_commit();
+
+    const int slot = (int)(i % L::RING);
+    const int stage = (int)(i % STAGES);
+    const int64_t u = s_meta[slot * 4 + 0];
+    const int j0 = s_meta[slot * 4 + 1];
     if (u != cur_u) {
       if (cur_u >= 0) flush(cur_u, cur_P, cur_cnt);
       cur_u = u;
-      cur_cnt = m_info[2];
-      cur_P = m_info[3];
+      cur_cnt = s_meta[slot * 4 + 2];
+      cur_P = s_meta[slot * 4 + 3];
       reset_state();
       load_q(u);
     }
-    const uint32_t sk0 = smem_u32(st);
-    // fast path: every row valid, no membership bits, whole tile in the
-    // committed prefix (positions ascending) -> no per-element masking
-    const int last_pos = m_pos[KT - 1];
-    const bool simple = (j0 + KT <= cur_cnt) && !p.member && (!causal || last_pos + causal_shift <= 0);
+    const uint32_t sk0 = stage_base + stage * L::STAGE;
+    // fast path: all keys valid, no membership bits, tile inside the committed
+    // prefix (positions ascending) -> no per-element masking
+    const bool simple = (j0 + KT <= cur_cnt) && !p.member && (!causal || slot_pos(slot, KT - 1) + causal_shift <= 0);
 
-    float s[SUB][NT][4];
-    bool okA[SUB][NT][2], okB[SUB][NT][2];
+    float s[SUB][4];
+    bool okA[SUB][2], okB[SUB][2];
 #pragma unroll
     for (int sub = 0; sub < SUB; ++sub) {
       const bool live = j0 + sub * KEY_TILE < cur_cnt;
-      const uint32_t sk = sk0 + sub * KEY_TILE * PITCH;
+      const uint32_t sk = sk0 + sub * L::SUBB;
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) s[sub][nt][c] = 0.f;
+      for (int c = 0; c < 4; ++c) s[sub][c] = 0.f;
       if (live) {
 #pragma unroll
         for (int kk = 0; kk < D / 16; kk += 2) {
-          uint32_t a0[4], a1[4];
+          uint32_t a0[4], a1[4], b[4];
           const int key = (mi & 1) * 8 + ri;
-          ldmatrix_x4(a0[0], a0[1], a0[2], a0[3], sk + key * PITCH + (2 * kk + (mi >> 1)) * 16);
-          ldmatrix_x4(a1[0], a1[1], a1[2], a1[3], sk + key * PITCH + (2 * kk + 2 + (mi >> 1)) * 16);
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            const int row = nt * 8 + ri;
-            uint32_t b[4];
-            ldmatrix_x4(b[0], b[1], b[2], b[3], q_base + row * (D * 2) + swz(row, 2 * kk + mi));
-            const uint32_t b0[2] = {b[0], b[1]};
-            const uint32_t b1[2] = {b[2], b[3]};
-            mma_bf16_16816(s[sub][nt], a0, b0);
-            mma_bf16_16816(s[sub][nt], a1, b1);
-          }
+          ldmatrix_x4(a0[0], a0[1], a0[2], a0[3], sk + key * L::ROW + swz(key, 2 * kk + (mi >> 1)));
+          ldmatrix_x4(a1[0], a1[1], a1[2], a1[3], sk + key * L::ROW + swz(key, 2 * kk + 2 + (mi >> 1)));
+          const int row = warp * 8 + ri;
+          ldmatrix_x4(b[0], b[1], b[2], b[3], q_base + row * L::ROW + swz(row, 2 * kk + mi));
+          const uint32_t b0[2] = {b[0], b[1]};
+          const uint32_t b1[2] = {b[2], b[3]};
+          mma_bf16_16816(s[sub], a0, b0);
+          mma_bf16_16816(s[sub], a1, b1);
         }
       }
       if (simple) {
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-          for (int c = 0; c < 2; ++c) okA[sub][nt][c] = okB[sub][nt][c] = true;
+        okA[sub][0] = okA[sub][1] = okB[sub][0] = okB[sub][1] = true;
       } else {
         const int kA = (lane >> 2) + sub * KEY_TILE, kB = kA + 8;
-        const int posA = m_pos[kA], posB = m_pos[kB];
-        const uint32_t memA = m_mem[kA], memB = m_mem[kB];
+        const int posA = live ? slot_pos(slot, kA) : -1;
+        const int posB = live ? slot_pos(slot, kB) : -1;
+        const uint32_t memA = p.member ? s_mem[slot * KT + kA] : 0xffffffffu;
+        const uint32_t memB = p.member ? s_mem[slot * KT + kB] : 0xffffffffu;
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const int r = nt * 8 + 2 * (lane & 3) + c;
-            bool a_ = posA >= 0, b_ = posB >= 0;
-            if (causal) {
-              a_ = a_ && (posA + causal_shift <= rmod[nt][c]);
-              b_ = b_ && (posB + causal_shift <= rmod[nt][c]);
-            }
-            okA[sub][nt][c] = a_ && ((memA >> (r & 31)) & 1u);
-            okB[sub][nt][c] = b_ && ((memB >> (r & 31)) & 1u);
+        for (int c = 0; c < 2; ++c) {
+          const int r = warp * 8 + 2 * (lane & 3) + c;
+          bool a_ = posA >= 0, b_ = posB >= 0;
+          if (causal) {
+            a_ = a_ && (posA + causal_shift <= rmod[c]);
+            b_ = b_ && (posB + causal_shift <= rmod[c]);
           }
+          okA[sub][c] = a_ && ((memA >> (r & 31)) & 1u);
+          okB[sub][c] = b_ && ((memB >> (r & 31)) & 1u);
+        }
       }
     }
 
     if constexpr (MODE == MODE_PROBS) {
+      // every warp writes its rows' probabilities; the CTA then reduces over
+      // the speculative rows of each head (a head's rows can span warps)
       const int lk = lane >> 2;
-      const int R = p.rows_per_head;
-      const int G = M / R;
 #pragma unroll
-      for (int sub = 0; sub < SUB; ++sub) {
-        if (j0 + sub * KEY_TILE >= cur_cnt) break;
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            const int r = nt * 8 + 2 * (lane & 3) + c;
-            s_prob[lk * MP + r] = okA[sub][nt][c] ? fast_exp2(s[sub][nt][c] * sl2 - lse2[nt][c]) : 0.f;
-            s_prob[(lk + 8) * MP + r] = okB[sub][nt][c] ? fast_exp2(s[sub][nt][2 + c] * sl2 - lse2[nt][c]) : 0.f;
-          }
-        __syncwarp();
-        const int jb = j0 + sub * KEY_TILE;
-        if (p.probs_mode == 0) {
-          for (int e2 = lane; e2 < KEY_TILE * G; e2 += 32) {
-            const int key = e2 % KEY_TILE, hh = e2 / KEY_TILE;
-            const int pos = m_pos[sub * KEY_TILE + key];
-            if (pos >= 0 && pos + p.pos_offset < p.causal_base) {
-              float acc = s_prob[key * MP + hh * R];
-              for (int ii = 1; ii < R; ++ii) acc = __fadd_rn(acc, s_prob[key * MP + hh * R + ii]);
-              p.probs_out[(u * G + hh) * p.out_ld + jb + key] = acc;
-            }
-          }
-        } else {
-          for (int e2 = lane; e2 < KEY_TILE * M; e2 += 32) {
-            const int key = e2 % KEY_TILE, r = e2 / KEY_TILE;
-            const int pos = m_pos[sub * KEY_TILE + key];
-            if (pos >= 0 && pos + p.pos_offset <= p.causal_base + r % R)
-              p.probs_out[(u * M + r) * p.out_ld + jb + key] = s_prob[key * MP + r];
-          }
-        }
-        __syncwarp();
-      }
-    } else {
-      float pv[SUB][NT][4];
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
+      for (int sub = 0; sub < SUB; ++sub)
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-          float tmax = -INFINITY;
-#pragma unroll
-          for (int sub = 0; sub < SUB; ++sub) {
-            const float vA = okA[sub][nt][c] ? s[sub][nt][c] * sl2 : -INFINITY;
-            const float vB = okB[sub][nt][c] ? s[sub][nt][2 + c] * sl2 : -INFINITY;
-            s[sub][nt][c] = vA;
-            s[sub][nt][2 + c] = vB;
-            tmax = fmaxf(tmax, fmaxf(vA, vB));
-          }
-          tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
-          tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
-          tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
-          const float m_old = m_run[nt][c];
-          const float m_new = fmaxf(m_old, tmax);
-          float alpha = 1.f, psum = 0.f;
-          if (m_new != -INFINITY) {
-            alpha = fast_exp2(m_old - m_new);
-#pragma unroll
-            for (int sub = 0; sub < SUB; ++sub) {
-              pv[sub][nt][c] = fast_exp2(s[sub][nt][c] - m_new);
-              pv[sub][nt][2 + c] = fast_exp2(s[sub][nt][2 + c] - m_new);
-              psum += pv[sub][nt][c] + pv[sub][nt][2 + c];
-            }
-          } else {
-#pragma unroll
-            for (int sub = 0; sub < SUB; ++sub) {
-              pv[sub][nt][c] = 0.f;
-              pv[sub][nt][2 + c] = 0.f;
-            }
-          }
-          m_run[nt][c] = m_new;
-          l_run[nt][c] = l_run[nt][c] * alpha + psum;
-          if constexpr (MODE == MODE_DECODE) {
-            if (alpha != 1.f) {
-#pragma unroll
-              for (int mt = 0; mt < D / 16; ++mt) {
-                o[mt][nt][c] *= alpha;
-                o[mt][nt][2 + c] *= alpha;
-              }
-            }
+          const int r = warp * 8 + 2 * (lane & 3) + c;
+          s_prob[(sub * 16 + lk) * MP + r] = okA[sub][c] ? fast_exp2(s[sub][c] * sl2 - lse2[c]) : 0.f;
+          s_prob[(sub * 16 + lk + 8) * MP + r] = okB[sub][c] ? fast_exp2(s[sub][2 + c] * sl2 - lse2[c]) : 0.f;
+        }
+      __syncthreads();
+      const int R = p.rows_per_head;
+      const int G = M / R;
+      if (p.probs_mode == 0) {
+        for (int e2 = tid; e2 < KT * G; e2 += NTH) {
+          const int key = e2 % KT, hh = e2 / KT;
+          const int pos = slot_pos(slot, key);
+          if (pos >= 0 && pos + p.pos_offset < p.causal_base) {
+            float acc = s_prob[key * MP + hh * R];
+            for (int ii = 1; ii < R; ++ii) acc = __fadd_rn(acc, s_prob[key * MP + hh * R + ii]);
+            p.probs_out[(u * G + hh) * p.out_ld + j0 + key] = acc;
           }
         }
+      } else {
+        for (int e2 = tid; e2 < KT * M; e2 += NTH) {
+          const int key = e2 % KT, r = e2 / KT;
+          const int pos = slot_pos(slot, key);
+          if (pos >= 0 && pos + p.pos_offset <= p.causal_base + r % R)
+            p.probs_out[(u * M + r) * p.out_ld + j0 + key] = s_prob[key * MP + r];
+        }
+      }
+      // the next iteration's barrier orders these reads before s_prob reuse
+    } else {
+      float pv[SUB][4];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float tmax = -INFINITY;
+#pragma unroll
+        for (int sub = 0; sub < SUB; ++sub) {
+          const float vA = okA[sub][c] ? s[sub][c] * sl2 : -INFINITY;
+          const float vB = okB[sub][c] ? s[sub][2 + c] * sl2 : -INFINITY;
+          s[sub][c] = vA;
+          s[sub][2 + c] = vB;
+          tmax = fmaxf(tmax, fmaxf(vA, vB));
+        }
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 4));
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 8));
+        tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 16));
+        const float m_old = m_run[c];
+        const float m_new = fmaxf(m_old, tmax);
+        float alpha = 1.f, psum = 0.f;
+        if (m_new != -INFINITY) {
+          alpha = fast_exp2(m_old - m_new);
+#pragma unroll
+          for (int sub = 0; sub < SUB; ++sub) {
+            pv[sub][c] = fast_exp2(s[sub][c] - m_new);
+            pv[sub][2 + c] = fast_exp2(s[sub][2 + c] - m_new);
+            psum += pv[sub][c] + pv[sub][2 + c];
+          }
+        } else {
+#pragma unroll
+          for (int sub = 0; sub < SUB; ++sub) pv[sub][c] = pv[sub][2 + c] = 0.f;
+        }
+        m_run[c] = m_new;
+        l_run[c] = l_run[c] * alpha + psum;
+        if constexpr (MODE == MODE_DECODE) {
+#pragma unroll
+          for (int mt = 0; mt < D / 16; ++mt) {
+            o[mt][c] *= alpha;
+            o[mt][2 + c] *= alpha;
+          }
+        }
+      }
       if constexpr (MODE == MODE_DECODE) {
 #pragma unroll
         for (int sub = 0; sub < SUB; ++sub) {
           if (j0 + sub * KEY_TILE >= cur_cnt) break;
-          const uint32_t sv = sk0 + L::ROWS_BYTES + sub * KEY_TILE * PITCH;
-          uint32_t pb[NT][2];
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            pb[nt][0] = movmatrix_trans(pack_bf16(pv[sub][nt][0], pv[sub][nt][1]));
-            pb[nt][1] = movmatrix_trans(pack_bf16(pv[sub][nt][2], pv[sub][nt][3]));
-          }
+          const uint32_t sv = sk0 + (SUB + sub) * L::SUBB;
+          const uint32_t b[2] = {movmatrix_trans(pack_bf16(pv[sub][0], pv[sub][1])),
+                                 movmatrix_trans(pack_bf16(pv[sub][2], pv[sub][3]))};
 #pragma unroll
           for (int mt = 0; mt < D / 16; ++mt) {
             uint32_t a[4];
             const int key = (mi >> 1) * 8 + ri;
-            ldmatrix_x4_trans(a[0], a[1], a[2], a[3], sv + key * PITCH + (2 * mt + (mi & 1)) * 16);
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-              const uint32_t b[2] = {pb[nt][0], pb[nt][1]};
-              mma_bf16_16816(o[mt][nt], a, b);
-            }
+            ldmatrix_x4_trans(a[0], a[1], a[2], a[3], sv + key * L::ROW + swz(key, 2 * mt + (mi & 1)));
+            mma_bf16_16816(o[mt], a, b);
           }
         }
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(empty_bar(k, slot));
-    ++n_used;
   }
+  cp_async_wait<0>();
   if (cur_u >= 0) flush(cur_u, cur_P, cur_cnt);
 }
 
 template <int D, int NT, int MODE>
 struct GCfg {
-  static constexpr int SUB = MODE == MODE_DECODE ? (D == 64 ? 2 : 1) : 2;
-  static constexpr int SPC = 3;
-  // as many consumer warps (<= 6) as fit in 227 KB of shared memory
-  static constexpr int NC = GL<D, NT, MODE, SUB, 6, SPC>::SMEM <= 227 * 1024 ? 6 : 5;
-  using L = GL<D, NT, MODE, SUB, NC, SPC>;
+  static constexpr int SUB = MODE == MODE_DECODE ? (D == 64 ? 2 : 1) : (D == 64 ? 4 : 2);
+  static constexpr int STAGES = 4;
+  using L = GL<D, NT, MODE, SUB, STAGES>;
 };
 
 template <int D, int NT, int MODE>
@@ -654,10 +543,12 @@ int launch_gather(DecodeParams& p, cudaStream_t st) {
   using C = GCfg<D, NT, MODE>;
   using L = typename C::L;
   static_assert(L::SMEM <= 227 * 1024, "gather kernel shared memory");
-  static_assert(L::KT <= 32, "producer keeps one key position per lane");
-  auto kern = gather_kernel<D, NT, MODE, C::SUB, C::NC, C::SPC>;
+  auto kern = gather_kernel<D, NT, MODE, C::SUB, C::STAGES>;
   STS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM));
-  kern<<<num_sms(), L::THREADS, L::SMEM, st>>>(p);
+  int per_sm = 0;
+  STS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::THREADS, L::SMEM));
+  if (per_sm < 1) per_sm = 1;
+  kern<<<num_sms() * per_sm, L::THREADS, L::SMEM, st>>>(p);
   STS_LAUNCH_CHECK();
   return STS_OK;
 }
@@ -683,8 +574,6 @@ int gdispatch_d(DecodeParams& p, cudaStream_t st) {
 }
 
 }  // namespace
-
-int gather_consumers_per_sm() { return 6; }
 
 int gather_launch(int mode, DecodeParams& p, cudaStream_t st) {
   if (mode == MODE_DECODE) return gdispatch_d<MODE_DECODE>(p, st);
