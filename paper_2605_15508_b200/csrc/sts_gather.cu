@@ -144,7 +144,10 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
   int64_t iPn = iP + (icnt + KT - 1) / KT;
 
   // index cursor: slice of relative tile i -> ring slot i % RING (+ meta)
+  int idx_slot = 0;  // ring slot of the next issue_idx call (calls are sequential in i)
   auto issue_idx = [&](int64_t i) {
+    const int slot = idx_slot;
+    idx_slot = idx_slot + 1 == L::RING ? 0 : idx_slot + 1;
     if (i >= ntile) return;
     const int64_t t = s_w + i;
     while (t >= iPn) {
@@ -153,7 +156,6 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
       icnt = p.idx ? p.cnt[iu] : p.n_dense;
       iPn = iP + (icnt + KT - 1) / KT;
     }
-    const int slot = (int)(i % L::RING);
     const int j0 = (int)(t - iP) * KT;
     if (tid == 0) {
       s_meta[slot * 4 + 0] = (int)iu;
@@ -176,28 +178,31 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
     return p.idx ? s_idx[slot * KT + r] : j;
   };
 
-  // K/V gather of relative tile i (its indices are already in the ring)
-  auto issue_data = [&](int64_t i) {
+  // K/V gather of relative tile i (its indices are already in the ring).
+  // Work item = (K or V, row, half row): one position lookup and one address
+  // per 8 chunks of 16 B (XOR-swizzled destination).
+  auto issue_data = [&](int64_t i, int slot, int stage) {
     if (i >= ntile) return;
-    const int slot = (int)(i % L::RING);
-    const int stage = (int)(i % STAGES);
     const int64_t u = s_meta[slot * 4 + 0];
     const int jb = s_meta[slot * 4 + 1], cu = s_meta[slot * 4 + 2];
-    const __nv_bfloat16* kg = static_cast<const __nv_bfloat16*>(p.k) + u * p.kv_stride;
-    const __nv_bfloat16* vg = static_cast<const __nv_bfloat16*>(p.v) + u * p.kv_stride;
     const uint32_t st = stage_base + stage * L::STAGE;
-    constexpr int CHUNKS = KT * CH;
-#pragma unroll 4
-    for (int c = tid; c < CHUNKS; c += NTH) {
-      const int r = c / CH, ch = c % CH;
+    constexpr int HALF = CH / 2;  // chunks per item
+    constexpr int ITEMS = (L::K_ONLY ? 1 : 2) * KT * 2;
+    for (int it = tid; it < ITEMS; it += NTH) {
+      const int half = it & 1;
+      const int r = (it >> 1) % KT;
+      const int isv = (it >> 1) / KT;
       const bool ok = jb + r < cu;
       const int pr = ok ? (p.idx ? s_idx[slot * KT + r] : jb + r) : 0;
-      const int64_t off = (int64_t)pr * p.row_stride + ch * 8;
-      const uint32_t sk = st + (r >> 4) * L::SUBB;
+      const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(isv ? p.v : p.k) + u * p.kv_stride +
+                                 (int64_t)pr * p.row_stride + half * HALF * 8;
       const int rr = r & 15;
-      cp_async_16_zfill(sk + rr * L::ROW + swz(rr, ch), kg + off, ok);
-      if constexpr (MODE == MODE_DECODE)
-        cp_async_16_zfill(sk + SUB * L::SUBB + rr * L::ROW + swz(rr, ch), vg + off, ok);
+      const uint32_t drow = st + (isv * SUB + (r >> 4)) * L::SUBB + rr * L::ROW;
+#pragma unroll
+      for (int c = 0; c < HALF; ++c) {
+        const int ch = half * HALF + c;
+        cp_async_16_zfill(drow + swz(rr, ch), src + c * 8, ok);
+      }
     }
   };
 
@@ -211,6 +216,7 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
   const int causal_shift = p.pos_offset - p.causal_base;
   const bool causal = p.causal_base >= 0;
   const int mi = lane >> 3, ri = lane & 7;
+  uint32_t qf[D / 16][2];  // this warp's Q^T B-fragments, loaded once per unit
   int64_t cur_u = -1;
   int cur_P = 0, cur_cnt = 0;
 
@@ -234,6 +240,12 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
       uint4 val = make_uint4(0, 0, 0, 0);
       if (r < M) val = *reinterpret_cast<const uint4*>(qg + (int64_t)r * D + ch * 8);
       *reinterpret_cast<uint4*>(s_q + r * L::ROW + swz(r, ch)) = val;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int kk = 0; kk < D / 16; kk += 2) {
+      const int row = warp * 8 + ri;
+      ldmatrix_x4(qf[kk][0], qf[kk][1], qf[kk + 1][0], qf[kk + 1][1], q_base + row * L::ROW + swz(row, 2 * kk + mi));
     }
     if constexpr (MODE == MODE_PROBS) {
 #pragma unroll
@@ -360,20 +372,22 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
   __syncthreads();
 #pragma unroll
   for (int s0 = 0; s0 < STAGES - 1; ++s0) {
-    issue_data(s0);
+    issue_data(s0, s0, s0);
     issue_idx(s0 + STAGES);
     cp_async_commit();
   }
 
+  int slot = 0, stage = 0;                              // of tile i
+  int f_slot = STAGES - 1, f_stage = STAGES - 1;        // of tile i + STAGES - 1
   for (int64_t i = 0; i < ntile; ++i) {
     cp_async_wait<STAGES - 2>();  // this thread's gathers of tile i landed (and idx of tile i+STAGES-1)
     __syncthreads();              // ... everyone's; everyone is done with tile i-1
-    issue_data(i + STAGES - 1);   // refill the stage tile i-1 used
+    issue_data(i + STAGES - 1, f_slot, f_stage);  // refill the stage tile i-1 used
     issue_idx(i + 2 * STAGES - 1);
     cp_async_commit();
+    f_slot = f_slot + 1 == L::RING ? 0 : f_slot + 1;
+    f_stage = f_stage + 1 == STAGES ? 0 : f_stage + 1;
 
-    const int slot = (int)(i % L::RING);
-    const int stage = (int)(i % STAGES);
     const int64_t u = s_meta[slot * 4 + 0];
     const int j0 = s_meta[slot * 4 + 1];
     if (u != cur_u) {
@@ -400,16 +414,12 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
       if (live) {
 #pragma unroll
         for (int kk = 0; kk < D / 16; kk += 2) {
-          uint32_t a0[4], a1[4], b[4];
+          uint32_t a0[4], a1[4];
           const int key = (mi & 1) * 8 + ri;
           ldmatrix_x4(a0[0], a0[1], a0[2], a0[3], sk + key * L::ROW + swz(key, 2 * kk + (mi >> 1)));
           ldmatrix_x4(a1[0], a1[1], a1[2], a1[3], sk + key * L::ROW + swz(key, 2 * kk + 2 + (mi >> 1)));
-          const int row = warp * 8 + ri;
-          ldmatrix_x4(b[0], b[1], b[2], b[3], q_base + row * L::ROW + swz(row, 2 * kk + mi));
-          const uint32_t b0[2] = {b[0], b[1]};
-          const uint32_t b1[2] = {b[2], b[3]};
-          mma_bf16_16816(s[sub], a0, b0);
-          mma_bf16_16816(s[sub], a1, b1);
+          mma_bf16_16816(s[sub], a0, qf[kk]);
+          mma_bf16_16816(s[sub], a1, qf[kk + 1]);
         }
       }
       if (simple) {
@@ -502,10 +512,12 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
         m_run[c] = m_new;
         l_run[c] = l_run[c] * alpha + psum;
         if constexpr (MODE == MODE_DECODE) {
+          if (__any_sync(0xffffffffu, alpha != 1.f)) {  // the running max rarely moves
 #pragma unroll
-          for (int mt = 0; mt < D / 16; ++mt) {
-            o[mt][c] *= alpha;
-            o[mt][2 + c] *= alpha;
+            for (int mt = 0; mt < D / 16; ++mt) {
+              o[mt][c] *= alpha;
+              o[mt][2 + c] *= alpha;
+            }
           }
         }
       }
@@ -526,6 +538,8 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
         }
       }
     }
+    slot = slot + 1 == L::RING ? 0 : slot + 1;
+    stage = stage + 1 == STAGES ? 0 : stage + 1;
   }
   cp_async_wait<0>();
   if (cur_u >= 0) flush(cur_u, cur_P, cur_cnt);
