@@ -179,30 +179,30 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
   };
 
   // K/V gather of relative tile i (its indices are already in the ring).
-  // Work item = (K or V, row, half row): one position lookup and one address
-  // per 8 chunks of 16 B (XOR-swizzled destination).
+  // A warp instruction covers 32/CH whole rows (512 contiguous bytes at
+  // d = 128) so every request is fully coalesced; the lane's chunk and its
+  // swizzle are loop invariants.
+  constexpr int RPI = 32 / CH;                 // rows per warp instruction
+  constexpr int ROWS = (L::K_ONLY ? 1 : 2) * KT;  // K rows then V rows
+  const int my_ch = lane % CH;
   auto issue_data = [&](int64_t i, int slot, int stage) {
     if (i >= ntile) return;
     const int64_t u = s_meta[slot * 4 + 0];
     const int jb = s_meta[slot * 4 + 1], cu = s_meta[slot * 4 + 2];
     const uint32_t st = stage_base + stage * L::STAGE;
-    constexpr int HALF = CH / 2;  // chunks per item
-    constexpr int ITEMS = (L::K_ONLY ? 1 : 2) * KT * 2;
-    for (int it = tid; it < ITEMS; it += NTH) {
-      const int half = it & 1;
-      const int r = (it >> 1) % KT;
-      const int isv = (it >> 1) / KT;
+    const __nv_bfloat16* kbase = static_cast<const __nv_bfloat16*>(p.k) + u * p.kv_stride + my_ch * 8;
+    const __nv_bfloat16* vbase = static_cast<const __nv_bfloat16*>(p.v) + u * p.kv_stride + my_ch * 8;
+#pragma unroll 2
+    for (int r0 = warp * RPI; r0 < ROWS; r0 += NT * RPI) {
+      const int rr_all = r0 + lane / CH;          // 0 .. ROWS-1
+      const bool isv = rr_all >= KT;
+      const int r = isv ? rr_all - KT : rr_all;
       const bool ok = jb + r < cu;
       const int pr = ok ? (p.idx ? s_idx[slot * KT + r] : jb + r) : 0;
-      const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(isv ? p.v : p.k) + u * p.kv_stride +
-                                 (int64_t)pr * p.row_stride + half * HALF * 8;
+      const __nv_bfloat16* src = (isv ? vbase : kbase) + (int64_t)pr * p.row_stride;
       const int rr = r & 15;
-      const uint32_t drow = st + (isv * SUB + (r >> 4)) * L::SUBB + rr * L::ROW;
-#pragma unroll
-      for (int c = 0; c < HALF; ++c) {
-        const int ch = half * HALF + c;
-        cp_async_16_zfill(drow + swz(rr, ch), src + c * 8, ok);
-      }
+      const uint32_t dst = st + ((isv ? SUB : 0) + (r >> 4)) * L::SUBB + rr * L::ROW + swz(rr, my_ch);
+      cp_async_16_zfill(dst, src, ok);
     }
   };
 
