@@ -179,30 +179,26 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
   };
 
   // K/V gather of relative tile i (its indices are already in the ring).
-  // A warp instruction covers 32/CH whole rows (512 contiguous bytes at
-  // d = 128) so every request is fully coalesced; the lane's chunk and its
-  // swizzle are loop invariants.
-  constexpr int RPI = 32 / CH;                 // rows per warp instruction
-  constexpr int ROWS = (L::K_ONLY ? 1 : 2) * KT;  // K rows then V rows
-  const int my_ch = lane % CH;
+  // Consecutive lanes take consecutive 16-byte chunks of a row, so a warp
+  // instruction covers 32/CH whole rows (fully coalesced); K and V of the same
+  // (row, chunk) share one index lookup and one address computation.
   auto issue_data = [&](int64_t i, int slot, int stage) {
     if (i >= ntile) return;
     const int64_t u = s_meta[slot * 4 + 0];
     const int jb = s_meta[slot * 4 + 1], cu = s_meta[slot * 4 + 2];
     const uint32_t st = stage_base + stage * L::STAGE;
-    const __nv_bfloat16* kbase = static_cast<const __nv_bfloat16*>(p.k) + u * p.kv_stride + my_ch * 8;
-    const __nv_bfloat16* vbase = static_cast<const __nv_bfloat16*>(p.v) + u * p.kv_stride + my_ch * 8;
-#pragma unroll 2
-    for (int r0 = warp * RPI; r0 < ROWS; r0 += NT * RPI) {
-      const int rr_all = r0 + lane / CH;          // 0 .. ROWS-1
-      const bool isv = rr_all >= KT;
-      const int r = isv ? rr_all - KT : rr_all;
+    const __nv_bfloat16* kg = static_cast<const __nv_bfloat16*>(p.k) + u * p.kv_stride;
+    const __nv_bfloat16* vg = static_cast<const __nv_bfloat16*>(p.v) + u * p.kv_stride;
+    constexpr int CHUNKS = KT * CH;
+#pragma unroll 4
+    for (int c = tid; c < CHUNKS; c += NTH) {
+      const int r = c / CH, ch = c % CH;
       const bool ok = jb + r < cu;
       const int pr = ok ? (p.idx ? s_idx[slot * KT + r] : jb + r) : 0;
-      const __nv_bfloat16* src = (isv ? vbase : kbase) + (int64_t)pr * p.row_stride;
-      const int rr = r & 15;
-      const uint32_t dst = st + ((isv ? SUB : 0) + (r >> 4)) * L::SUBB + rr * L::ROW + swz(rr, my_ch);
-      cp_async_16_zfill(dst, src, ok);
+      const int64_t off = (int64_t)pr * p.row_stride + ch * 8;
+      const uint32_t sk = st + (r >> 4) * L::SUBB + (r & 15) * L::ROW + swz(r & 15, ch);
+      cp_async_16_zfill(sk, kg + off, ok);
+      if constexpr (MODE == MODE_DECODE) cp_async_16_zfill(sk + SUB * L::SUBB, vg + off, ok);
     }
   };
 
@@ -547,8 +543,8 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
 
 template <int D, int NT, int MODE>
 struct GCfg {
-  static constexpr int SUB = MODE == MODE_DECODE ? (D == 64 ? 2 : 1) : (D == 64 ? 4 : 2);
-  static constexpr int STAGES = 4;
+  static constexpr int SUB = MODE == MODE_DECODE ? 2 : (D == 64 ? 4 : 2);
+  static constexpr int STAGES = MODE == MODE_DECODE && D == 128 ? 3 : 4;
   using L = GL<D, NT, MODE, SUB, STAGES>;
 };
 
