@@ -9,15 +9,21 @@
 //    (M = GQA group x (gamma+1) rows; M = 20 -> 3 warps).  All warps consume
 //    the SAME gathered K/V tile, each for its own 8 query rows, so the tile is
 //    fetched once, no math is duplicated, and a warp carries only its rows'
-//    accumulators (32 fp32 registers at d = 128).  That keeps registers low
-//    enough for 5+ CTAs (15+ warps) per SM — the latency hiding a 256-byte
-//    random-row gather needs.
+//    accumulators (32 fp32 registers at d = 128) and its Q fragments (16
+//    registers).  That keeps registers low enough for 4+ CTAs (12+ warps) per
+//    SM — the latency hiding a 256-byte random-row gather needs.
 //  * One cp.async pipeline per CTA, STAGES deep, continuous across unit
 //    boundaries: index slices are prefetched STAGES tiles ahead into a ring,
-//    K/V rows (16-byte cp.async, XOR-swizzled) STAGES-1 tiles ahead of the
+//    K/V rows (16-byte cp.async into padded rows) STAGES-1 tiles ahead of the
 //    math, one CTA barrier per tile.  Entering a new unit flushes each warp's
-//    softmax state and reloads Q; units spanning several CTAs are merged by the
-//    last CTA to arrive (per-unit counter), in CTA order (deterministic).
+//    softmax state and reloads its Q fragments; units spanning several CTAs are
+//    merged by the last CTA to arrive (per-unit counter), in CTA order
+//    (deterministic).
+//  * Instruction economy: rows are padded to 2d+16 bytes (conflict-free
+//    ldmatrix without an XOR swizzle), so every ldmatrix / cp.async address is
+//    a per-lane constant plus a compile-time offset; tiles fully inside the
+//    committed prefix skip per-element masking; the O rescale is skipped when
+//    no row's running max moved.
 //
 // (A warp-specialised variant — one producer warp issuing one cp.async.bulk
 // per gathered row into mbarrier rings — was measured 3-4x slower: 256-byte
@@ -39,20 +45,19 @@ struct GL {
   static constexpr int KT = KEY_TILE * SUB;
   static constexpr int MP = 8 * NT;
   static constexpr int CH = D / 8;
-  static constexpr int ROW = D * 2;
-  static constexpr int SUBB = KEY_TILE * ROW;  // one 16-key K (or V) block
-  static constexpr int STAGE = (K_ONLY ? 1 : 2) * SUB * SUBB;
+  static constexpr int PITCH = D * 2 + 16;        // padded row: ldmatrix conflict-free
+  static constexpr int SUBB = KEY_TILE * PITCH;   // one 16-key K (or V) block
+  static constexpr int KV = KT * PITCH;           // K block -> V block
+  static constexpr int STAGE = (K_ONLY ? 1 : 2) * KV;
   static constexpr int RING = 2 * STAGES;
-  static constexpr int Q_BYTES = MP * ROW;
   static constexpr int IDX_BYTES = RING * KT * 4;
   static constexpr int META_BYTES = RING * 16;
   static constexpr int PROB = MODE == MODE_PROBS ? KT * MP * 4 : 0;
   static constexpr int MERGE = MP * 2 * 4;
-  static constexpr int SMEM = Q_BYTES + STAGES * STAGE + 2 * IDX_BYTES + META_BYTES + PROB + MERGE + 16;
+  static constexpr int SMEM = STAGES * STAGE + 2 * IDX_BYTES + META_BYTES + PROB + MERGE + 16;
   static constexpr int THREADS = NT * 32;
+  static constexpr int GROWS = THREADS / CH;      // rows per gather pass
 };
-
-__device__ __forceinline__ uint32_t swz(int row, int chunk) { return (uint32_t)((chunk ^ (row & 7)) << 4); }
 
 __device__ __forceinline__ void cp_async_4_zfill(uint32_t dst, const void* src, bool valid) {
   int sz = valid ? 4 : 0;
@@ -69,7 +74,7 @@ __device__ __forceinline__ int owner_of(int64_t t, int64_t T, int W) { return (i
 template <int D, int NT, int MODE, int SUB, int STAGES>
 __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p) {
   using L = GL<D, NT, MODE, SUB, STAGES>;
-  constexpr int KT = L::KT, MP = L::MP, CH = L::CH, NTH = L::THREADS;
+  constexpr int KT = L::KT, MP = L::MP, CH = L::CH, NTH = L::THREADS, PITCH = L::PITCH;
   extern __shared__ __align__(128) uint8_t smem[];
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -77,15 +82,13 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
   const int M = p.M;
   const int64_t U = p.units;
 
-  uint8_t* s_q = smem;
-  uint8_t* s_stage = s_q + L::Q_BYTES;
+  uint8_t* s_stage = smem;
   int* s_idx = reinterpret_cast<int*>(s_stage + STAGES * L::STAGE);
   uint32_t* s_mem = reinterpret_cast<uint32_t*>(s_idx + L::RING * KT);
   int* s_meta = reinterpret_cast<int*>(s_mem + L::RING * KT);
   float* s_prob = reinterpret_cast<float*>(s_meta + L::RING * 4);
   float* s_merge = s_prob + (L::PROB / 4);
   int* s_flag = reinterpret_cast<int*>(s_merge + L::MERGE / 4);
-  const uint32_t q_base = smem_u32(s_q);
   const uint32_t stage_base = smem_u32(s_stage);
   const uint32_t idx_base = smem_u32(s_idx);
   const uint32_t mem_base = smem_u32(s_mem);
@@ -114,7 +117,7 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
   if (w >= W) return;
   const int64_t s_w = (int64_t)w * T / W;
   const int64_t e_w = (int64_t)(w + 1) * T / W;
-  const int64_t ntile = e_w - s_w;
+  const int ntile = (int)(e_w - s_w);
 
   // unit holding tile s_w (warp-cooperative prefix scan over unit tile counts)
   int64_t iu = 0, iP = 0;
@@ -143,9 +146,9 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
   int icnt = p.idx ? p.cnt[iu] : p.n_dense;
   int64_t iPn = iP + (icnt + KT - 1) / KT;
 
-  // index cursor: slice of relative tile i -> ring slot i % RING (+ meta)
-  int idx_slot = 0;  // ring slot of the next issue_idx call (calls are sequential in i)
-  auto issue_idx = [&](int64_t i) {
+  // index cursor: slice of relative tile i -> next ring slot (+ meta)
+  int idx_slot = 0;
+  auto issue_idx = [&](int i) {
     const int slot = idx_slot;
     idx_slot = idx_slot + 1 == L::RING ? 0 : idx_slot + 1;
     if (i >= ntile) return;
@@ -178,27 +181,28 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
     return p.idx ? s_idx[slot * KT + r] : j;
   };
 
-  // K/V gather of relative tile i (its indices are already in the ring).
-  // Consecutive lanes take consecutive 16-byte chunks of a row, so a warp
-  // instruction covers 32/CH whole rows (fully coalesced); K and V of the same
-  // (row, chunk) share one index lookup and one address computation.
-  auto issue_data = [&](int64_t i, int slot, int stage) {
+  // K/V gather: thread -> (chunk g_ch, rows g_r0 + GROWS*j); K and V of a
+  // (row, chunk) share the index lookup and the address
+  const int g_ch = tid % CH, g_r0 = tid / CH;
+  const uint32_t g_dst = (uint32_t)(g_r0 * PITCH + g_ch * 16);
+  auto issue_data = [&](int i, int slot, int stage) {
     if (i >= ntile) return;
     const int64_t u = s_meta[slot * 4 + 0];
     const int jb = s_meta[slot * 4 + 1], cu = s_meta[slot * 4 + 2];
-    const uint32_t st = stage_base + stage * L::STAGE;
-    const __nv_bfloat16* kg = static_cast<const __nv_bfloat16*>(p.k) + u * p.kv_stride;
-    const __nv_bfloat16* vg = static_cast<const __nv_bfloat16*>(p.v) + u * p.kv_stride;
-    constexpr int CHUNKS = KT * CH;
-#pragma unroll 4
-    for (int c = tid; c < CHUNKS; c += NTH) {
-      const int r = c / CH, ch = c % CH;
+    const uint32_t dst0 = stage_base + stage * L::STAGE + g_dst;
+    const __nv_bfloat16* kg = static_cast<const __nv_bfloat16*>(p.k) + u * p.kv_stride + g_ch * 8;
+    const __nv_bfloat16* vg = static_cast<const __nv_bfloat16*>(p.v) + u * p.kv_stride + g_ch * 8;
+    const int* ring = s_idx + slot * KT;
+#pragma unroll
+    for (int j = 0; j < (KT + L::GROWS - 1) / L::GROWS; ++j) {
+      const int r = g_r0 + j * L::GROWS;
+      if (KT % L::GROWS != 0 && r >= KT) break;
       const bool ok = jb + r < cu;
-      const int pr = ok ? (p.idx ? s_idx[slot * KT + r] : jb + r) : 0;
-      const int64_t off = (int64_t)pr * p.row_stride + ch * 8;
-      const uint32_t sk = st + (r >> 4) * L::SUBB + (r & 15) * L::ROW + swz(r & 15, ch);
-      cp_async_16_zfill(sk, kg + off, ok);
-      if constexpr (MODE == MODE_DECODE) cp_async_16_zfill(sk + SUB * L::SUBB, vg + off, ok);
+      const int pr = ok ? (p.idx ? ring[r] : jb + r) : 0;
+      const int64_t off = (int64_t)pr * p.row_stride;
+      const uint32_t dst = dst0 + j * L::GROWS * PITCH;
+      cp_async_16_zfill(dst, kg + off, ok);
+      if constexpr (MODE == MODE_DECODE) cp_async_16_zfill(dst + L::KV, vg + off, ok);
     }
   };
 
@@ -212,7 +216,10 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
   const int causal_shift = p.pos_offset - p.causal_base;
   const bool causal = p.causal_base >= 0;
   const int mi = lane >> 3, ri = lane & 7;
-  uint32_t qf[D / 16][2];  // this warp's Q^T B-fragments, loaded once per unit
+  // per-lane ldmatrix offsets inside a 16-key block (padded rows)
+  const uint32_t offK = (uint32_t)(((mi & 1) * 8 + ri) * PITCH + (mi >> 1) * 16);
+  const uint32_t offV = (uint32_t)(((mi >> 1) * 8 + ri) * PITCH + (mi & 1) * 16);
+  uint32_t qf[D / 16][2];  // this warp's Q^T B-fragments (loaded per unit)
   int64_t cur_u = -1;
   int cur_P = 0, cur_cnt = 0;
 
@@ -228,20 +235,15 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
     }
   };
 
-  // Q of unit u: each warp loads its own 8 rows (only it reads them)
+  // Q^T B-fragments straight from global: lane holds Q[row][k-step cols]
   auto load_q = [&](int64_t u) {
-    const __nv_bfloat16* qg = static_cast<const __nv_bfloat16*>(p.q) + u * (int64_t)M * D;
-    for (int c = lane; c < 8 * CH; c += 32) {
-      const int r = warp * 8 + c / CH, ch = c % CH;
-      uint4 val = make_uint4(0, 0, 0, 0);
-      if (r < M) val = *reinterpret_cast<const uint4*>(qg + (int64_t)r * D + ch * 8);
-      *reinterpret_cast<uint4*>(s_q + r * L::ROW + swz(r, ch)) = val;
-    }
-    __syncwarp();
+    const int row = warp * 8 + (lane >> 2);
+    const uint32_t* qg = reinterpret_cast<const uint32_t*>(static_cast<const __nv_bfloat16*>(p.q) +
+                                                           (u * M + row) * (int64_t)D) + (lane & 3);
 #pragma unroll
-    for (int kk = 0; kk < D / 16; kk += 2) {
-      const int row = warp * 8 + ri;
-      ldmatrix_x4(qf[kk][0], qf[kk][1], qf[kk + 1][0], qf[kk + 1][1], q_base + row * L::ROW + swz(row, 2 * kk + mi));
+    for (int kk = 0; kk < D / 16; ++kk) {
+      qf[kk][0] = row < M ? __ldg(qg + kk * 8) : 0u;
+      qf[kk][1] = row < M ? __ldg(qg + kk * 8 + 4) : 0u;
     }
     if constexpr (MODE == MODE_PROBS) {
 #pragma unroll
@@ -250,7 +252,6 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
         lse2[c] = r < M ? p.lse_in[u * M + r] * LOG2E : 0.f;
       }
     }
-    __syncwarp();
   };
 
   // finish unit u for this CTA: final rows, or partial + (last CTA) merge
@@ -373,9 +374,9 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
     cp_async_commit();
   }
 
-  int slot = 0, stage = 0;                              // of tile i
-  int f_slot = STAGES - 1, f_stage = STAGES - 1;        // of tile i + STAGES - 1
-  for (int64_t i = 0; i < ntile; ++i) {
+  int slot = 0, stage = 0;                        // of tile i
+  int f_slot = STAGES - 1, f_stage = STAGES - 1;  // of tile i + STAGES - 1
+  for (int i = 0; i < ntile; ++i) {
     cp_async_wait<STAGES - 2>();  // this thread's gathers of tile i landed (and idx of tile i+STAGES-1)
     __syncthreads();              // ... everyone's; everyone is done with tile i-1
     issue_data(i + STAGES - 1, f_slot, f_stage);  // refill the stage tile i-1 used
@@ -404,16 +405,15 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
 #pragma unroll
     for (int sub = 0; sub < SUB; ++sub) {
       const bool live = j0 + sub * KEY_TILE < cur_cnt;
-      const uint32_t sk = sk0 + sub * L::SUBB;
+      const uint32_t ak = sk0 + sub * L::SUBB + offK;
 #pragma unroll
       for (int c = 0; c < 4; ++c) s[sub][c] = 0.f;
       if (live) {
 #pragma unroll
         for (int kk = 0; kk < D / 16; kk += 2) {
           uint32_t a0[4], a1[4];
-          const int key = (mi & 1) * 8 + ri;
-          ldmatrix_x4(a0[0], a0[1], a0[2], a0[3], sk + key * L::ROW + swz(key, 2 * kk + (mi >> 1)));
-          ldmatrix_x4(a1[0], a1[1], a1[2], a1[3], sk + key * L::ROW + swz(key, 2 * kk + 2 + (mi >> 1)));
+          ldmatrix_x4(a0[0], a0[1], a0[2], a0[3], ak + kk * 32);
+          ldmatrix_x4(a1[0], a1[1], a1[2], a1[3], ak + kk * 32 + 32);
           mma_bf16_16816(s[sub], a0, qf[kk]);
           mma_bf16_16816(s[sub], a1, qf[kk + 1]);
         }
@@ -521,14 +521,13 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
 #pragma unroll
         for (int sub = 0; sub < SUB; ++sub) {
           if (j0 + sub * KEY_TILE >= cur_cnt) break;
-          const uint32_t sv = sk0 + (SUB + sub) * L::SUBB;
+          const uint32_t av = sk0 + L::KV + sub * L::SUBB + offV;
           const uint32_t b[2] = {movmatrix_trans(pack_bf16(pv[sub][0], pv[sub][1])),
                                  movmatrix_trans(pack_bf16(pv[sub][2], pv[sub][3]))};
 #pragma unroll
           for (int mt = 0; mt < D / 16; ++mt) {
             uint32_t a[4];
-            const int key = (mi >> 1) * 8 + ri;
-            ldmatrix_x4_trans(a[0], a[1], a[2], a[3], sv + key * L::ROW + swz(key, 2 * mt + (mi & 1)));
+            ldmatrix_x4_trans(a[0], a[1], a[2], a[3], av + mt * 32);
             mma_bf16_16816(o[mt], a, b);
           }
         }
