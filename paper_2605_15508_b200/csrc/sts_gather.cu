@@ -32,6 +32,8 @@
 // Modes: DECODE (K+V, online softmax, O = P.V), LSE (K only, draft-row
 // log-sum-exp), PROBS (K only, probabilities from a known LSE, per row or
 // summed over the speculative rows of each head).
+#include <stdlib.h>
+
 #include "sts_decode.cuh"
 
 namespace sts {
@@ -547,12 +549,11 @@ struct GCfg {
   using L = GL<D, NT, MODE, SUB, STAGES>;
 };
 
-template <int D, int NT, int MODE>
-int launch_gather(DecodeParams& p, cudaStream_t st) {
-  using C = GCfg<D, NT, MODE>;
-  using L = typename C::L;
+template <int D, int NT, int MODE, int SUB, int STAGES>
+int launch_cfg(DecodeParams& p, cudaStream_t st) {
+  using L = GL<D, NT, MODE, SUB, STAGES>;
   static_assert(L::SMEM <= 227 * 1024, "gather kernel shared memory");
-  auto kern = gather_kernel<D, NT, MODE, C::SUB, C::STAGES>;
+  auto kern = gather_kernel<D, NT, MODE, SUB, STAGES>;
   STS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM));
   int per_sm = 0;
   STS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::THREADS, L::SMEM));
@@ -560,6 +561,32 @@ int launch_gather(DecodeParams& p, cudaStream_t st) {
   kern<<<num_sms() * per_sm, L::THREADS, L::SMEM, st>>>(p);
   STS_LAUNCH_CHECK();
   return STS_OK;
+}
+
+// pipeline shape of the d=128, M<=24 decode (the headline configuration):
+// STS_GATHER_CFG = 0: 32-key stages x3 (default), 1: 32 x4, 2: 16 x4, 3: 16 x6
+int decode_cfg() {
+  static int cfg = -1;
+  if (cfg < 0) {
+    const char* e = getenv("STS_GATHER_CFG");
+    cfg = e ? atoi(e) : 0;
+    if (cfg < 0 || cfg > 3) cfg = 0;
+  }
+  return cfg;
+}
+
+template <int D, int NT, int MODE>
+int launch_gather(DecodeParams& p, cudaStream_t st) {
+  if constexpr (D == 128 && NT == 3 && MODE == MODE_DECODE) {
+    switch (decode_cfg()) {
+      case 1: return launch_cfg<D, NT, MODE, 2, 4>(p, st);
+      case 2: return launch_cfg<D, NT, MODE, 1, 4>(p, st);
+      case 3: return launch_cfg<D, NT, MODE, 1, 6>(p, st);
+      default: break;
+    }
+  }
+  using C = GCfg<D, NT, MODE>;
+  return launch_cfg<D, NT, MODE, C::SUB, C::STAGES>(p, st);
 }
 
 template <int D, int MODE>
