@@ -411,14 +411,18 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
 #pragma unroll
       for (int c = 0; c < 4; ++c) s[sub][c] = 0.f;
       if (live) {
+        // two independent accumulators halve the MMA dependency chain
+        float s1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int kk = 0; kk < D / 16; kk += 2) {
           uint32_t a0[4], a1[4];
           ldmatrix_x4(a0[0], a0[1], a0[2], a0[3], ak + kk * 32);
           ldmatrix_x4(a1[0], a1[1], a1[2], a1[3], ak + kk * 32 + 32);
           mma_bf16_16816(s[sub], a0, qf[kk]);
-          mma_bf16_16816(s[sub], a1, qf[kk + 1]);
+          mma_bf16_16816(s1, a1, qf[kk + 1]);
         }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) s[sub][c] += s1[c];
       }
       if (simple) {
         okA[sub][0] = okA[sub][1] = okB[sub][0] = okB[sub][1] = true;
@@ -564,7 +568,7 @@ int launch_cfg(DecodeParams& p, cudaStream_t st) {
 }
 
 // pipeline shape of the d=128, M<=24 decode (the headline configuration):
-// STS_GATHER_CFG = 0: 32-key stages x3 (default), 1: 32 x4, 2: 16 x4, 3: 16 x6
+// STS_GATHER_CFG = 0: 32-key stages x3 (default), 1: 32 x2, 2: 16 x4, 3: 64 x2
 int decode_cfg() {
   static int cfg = -1;
   if (cfg < 0) {
@@ -579,9 +583,9 @@ template <int D, int NT, int MODE>
 int launch_gather(DecodeParams& p, cudaStream_t st) {
   if constexpr (D == 128 && NT == 3 && MODE == MODE_DECODE) {
     switch (decode_cfg()) {
-      case 1: return launch_cfg<D, NT, MODE, 2, 4>(p, st);
+      case 1: return launch_cfg<D, NT, MODE, 2, 2>(p, st);
       case 2: return launch_cfg<D, NT, MODE, 1, 4>(p, st);
-      case 3: return launch_cfg<D, NT, MODE, 1, 6>(p, st);
+      case 3: return launch_cfg<D, NT, MODE, 4, 2>(p, st);
       default: break;
     }
   }
