@@ -549,7 +549,8 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
 template <int D, int NT, int MODE>
 struct GCfg {
   static constexpr int SUB = MODE == MODE_DECODE ? 2 : (D == 64 ? 4 : 2);
-  static constexpr int STAGES = MODE == MODE_DECODE && D == 128 ? 3 : 4;
+  // measured on B200 (d=128, M=20): 32-key stages x2 (6 CTAs/SM) > x3 (4/SM) > 16 x4
+  static constexpr int STAGES = MODE == MODE_DECODE && D == 128 ? 2 : 4;
   using L = GL<D, NT, MODE, SUB, STAGES>;
 };
 
@@ -568,7 +569,7 @@ int launch_cfg(DecodeParams& p, cudaStream_t st) {
 }
 
 // pipeline shape of the d=128, M<=24 decode (the headline configuration):
-// STS_GATHER_CFG = 0: 32-key stages x3 (default), 1: 32 x2, 2: 16 x4, 3: 64 x2
+// STS_GATHER_CFG = 0: 32-key stages x2 (default), 1: 32 x3, 2: 16 x4, 3: 64 x2
 int decode_cfg() {
   static int cfg = -1;
   if (cfg < 0) {
@@ -583,7 +584,7 @@ template <int D, int NT, int MODE>
 int launch_gather(DecodeParams& p, cudaStream_t st) {
   if constexpr (D == 128 && NT == 3 && MODE == MODE_DECODE) {
     switch (decode_cfg()) {
-      case 1: return launch_cfg<D, NT, MODE, 2, 2>(p, st);
+      case 1: return launch_cfg<D, NT, MODE, 2, 3>(p, st);
       case 2: return launch_cfg<D, NT, MODE, 1, 4>(p, st);
       case 3: return launch_cfg<D, NT, MODE, 4, 2>(p, st);
       default: break;

@@ -131,17 +131,30 @@ __device__ __forceinline__ int block_scan_int(int v, int* warp_tot, int& total) 
 // After the first digit the surviving keys are compacted into `cand` (when
 // they fit) so later digits only touch the candidates.
 template <typename K>
-__device__ void radix_select(const K* keys, int n, int k, SelShared& sh, K* cand, int cand_cap, K& T,
-                             int& need, int& ties) {
+__device__ void radix_select(const K* keys, int n, int k, K key_or, K key_and, SelShared& sh, K* cand, int cand_cap,
+                             K& T, int& need, int& ties) {
   constexpr int KBITS = sizeof(K) * 8;
-  K prefix = 0, pmask = 0;
+  const K diff = key_or ^ key_and;  // bits that vary across the row
+  if (diff == 0) {                  // every key identical: all ties
+    T = key_and;
+    need = k;
+    ties = n;
+    return;
+  }
+  const int h = KBITS - 1 - (sizeof(K) == 8 ? __clzll((long long)diff) : __clz((int)diff));
+  // bits above h are common to all keys: start the first digit at bit h so the
+  // histogram spreads over the bits that actually discriminate (probability
+  // rows share sign + most exponent bits; a fixed top digit piles them into a
+  // handful of bins and serialises the shared-memory atomics)
+  K pmask = h + 1 >= KBITS ? (K)0 : ~(((K)1 << (h + 1)) - 1);
+  K prefix = key_and & pmask;
   int krem = k;
   const K* src = keys;
   int len = n;
   bool compacted = false;
-  for (int shift = KBITS - DIGIT_BITS;; shift -= DIGIT_BITS) {
-    const int s = shift < 0 ? 0 : shift;
-    const int width = shift < 0 ? DIGIT_BITS + shift : DIGIT_BITS;
+  for (int top = h;; top -= DIGIT_BITS) {
+    const int s = top - DIGIT_BITS + 1 < 0 ? 0 : top - DIGIT_BITS + 1;
+    const int width = top - s + 1;
     const int nb = 1 << width;
     for (int i = threadIdx.x; i < nb; i += SEL_THREADS) sh.hist[i] = 0;
     __syncthreads();
@@ -207,6 +220,32 @@ __device__ void radix_select(const K* keys, int n, int k, SelShared& sh, K* cand
   }
   T = prefix;
   need = krem;
+}
+
+// block-wide OR / AND of per-thread partials (used to locate varying key bits)
+template <typename K>
+__device__ __forceinline__ void block_or_and(K& v_or, K& v_and, SelShared& sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v_or |= __shfl_xor_sync(0xffffffffu, v_or, o);
+    v_and &= __shfl_xor_sync(0xffffffffu, v_and, o);
+  }
+  K* red = reinterpret_cast<K*>(sh.cand);  // scratch (cand is free at this point)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    red[warp] = v_or;
+    red[SEL_WARPS + warp] = v_and;
+  }
+  __syncthreads();
+  K a = (K)0, b = ~(K)0;
+#pragma unroll 8
+  for (int w = 0; w < SEL_WARPS; ++w) {
+    a |= red[w];
+    b &= red[SEL_WARPS + w];
+  }
+  __syncthreads();
+  v_or = a;
+  v_and = b;
 }
 
 __device__ __forceinline__ bool is_extra(const SelectParams& p, int j, int n) {
@@ -371,11 +410,18 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(SelectParams p) 
       count = n;
     } else if (p.page_size == 1) {
       uint32_t* keys = reinterpret_cast<uint32_t*>(buf);
-      for_row_values(p, srcs, n, [&](int j, float v) { keys[j] = f32_key(v); });
-      __syncthreads();
+      uint32_t k_or = 0u, k_and = 0xffffffffu;
+      for_row_values(p, srcs, n, [&](int j, float v) {
+        const uint32_t key = f32_key(v);
+        keys[j] = key;
+        k_or |= key;
+        k_and &= key;
+      });
+      block_or_and(k_or, k_and, sh);  // (its barrier also publishes keys[])
       uint32_t T;
       int need, ties;
-      radix_select<uint32_t>(keys, n, b, sh, reinterpret_cast<uint32_t*>(sh.cand), CAND_BYTES / 4, T, need, ties);
+      radix_select<uint32_t>(keys, n, b, k_or, k_and, sh, reinterpret_cast<uint32_t*>(sh.cand), CAND_BYTES / 4, T,
+                             need, ties);
       count = emit_sorted(p, sh, out, n, [&](int j) { return (uint64_t)keys[j]; }, (uint64_t)T, need, extra, 0,
                           false, nullptr, need == ties);
     } else {
@@ -390,18 +436,22 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(SelectParams p) 
       } else {
         for_row_values(p, srcs, n, [&](int j, float v) { vals[j] = v; });
         __syncthreads();
+        uint64_t p_or = 0ull, p_and = ~0ull;
         for (int pg = threadIdx.x; pg < P; pg += SEL_THREADS) {
           const int start = pg * ps;
           const int len = min(ps, n - start);
           // np.add.reduceat segment: x[start] + pairwise(x[start+1 : start+len])
           const double x0 = (double)vals[start];
-          pkeys[pg] = f64_key(len == 1 ? x0 : __dadd_rn(x0, pairwise_vals(vals, start + 1, len - 1)));
+          const uint64_t key = f64_key(len == 1 ? x0 : __dadd_rn(x0, pairwise_vals(vals, start + 1, len - 1)));
+          pkeys[pg] = key;
+          p_or |= key;
+          p_and &= key;
         }
-        __syncthreads();
+        block_or_and(p_or, p_and, sh);
         uint64_t T;
         int need, ties;
-        radix_select<uint64_t>(pkeys, P, kp, sh, reinterpret_cast<uint64_t*>(sh.cand), CAND_BYTES / 8, T, need,
-                               ties);
+        radix_select<uint64_t>(pkeys, P, kp, p_or, p_and, sh, reinterpret_cast<uint64_t*>(sh.cand), CAND_BYTES / 8, T,
+                               need, ties);
         emit_sorted(p, sh, out, P, [&](int j) { return pkeys[j]; }, T, need, [](int) { return false; }, 0, true,
                     pbits, need == ties);
       }
