@@ -158,9 +158,25 @@ __device__ void radix_select(const K* keys, int n, int k, K key_or, K key_and, S
     const int nb = 1 << width;
     for (int i = threadIdx.x; i < nb; i += SEL_THREADS) sh.hist[i] = 0;
     __syncthreads();
-    for (int j = threadIdx.x; j < len; j += SEL_THREADS) {
-      const K key = src[j];
-      if ((key & pmask) == prefix) atomicAdd(&sh.hist[(uint32_t)((key >> s) & (K)(nb - 1))], 1u);
+    if constexpr (sizeof(K) == 4) {
+      // 4 keys per thread per step (128-bit shared loads)
+      const int n4 = ((reinterpret_cast<uintptr_t>(src) & 15) == 0) ? len / 4 : 0;
+      for (int v = threadIdx.x; v < n4; v += SEL_THREADS) {
+        const uint4 q = reinterpret_cast<const uint4*>(src)[v];
+        const uint32_t kk[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (((K)kk[e] & pmask) == prefix) atomicAdd(&sh.hist[(uint32_t)(((K)kk[e] >> s) & (K)(nb - 1))], 1u);
+      }
+      for (int j = 4 * n4 + threadIdx.x; j < len; j += SEL_THREADS) {
+        const K key = src[j];
+        if ((key & pmask) == prefix) atomicAdd(&sh.hist[(uint32_t)((key >> s) & (K)(nb - 1))], 1u);
+      }
+    } else {
+      for (int j = threadIdx.x; j < len; j += SEL_THREADS) {
+        const K key = src[j];
+        if ((key & pmask) == prefix) atomicAdd(&sh.hist[(uint32_t)((key >> s) & (K)(nb - 1))], 1u);
+      }
     }
     __syncthreads();
     // descending scan over bins: thread t owns bins nb-1-4t .. nb-4-4t
@@ -198,7 +214,7 @@ __device__ void radix_select(const K* keys, int n, int k, K key_or, K key_and, S
       ties = inbin;
       break;
     }
-    if (!compacted && inbin <= cand_cap && inbin < len) {
+    if (sizeof(K) == 8 && !compacted && inbin <= cand_cap && inbin < len) {
       if (threadIdx.x == 0) sh.bcast[3] = 0;
       __syncthreads();
       const int lane = threadIdx.x & 31;
@@ -374,6 +390,65 @@ __device__ __forceinline__ int emit_sorted(const SelectParams& p, SelShared& sh,
   return run_sel;
 }
 
+// Token-mode emit: 8 keys per thread per step (two 128-bit shared loads),
+// one block scan per 8192 keys when every tie at T is taken, two otherwise.
+__device__ int emit_tokens(const SelectParams& p, SelShared& sh, int32_t* out, const uint32_t* keys, int n,
+                           uint32_t T, int need, bool all_ties) {
+  const int lo_extra = p.recent_window > 0 ? n - p.recent_window : n;  // [lo_extra, n) always kept
+  const bool cur = (p.flags & STS_SEL_CURRENT) != 0, sink = (p.flags & STS_SEL_SINK) != 0;
+  int run_sel = 0, run_tie = 0;
+  for (int base = 0; base < n; base += 8 * SEL_THREADS) {
+    const int j0 = base + 8 * threadIdx.x;
+    uint32_t k8[8];
+    if (j0 + 8 <= n) {
+      const uint4 a = reinterpret_cast<const uint4*>(keys + j0)[0];
+      const uint4 b = reinterpret_cast<const uint4*>(keys + j0)[1];
+      k8[0] = a.x; k8[1] = a.y; k8[2] = a.z; k8[3] = a.w;
+      k8[4] = b.x; k8[5] = b.y; k8[6] = b.z; k8[7] = b.w;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) k8[q] = j0 + q < n ? keys[j0 + q] : 0u;
+    }
+    uint32_t gt = 0, eq = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const bool valid = j0 + q < n;
+      gt |= (valid && k8[q] > T) ? (1u << q) : 0u;
+      eq |= (valid && k8[q] == T) ? (1u << q) : 0u;
+    }
+    uint32_t sel = gt;
+    if (all_ties) {
+      sel |= eq;
+    } else {
+      int tie_tot;
+      const int tie_ex = block_scan_int(__popc(eq), sh.warp_tot, tie_tot);
+      int rank = run_tie + tie_ex;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if ((eq >> q) & 1u) {
+          if (rank < need) sel |= 1u << q;
+          ++rank;
+        }
+      run_tie += tie_tot;
+    }
+    // always-include extras (current, sink, recent window): only near the ends
+    if (j0 + 7 >= lo_extra || (sink && j0 == 0) || (cur && j0 + 7 >= n - 1)) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int j = j0 + q;
+        if (j < n && (j >= lo_extra || (sink && j == 0) || (cur && j == n - 1))) sel |= 1u << q;
+      }
+    }
+    int sel_tot;
+    int pos = run_sel + block_scan_int(__popc(sel), sh.warp_tot, sel_tot);
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if ((sel >> q) & 1u) write_idx(p, out, pos++, j0 + q);
+    run_sel += sel_tot;
+  }
+  return run_sel;
+}
+
 __global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(SelectParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   SelShared& sh = *reinterpret_cast<SelShared*>(smem_raw);
@@ -422,9 +497,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(SelectParams p) 
       int need, ties;
       radix_select<uint32_t>(keys, n, b, k_or, k_and, sh, reinterpret_cast<uint32_t*>(sh.cand), CAND_BYTES / 4, T,
                              need, ties);
-      count = emit_sorted(p, sh, out, n, [&](int j) { return (uint64_t)keys[j]; }, (uint64_t)T, need, extra, 0,
-                          false, nullptr, need == ties);
-    } else {
+      count = emit_tokens(p, sh, out, keys, n, T, need, need == ties);    } else {
       const int ps = p.page_size;
       const int P = (n + ps - 1) / ps;
       const int kp = (b + ps - 1) / ps;
