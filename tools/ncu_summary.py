@@ -11,7 +11,7 @@ import json
 import subprocess
 
 METRICS = {
-    "dur_us": ("gpu__time_duration.sum", 1e-3),
+    "dur_us": ("gpu__time_duration.sum", 1),
     "dram_read_MB": ("dram__bytes_read.sum", 1e-6),
     "dram_write_MB": ("dram__bytes_write.sum", 1e-6),
     "dram_pct": ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", 1),
