@@ -41,7 +41,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="auto",
+                    help="auto = c2 on one GPU, c4 (1M context, KV sharded by sequence) when --gpus > 1")
     ap.add_argument("--mode", default="S", choices=["S", "R"])
     ap.add_argument("--sparsity", type=float, default=0.9)
     ap.add_argument("--page-size", type=int, default=1)
@@ -174,6 +175,9 @@ def run_reference(args):
     budget = round(1.0 - args.sparsity, 10)
     k_sel = max(1, math.ceil(budget * (shape.context + 1))) + shape.rows
     workers = os.cpu_count() or 1
+    # each call holds K/V in fp32 + their fp64 copies (src/sparsity.py:167-168): ~24 B per element
+    per_call_bytes = 24 * shape.n_kv * shape.head_dim
+    workers = max(1, min(workers, int(8e9 // per_call_bytes)))
     vals = []
     for i in range(args.warmup + args.steps):
         v, calls, per_call = cpu_reference_sample(shape, k_sel, max(2.0, args.cpu_seconds / max(args.steps, 1)),
@@ -204,8 +208,12 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.config == "auto":
+        args.config = "c2" if world == 1 else "c4"
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "c4" or world > 1:
+        return run_sharded(args, world, rank, local)
 
     import numpy as np
     import torch
@@ -360,6 +368,142 @@ def main():
         "gpu_launches": int(launches),
         "clocks": clocks.summary(),
         "wall_s_timed_loop": round(wall, 3),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# sequence-sharded path (config c4: 1M context, KV split by sequence over ranks)
+# ---------------------------------------------------------------------------
+
+def run_sharded(args, world, rank, local):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_15508_b200 import SparsityConfig, _lib, sharded
+    from paper_2605_15508_b200.verify import algorithmic_bytes, config_shape, random_mapping_table
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+        drive = lambda proto: sharded.run(proto)  # noqa: E731
+    else:
+        drive = sharded.run_single
+    _lib.load()
+    shape = config_shape(args.config)
+    budget = round(1.0 - args.sparsity, 10)
+    cfg = SparsityConfig(budget=budget, page_size=args.page_size)
+    table = random_mapping_table(shape, seed=5)
+    step = sharded.ShardedVerifyStep(shape, cfg, table, rank, world, device=dev, align=max(64, args.page_size))
+    dq, dk, tq, tk, tv = sharded.local_synthetic_inputs(shape, step.bounds, rank, dev, seed=0)
+    dqv, dkv, q, k, v = step.local_views(dq, dk, tq, tk, tv, full=False)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    st = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        drive(step.step(dqv, dkv, q, k, v))
+        drive(step.attend_dense(q, k, v))
+    barrier()
+    assert step.status.item() == 0, f"device status {step.status.item()}"
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    t_cap, t_sel, t_att, t_den = [], [], [], []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            flush.zero_()
+            barrier()
+            e = [ev() for _ in range(3)]
+            e[0].record(st)
+            drive(step.capture(dqv, dkv))
+            e[1].record(st)
+            drive(step.build_masks())
+            e[2].record(st)
+            flush.zero_()
+            barrier()
+            e3, e4 = ev(), ev()
+            e3.record(st)
+            drive(step.attend(q, k, v))
+            e4.record(st)
+            flush.zero_()
+            barrier()
+            e5, e6 = ev(), ev()
+            e5.record(st)
+            drive(step.attend_dense(q, k, v))
+            e6.record(st)
+            torch.cuda.synchronize()
+            t_cap.append(e[0].elapsed_time(e[1]) * 1e3)
+            t_sel.append(e[1].elapsed_time(e[2]) * 1e3)
+            t_att.append(e3.elapsed_time(e4) * 1e3)
+            t_den.append(e5.elapsed_time(e6) * 1e3)
+    # end to end through the public API: host Q in, host O out (every rank)
+    h_tq, h_dq = tq.cpu().pin_memory(), dq.cpu().pin_memory()
+    h_out = torch.empty(step.out.shape, dtype=step.out.dtype).pin_memory()
+    d_tq, d_dq = torch.empty_like(tq), torch.empty_like(dq)
+    dqe, _, qe, _, _ = step.local_views(d_dq, dk, d_tq, tk, tv, full=False)
+    t_e2e = []
+    for i in range(args.warmup + args.steps):
+        flush.zero_()
+        barrier()
+        e0, e1 = ev(), ev()
+        e0.record(st)
+        d_tq.copy_(h_tq, non_blocking=True)
+        d_dq.copy_(h_dq, non_blocking=True)
+        out, _ = drive(step.step(dqe, dkv, qe, k, v))
+        h_out.copy_(out, non_blocking=True)
+        e1.record(st)
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            t_e2e.append(e0.elapsed_time(e1) * 1e3)
+
+    mean = lambda x: float(sum(x) / len(x))  # noqa: E731
+    stats = torch.tensor([mean(t_att), mean(t_den), mean(t_cap), mean(t_sel), mean(t_e2e)], device=dev)
+    cnt_local = torch.tensor([float(step.cnt.float().sum().item())], device=dev)
+    if world > 1:
+        dist.all_reduce(stats, op=dist.ReduceOp.MAX)
+        dist.all_reduce(cnt_local, op=dist.ReduceOp.SUM)
+    att, den, cap, sel, e2e = stats.tolist()
+    keys_per_unit = cnt_local.item() / shape.target_units
+    nbytes = algorithmic_bytes(shape, keys_per_unit)
+    peak, peak_src = peaks()
+    achieved = nbytes / (att * 1e-6) / 1e9 / world  # per GPU
+    h2d = tq.numel() * tq.element_size() + dq.numel() * dq.element_size()
+    d2h = step.out.numel() * step.out.element_size()
+    rounds = step.selector.rounds
+    line = {
+        "metric": METRIC, "value": round(att, 2), "unit": "us", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(att / 1e3, 5), "higher_is_better": False,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded N(0,1) bf16 Q/K/V per shard, random head mapping)",
+        "config": {"workload": f"{args.config}: Llama-3.1-8B target / Llama-3.2-1B draft shapes, {shape.context} "
+                               f"context, KV sharded by sequence over {world} GPU(s), batch {shape.batch}, gamma "
+                               f"{shape.gamma}, sparsity {args.sparsity}, mode S, page_size {args.page_size}",
+                   "context": shape.context, "batch": shape.batch, "gamma": shape.gamma, "mode": "S",
+                   "page_size": args.page_size, "shard_positions": step.n_loc,
+                   "keys_per_kv_head": round(keys_per_unit, 1), "l2": "flushed (256 MB write) before every timed stage",
+                   "parallelism": f"sequence-sharded x{world} (NCCL histogram allreduce + LSE merge)"},
+        "dense_us": round(den, 2), "speedup_vs_dense": round(den / att, 3),
+        "mask_build_us": {"draft_capture": round(cap, 2), "select": round(sel, 2)},
+        "sts_step_us": round(cap + sel + att, 2), "step_speedup_vs_dense": round(den / (cap + sel + att), 3),
+        "hbm_gbs_per_gpu": round(achieved, 1),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "kernel": "sts_sparse_decode + all-gather + sts_lse_merge (per GPU)",
+                     "algorithmic_bytes_per_launch": int(nbytes / world), "peak_source": peak_src},
+        "collectives_per_step": {"capture": 1, "select": rounds + 1, "attend": 2},
+        "cpu_baseline": None,
+        "e2e": {"value": round(e2e, 2), "unit": "us", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "what": "ShardedVerifyStep.step per rank: H2D target+draft Q, capture, select, attention, merge, D2H"},
+        "gpu_launches": None,
+        "clocks": clocks.summary(),
     }
     if rank == 0:
         print(json.dumps(line), flush=True)

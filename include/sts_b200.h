@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define STS_ABI_VERSION 1
+#define STS_ABI_VERSION 2
 
 #define STS_OK 0
 #define STS_ERR_INPUT 1
@@ -114,7 +114,9 @@ STS_API int sts_page_aggregate(const float* scores_dev, int64_t ld, int64_t rows
  *   0..n_dense-1).  Row r attends key p iff
  *     (causal_base < 0 || pos_offset + p - causal_base <= r % rows_per_head)
  *     && (member_dev == NULL || bit r of member_dev[u*idx_ld + j]).
- *   out[u][M][d] (dtype) = softmax_S(q.k*scale) V ; lse_dev[u][M] = natural
+ *   out[u][M][d] (out_dtype: dtype, or F32 for partials that a later
+ *   sts_lse_merge combines, e.g. per-rank results of the sharded path)
+ *   = softmax_S(q.k*scale) V ; lse_dev[u][M] = natural
  *   log-sum-exp of the scaled scores (nullable).  dtype F32 computes in fp32
  *   on CUDA cores (parity path); BF16 uses tensor cores with fp32 accumulate.
  * ---------------------------------------------------------------------- */
@@ -122,7 +124,7 @@ STS_API size_t sts_sparse_decode_workspace_bytes(int64_t units, int32_t M, int32
 /* split-K factor that fills 148 SMs x 2 CTAs in whole waves (>= 8 key tiles
  * of 16 per CTA); what the host uses when it has no better knowledge. */
 STS_API int32_t sts_auto_splits(int64_t units, int64_t keys_per_unit);
-STS_API int sts_sparse_decode(int32_t dtype, const void* q_dev, const void* k_cache_dev,
+STS_API int sts_sparse_decode(int32_t dtype, int32_t out_dtype, const void* q_dev, const void* k_cache_dev,
                       const void* v_cache_dev, int64_t kv_unit_stride, int64_t kv_row_stride, int64_t units,
                       int32_t M, int32_t d, const int32_t* idx_dev, int64_t idx_ld,
                       const int32_t* cnt_dev, int32_t n_dense, const uint32_t* member_dev,
@@ -182,6 +184,59 @@ STS_API int sts_row_union(const int32_t* idx_in_dev, int64_t in_ld, const int32_
                   const int32_t* src_dev, int64_t units, int32_t M, int32_t n_max,
                   uint32_t* bitmap_ws_dev, int32_t* idx_out_dev, uint32_t* member_out_dev,
                   int64_t out_ld, int32_t* cnt_out_dev, int32_t* status_dev, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Sequence-sharded selection (context-parallel decode): the
+ * global top-k of a row whose positions are split over P ranks, without
+ * moving scores.  Replaces numkit.topk_indices / sparsity._select_row
+ * (src/numkit.py:74-86, src/sparsity.py:86-112) when the row is sharded.
+ * The union over ranks of the emitted sets equals sts_select_topk on the
+ * concatenated row, bit for bit (ties to the lowest GLOBAL index).
+ *
+ * This rank holds global positions [lo, lo + n_local) (lo page-aligned) of
+ * rows whose committed length is n_global; k_top counts tokens
+ * (page_size 1) or pages.  Row values are formed as in sts_select_topk
+ * (fp32 sum of nsrc source rows).  Host protocol, identical on every rank:
+ *
+ *   begin(g, hist)                                   local keys + digit-0 hist
+ *   for r in 0 .. sts_dist_select_rounds(ps)-1:
+ *       hist_g = allreduce_sum(hist)                 (NCCL, int32 [rows][256])
+ *       round(g, r, hist_g, hist, r == last ? ties : NULL)
+ *   ties_all = allgather(ties)                       (int32 [P][rows])
+ *   finish(g, rank, P, ties_all, ...)                local index lists
+ *
+ * Output: ascending LOCAL offsets (global = lo + offset) of the selected
+ * committed positions, the extras (sink = global 0, recent window, current =
+ * n_global-1; flags as sts_select_topk) held here, and the in-block tail
+ * [n_global, n_global + tail_len) ∩ [lo, lo + n_kv_local).
+ * ---------------------------------------------------------------------- */
+typedef struct sts_dist_rows {
+  const float* scores_dev;   /* [S][ld] fp32 local score rows (columns = local positions) */
+  int64_t ld;
+  const int32_t* row_src_dev; /* [rows][nsrc] or NULL (nsrc == 1, identity) */
+  int32_t nsrc;
+  int64_t rows;
+  int32_t n_global;          /* committed positions of every logical row */
+  int32_t lo;                /* first global position held here */
+  int32_t n_local;           /* positions held here */
+  int32_t k_top;             /* tokens (page_size 1) or pages to keep */
+  int32_t page_size;
+} sts_dist_rows;
+
+#define STS_DIST_BINS 256
+
+STS_API int32_t sts_dist_select_rounds(int32_t page_size);
+STS_API size_t sts_dist_select_workspace_bytes(int64_t rows, int32_t n_local, int32_t page_size);
+STS_API int sts_dist_select_begin(const sts_dist_rows* g, int32_t* hist_local_dev, void* workspace_dev,
+                                  size_t workspace_bytes, void* stream);
+STS_API int sts_dist_select_round(const sts_dist_rows* g, int32_t round, const int32_t* hist_global_dev,
+                                  int32_t* hist_local_dev, int32_t* ties_local_dev, void* workspace_dev,
+                                  size_t workspace_bytes, void* stream);
+STS_API int sts_dist_select_finish(const sts_dist_rows* g, int32_t rank, int32_t nranks,
+                                   const int32_t* ties_all_dev, uint32_t flags, int32_t recent_window,
+                                   int32_t tail_len, int32_t n_kv_local, int32_t* idx_out_dev, int64_t idx_ld,
+                                   int32_t* cnt_out_dev, int32_t* status_dev, void* workspace_dev,
+                                   size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

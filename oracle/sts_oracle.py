@@ -386,3 +386,77 @@ def fp32_order_keys(x) -> np.ndarray:
     keys = np.where(b >> 31 == 1, ~b, b | np.uint32(0x80000000)).astype(np.uint32)
     keys[np.isnan(x)] = 0
     return keys
+
+
+# ---------------------------------------------------------------------------
+# 5. sequence-sharded radix-select protocol (restates csrc/sts_select_dist.cu)
+# ---------------------------------------------------------------------------
+
+DIST_BITS = 8
+
+
+def dist_select_protocol(values_local, lo: int, n_global: int, k: int, rank: int, nranks: int, torch_mod=None):
+    """One rank of the sharded top-k protocol, in numpy, yielding the same
+    collective requests as paper_2605_15508_b200.sharded.DistSelector
+    (("all_reduce_sum", int32 tensor [rows][256]), ("all_gather", ties [rows],
+    ties_all [P][rows])).  Returns the selected GLOBAL indices per row
+    (ascending).  ``values_local``: fp32 [rows, n_local] at global positions
+    lo.. ; positions >= n_global are ignored.  Token mode, fp32 keys, 8-bit
+    digits from the top; the threshold/tie rule of topk_indices (src/numkit.py:74-86)."""
+    import torch
+
+    vals = np.asarray(values_local, dtype=np.float32)
+    rows = vals.shape[0]
+    nc = max(0, min(n_global - lo, vals.shape[1]))
+    keys = fp32_order_keys(vals[:, :nc]).astype(np.uint64) if nc else np.zeros((rows, 0), np.uint64)
+    prefix = np.zeros(rows, np.uint64)
+    pmask = np.zeros(rows, np.uint64)
+    krem = np.full(rows, k, np.int64)
+    dense = k >= n_global
+    done = np.full(rows, dense, bool)
+    ties_local = np.zeros(rows, np.int64)
+    for rnd in range(32 // DIST_BITS):
+        shift = 32 - DIST_BITS * (rnd + 1)
+        hist = np.zeros((rows, 1 << DIST_BITS), np.int64)
+        for r in range(rows):
+            if done[r]:
+                continue
+            m = (keys[r] & pmask[r]) == prefix[r]
+            d = ((keys[r][m] >> np.uint64(shift)) & np.uint64(0xFF)).astype(np.int64)
+            hist[r] = np.bincount(d, minlength=256)
+        h_local = hist.copy()
+        t = torch.from_numpy(hist.astype(np.int32))
+        yield ("all_reduce_sum", t)
+        hg = t.numpy().astype(np.int64)
+        for r in range(rows):
+            if done[r]:
+                continue
+            acc = 0
+            for digit in range(255, -1, -1):
+                c = int(hg[r, digit])
+                if acc < krem[r] <= acc + c:
+                    break
+                acc += c
+            prefix[r] |= np.uint64(digit) << np.uint64(shift)
+            pmask[r] |= np.uint64(0xFF) << np.uint64(shift)
+            krem[r] -= acc
+            if shift == 0 or krem[r] == c:
+                done[r] = True
+                ties_local[r] = h_local[r, digit]
+    tl = torch.from_numpy(ties_local.astype(np.int32))
+    ta = torch.zeros((nranks, rows), dtype=torch.int32)
+    yield ("all_gather", tl, ta)
+    ties_all = ta.numpy().astype(np.int64)
+    out = []
+    for r in range(rows):
+        if dense:
+            out.append(lo + np.arange(nc, dtype=np.int64))
+            continue
+        mk = keys[r] & pmask[r]
+        above = mk > prefix[r]
+        tie = mk == prefix[r]
+        need = max(int(krem[r]) - int(ties_all[:rank, r].sum()), 0)
+        take = np.zeros(nc, bool)
+        take[np.nonzero(tie)[0][:need]] = True
+        out.append(lo + np.nonzero(above | take)[0].astype(np.int64))
+    return out

@@ -37,7 +37,7 @@ SIGNATURES = {
     "sts_page_aggregate": (C.c_int, [_p, _i64, _i64, _p, _i32, _i32, _p, _i64, _p]),
     "sts_sparse_decode_workspace_bytes": (_sz, [_i64, _i32, _i32, _i32]),
     "sts_auto_splits": (_i32, [_i64, _i64]),
-    "sts_sparse_decode": (C.c_int, [_i32, _p, _p, _p, _i64, _i64, _i64, _i32, _i32, _p, _i64, _p, _i32, _p,
+    "sts_sparse_decode": (C.c_int, [_i32, _i32, _p, _p, _p, _i64, _i64, _i64, _i32, _i32, _p, _i64, _p, _i32, _p,
                                     _i32, _i32, _i32, _f32, _p, _p, _i32, _p, _p, _sz, _p]),
     "sts_draft_workspace_bytes": (_sz, [_i64, _i32, _i32]),
     "sts_draft_lse": (C.c_int, [_i32, _p, _p, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _i32, _f32,
@@ -46,7 +46,32 @@ SIGNATURES = {
                                   _p, _i32, _p, _i64, _p]),
     "sts_lse_merge": (C.c_int, [_p, _p, _i32, _i64, _i32, _i32, _p, _p, _p]),
     "sts_row_union": (C.c_int, [_p, _i64, _p, _p, _i64, _i32, _i32, _p, _p, _p, _i64, _p, _p, _p]),
+    "sts_dist_select_rounds": (_i32, [_i32]),
+    "sts_dist_select_workspace_bytes": (_sz, [_i64, _i32, _i32]),
+    "sts_dist_select_begin": (C.c_int, [_p, _p, _p, _sz, _p]),
+    "sts_dist_select_round": (C.c_int, [_p, _i32, _p, _p, _p, _p, _sz, _p]),
+    "sts_dist_select_finish": (C.c_int, [_p, _i32, _i32, _p, _u32, _i32, _i32, _i32, _p, _i64, _p, _p, _p, _sz,
+                                         _p]),
 }
+
+STS_DIST_BINS = 256
+
+
+class DistRows(C.Structure):
+    """struct sts_dist_rows (include/sts_b200.h)."""
+
+    _fields_ = [
+        ("scores_dev", _p),
+        ("ld", _i64),
+        ("row_src_dev", _p),
+        ("nsrc", _i32),
+        ("rows", _i64),
+        ("n_global", _i32),
+        ("lo", _i32),
+        ("n_local", _i32),
+        ("k_top", _i32),
+        ("page_size", _i32),
+    ]
 
 _LIB = None
 

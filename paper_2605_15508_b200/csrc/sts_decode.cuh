@@ -28,7 +28,8 @@ struct DecodeParams {
   int rows_per_head;
   int pos_offset;
   float scale;
-  void* out;      // final output
+  void* out;      // final output (dtype of q, or fp32 when out_f32)
+  int out_f32;
   float* lse;     // final lse (nullable)
   float* o_part;  // partials
   float* l_part;

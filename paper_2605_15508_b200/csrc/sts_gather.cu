@@ -99,8 +99,13 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
   for (int64_t u = blockIdx.x; u < U; u += gridDim.x) {
     if (tiles_of(p, u, KT) != 0) continue;
     if constexpr (MODE == MODE_DECODE) {
-      __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + u * (int64_t)M * D;
-      for (int e = tid; e < M * D; e += NTH) og[e] = __float2bfloat16_rn(0.f);
+      if (p.out_f32) {
+        float* og = static_cast<float*>(p.out) + u * (int64_t)M * D;
+        for (int e = tid; e < M * D; e += NTH) og[e] = 0.f;
+      } else {
+        __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + u * (int64_t)M * D;
+        for (int e = tid; e < M * D; e += NTH) og[e] = __float2bfloat16_rn(0.f);
+      }
       if (tid == 0 && M > 0) set_status(p.status, STS_DEV_EMPTY_ROW);
     }
     if constexpr (MODE != MODE_PROBS)
@@ -286,9 +291,15 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
           for (int mt = 0; mt < D / 16; ++mt) {
             const int d0 = mt * 16 + (lane >> 2);
             if (single) {
-              __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + (u * M + r) * (int64_t)D;
-              og[d0] = __float2bfloat16_rn(o[mt][c] * inv);
-              og[d0 + 8] = __float2bfloat16_rn(o[mt][2 + c] * inv);
+              if (p.out_f32) {
+                float* og = static_cast<float*>(p.out) + (u * M + r) * (int64_t)D;
+                og[d0] = o[mt][c] * inv;
+                og[d0 + 8] = o[mt][2 + c] * inv;
+              } else {
+                __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + (u * M + r) * (int64_t)D;
+                og[d0] = __float2bfloat16_rn(o[mt][c] * inv);
+                og[d0 + 8] = __float2bfloat16_rn(o[mt][2 + c] * inv);
+              }
             } else {
               part_o[r * D + d0] = o[mt][c] * inv;
               part_o[r * D + d0 + 8] = o[mt][2 + c] * inv;
@@ -355,9 +366,13 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
               acc.w += f * x.w;
             }
           }
-          __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + (u * M + r) * (int64_t)D + 4 * d4;
-          *reinterpret_cast<__nv_bfloat162*>(og) = __floats2bfloat162_rn(acc.x, acc.y);
-          *reinterpret_cast<__nv_bfloat162*>(og + 2) = __floats2bfloat162_rn(acc.z, acc.w);
+          if (p.out_f32) {
+            *reinterpret_cast<float4*>(static_cast<float*>(p.out) + (u * M + r) * (int64_t)D + 4 * d4) = acc;
+          } else {
+            __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + (u * M + r) * (int64_t)D + 4 * d4;
+            *reinterpret_cast<__nv_bfloat162*>(og) = __floats2bfloat162_rn(acc.x, acc.y);
+            *reinterpret_cast<__nv_bfloat162*>(og + 2) = __floats2bfloat162_rn(acc.z, acc.w);
+          }
         }
       }
       __syncwarp();

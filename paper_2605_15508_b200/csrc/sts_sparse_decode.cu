@@ -150,7 +150,7 @@ extern "C" size_t sts_sparse_decode_workspace_bytes(int64_t units, int32_t M, in
   return f32 > bf16 ? f32 : bf16;
 }
 
-extern "C" int sts_sparse_decode(int32_t dtype, const void* q_dev, const void* k_cache_dev,
+extern "C" int sts_sparse_decode(int32_t dtype, int32_t out_dtype, const void* q_dev, const void* k_cache_dev,
                                  const void* v_cache_dev, int64_t kv_unit_stride, int64_t kv_row_stride,
                                  int64_t units,
                                  int32_t M, int32_t d, const int32_t* idx_dev, int64_t idx_ld,
@@ -192,6 +192,9 @@ extern "C" int sts_sparse_decode(int32_t dtype, const void* q_dev, const void* k
   p.pos_offset = pos_offset;
   p.scale = scale;
   p.out = out_dev;
+  STS_REQUIRE(out_dtype == dtype || out_dtype == STS_DTYPE_F32, STS_ERR_CONTRACT,
+              "out_dtype must equal dtype or be F32 (partials for a later LSE merge)");
+  p.out_f32 = out_dtype == STS_DTYPE_F32 ? 1 : 0;
   p.lse = lse_dev;
   p.splits = splits;
   p.status = status_dev;

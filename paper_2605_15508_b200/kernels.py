@@ -118,7 +118,7 @@ def select_topk(scores: torch.Tensor, *, budget, page_size: int = 1, include_cur
 def sparse_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, *, idx=None,
                   cnt=None, n_dense: int = 0, member=None, causal_base: int = -1,
                   rows_per_head: int = 1, pos_offset: int = 0, scale=None, splits=None, out=None,
-                  lse=None, status=None, workspace: Workspace | None = None, stream=None):
+                  lse=None, status=None, out_dtype=None, workspace: Workspace | None = None, stream=None):
     """Gathered-KV sparse flash-decode.
 
     q: [U, M, d] (bf16 or fp32); k_cache/v_cache: [U, N, d] views of the same
@@ -144,15 +144,20 @@ def sparse_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
         keys = idx.shape[1] if idx is not None else n_dense
         splits = _lib.load().sts_auto_splits(U, keys) if q.dtype == torch.bfloat16 else 1
     dev = q.device
+    out_dtype = q.dtype if out_dtype is None else out_dtype
+    if out_dtype not in (q.dtype, torch.float32):
+        raise ValueError("out_dtype must be q.dtype or float32")
     if out is None:
-        out = torch.empty((U, M, d), dtype=q.dtype, device=dev)
+        out = torch.empty((U, M, d), dtype=out_dtype, device=dev)
+    elif out.dtype != out_dtype:
+        raise ValueError(f"out must be {out_dtype}")
     if lse is None:
         lse = torch.empty((U, M), dtype=torch.float32, device=dev)
     lib = _lib.load()
     wbytes = lib.sts_sparse_decode_workspace_bytes(U, M, d, splits)
     ws = workspace or _ws("decode", dev)
     wbuf, wlen = ws.get(wbytes)
-    call("sts_sparse_decode", STS_DTYPE[q.dtype], ptr(q), ptr(k_cache), ptr(v_cache), kv_stride, row_stride, U, M,
+    call("sts_sparse_decode", STS_DTYPE[q.dtype], STS_DTYPE[out_dtype], ptr(q), ptr(k_cache), ptr(v_cache), kv_stride, row_stride, U, M,
          d, ptr(idx), idx_ld, ptr(cnt), int(n_dense), ptr(member), int(causal_base), int(rows_per_head),
          int(pos_offset), scale, ptr(out), ptr(lse), int(splits), ptr(status), ptr(wbuf), wlen,
          stream_handle(stream))

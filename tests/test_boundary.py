@@ -29,7 +29,7 @@ def test_library_builds_and_exports_header_symbols():
     nm = subprocess.run(["nm", "-D", "--defined-only", str(lib_path)], capture_output=True, text=True).stdout
     exported = set(re.findall(r" T (sts_\w+)", nm))
     assert declared <= exported, f"missing exports: {declared - exported}"
-    assert lib.sts_abi_version() == 1
+    assert lib.sts_abi_version() == 2
 
 
 def test_status_codes_map_to_reference_exceptions():
@@ -62,8 +62,25 @@ def test_host_validation_without_gpu():
         _lib.call("sts_select_topk", 8, 4, None, 3, 1, None, 4, 2.0, 0, 1, 0, 0, 0, 8, 4, 8, None,
                   None, 0, None)
     with pytest.raises(ContractViolation, match="membership"):
-        _lib.call("sts_sparse_decode", 1, 8, 8, 8, 64, 0, 1, 40, 64, 8, 4, 8, 0, 8, -1, 1, 0, 0.125, 8,
+        _lib.call("sts_sparse_decode", 1, 1, 8, 8, 8, 64, 0, 1, 40, 64, 8, 4, 8, 0, 8, -1, 1, 0, 0.125, 8,
                   None, 1, None, None, 0, None)
+    with pytest.raises(ContractViolation, match="out_dtype"):
+        _lib.call("sts_sparse_decode", 0, 1, 8, 8, 8, 64, 0, 1, 4, 64, 8, 4, 8, 0, None, -1, 1, 0, 0.125, 8,
+                  None, 1, None, None, 0, None)
+    # sharded selection: geometry checked before any launch
+    g = _lib.DistRows(8, 64, None, 1, 4, 100, 3, 32, 10, 2)
+    import ctypes
+    with pytest.raises(ContractViolation, match="page-aligned"):
+        _lib.call("sts_dist_select_begin", ctypes.addressof(g), 8, 8, 1 << 30, None)
+    g = _lib.DistRows(8, 64, None, 1, 4, 100, 0, 32, 10, 1)
+    with pytest.raises(ContractViolation, match="workspace too small"):
+        _lib.call("sts_dist_select_begin", ctypes.addressof(g), 8, 8, 16, None)
+    g = _lib.DistRows(8, 64, None, 1, 4, 100, 0, 32, 0, 1)
+    with pytest.raises(ConfigError, match="k must be"):
+        _lib.call("sts_dist_select_begin", ctypes.addressof(g), 8, 8, 1 << 30, None)
+    lib = _lib.load()
+    assert lib.sts_dist_select_rounds(1) == 4 and lib.sts_dist_select_rounds(16) == 8
+    assert lib.sts_dist_select_workspace_bytes(256, 131072, 1) >= 256 * 131072 * 4
 
 
 def test_sparsity_config_mirrors_reference():
