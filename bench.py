@@ -49,7 +49,18 @@ def parse():
     ap.add_argument("--layout", default="separate", choices=["separate", "interleaved"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bound of the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--context", type=int, default=None, help="override the config's context length")
+    ap.add_argument("--batch", type=int, default=None, help="override the config's batch")
     return ap.parse_args()
+
+
+def shape_overrides(args):
+    o = {}
+    if args.context is not None:
+        o["context"] = args.context
+    if args.batch is not None:
+        o["batch"] = args.batch
+    return o
 
 
 def peaks():
@@ -171,7 +182,7 @@ def run_reference(args):
         return
     from paper_2605_15508_b200.verify import config_shape
 
-    shape = config_shape(args.config)
+    shape = config_shape(args.config, **shape_overrides(args))
     budget = round(1.0 - args.sparsity, 10)
     k_sel = max(1, math.ceil(budget * (shape.context + 1))) + shape.rows
     workers = os.cpu_count() or 1
@@ -230,7 +241,7 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     _lib.load()
 
-    shape = config_shape(args.config)
+    shape = config_shape(args.config, **shape_overrides(args))
     budget = round(1.0 - args.sparsity, 10)
     cfg = SparsityConfig(budget=budget, page_size=args.page_size)
     table = random_mapping_table(shape, seed=5 + rank)
@@ -395,7 +406,7 @@ def run_sharded(args, world, rank, local):
     else:
         drive = sharded.run_single
     _lib.load()
-    shape = config_shape(args.config)
+    shape = config_shape(args.config, **shape_overrides(args))
     budget = round(1.0 - args.sparsity, 10)
     cfg = SparsityConfig(budget=budget, page_size=args.page_size)
     table = random_mapping_table(shape, seed=5)
