@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--layout", default="separate", choices=["separate", "interleaved"])
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bound of the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--eager", action="store_true", help="time stages as eager launches instead of CUDA graphs")
+    ap.add_argument("--flush", default="clean", choices=["clean", "write", "none"], help="L2 flush between stages")
     ap.add_argument("--context", type=int, default=None, help="override the config's context length")
     ap.add_argument("--batch", type=int, default=None, help="override the config's batch")
     return ap.parse_args()
@@ -69,6 +71,37 @@ def peaks():
         d = json.loads(p.read_text())
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class L2Flush:
+    """Evict L2 (126 MB) between timed stages with a 256 MB buffer.
+
+    "write": zero the buffer (leaves ~126 MB of dirty lines that the next
+    kernel's reads must write back); "clean": zero it and then read it back
+    (the L2 ends full of clean, useless lines — the timed kernel starts cold
+    without inheriting the flush's write-back traffic); "none": no flush.
+    """
+
+    def __init__(self, dev, mode="clean"):
+        import torch
+
+        self.mode = mode
+        self.buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if mode != "none" else None
+        self.acc = torch.empty((), dtype=torch.int64, device=dev) if mode == "clean" else None
+
+    def __call__(self):
+        import torch
+
+        if self.mode == "none":
+            return
+        self.buf.zero_()
+        if self.mode == "clean":
+            torch.sum(self.buf.view(-1, 8).view(torch.int64), dim=(0, 1), out=self.acc)
+
+    def describe(self):
+        return {"write": "flushed by a 256 MB write before every timed stage",
+                "clean": "flushed by a 256 MB write + read-back (clean eviction) before every timed stage",
+                "none": "not flushed (inputs larger than L2)"}[self.mode]
 
 
 class ClockSampler:
@@ -251,7 +284,7 @@ def main():
     dqv, dkv = step.draft_views(dq, dk)
     dense_out = torch.empty_like(step.out)
     dense_lse = torch.empty_like(step.lse)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    flush = L2Flush(dev, args.flush)
     st = torch.cuda.current_stream()
 
     def barrier():
@@ -266,27 +299,48 @@ def main():
     assert step.status.item() == 0, f"device status {step.status.item()}"
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    # each stage is captured once into a CUDA graph and replayed, so the
+    # device-timed regions hold the kernels only (no Python launch gaps)
+    stages = {
+        "capture": lambda: step.capture(dqv, dkv),
+        "select": lambda: step.build_masks(),
+        "attend": lambda: step.attend(q, k, v),
+        "dense": lambda: step.attend_dense(q, k, v, out=dense_out, lse=dense_lse),
+    }
+    run_stage = {}
+    for name, fn in stages.items():
+        if args.eager:
+            run_stage[name] = fn
+        else:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            run_stage[name] = g.replay
+    for _ in range(2):
+        for fn in run_stage.values():
+            fn()
+    barrier()
     t_cap, t_sel, t_att, t_den = [], [], [], []
     with ClockSampler(local) as clocks:
         barrier()
         wall0 = time.perf_counter()
         for _ in range(args.steps):
-            flush.zero_()
+            flush()
             e = [ev() for _ in range(4)]
             e[0].record(st)
-            step.capture(dqv, dkv)
+            run_stage["capture"]()
             e[1].record(st)
-            step.build_masks()
+            run_stage["select"]()
             e[2].record(st)
-            flush.zero_()
+            flush()
             e.append(ev())
             e[3].record(st)
-            step.attend(q, k, v)
+            run_stage["attend"]()
             e[4].record(st)
-            flush.zero_()
+            flush()
             e5, e6 = ev(), ev()
             e5.record(st)
-            step.attend_dense(q, k, v, out=dense_out, lse=dense_lse)
+            run_stage["dense"]()
             e6.record(st)
             torch.cuda.synchronize()
             t_cap.append(e[0].elapsed_time(e[1]) * 1e3)
@@ -305,7 +359,7 @@ def main():
     dqe, _ = step.draft_views(d_dq, dk)
     t_e2e = []
     for i in range(args.warmup + args.steps):
-        flush.zero_()
+        flush()
         e0, e1 = ev(), ev()
         e0.record(st)
         d_tq.copy_(h_tq, non_blocking=True)
@@ -363,7 +417,8 @@ def main():
                                f"kv layout {args.layout}",
                    "context": shape.context, "batch": shape.batch, "gamma": shape.gamma, "mode": args.mode,
                    "page_size": args.page_size, "kv_layout": args.layout,
-                   "keys_per_kv_head": round(cnt, 1), "l2": "flushed (256 MB write) before every timed stage",
+                   "keys_per_kv_head": round(cnt, 1), "l2": flush.describe(),
+                   "launch": "eager" if args.eager else "CUDA graph per stage",
                    "parallelism": "replicas" if world > 1 else "single"},
         "dense_us": round(den, 2), "speedup_vs_dense": round(den / att, 3),
         "mask_build_us": {"draft_capture": round(cap, 2), "select": round(sel, 2)},
@@ -413,7 +468,7 @@ def run_sharded(args, world, rank, local):
     step = sharded.ShardedVerifyStep(shape, cfg, table, rank, world, device=dev, align=max(64, args.page_size))
     dq, dk, tq, tk, tv = sharded.local_synthetic_inputs(shape, step.bounds, rank, dev, seed=0)
     dqv, dkv, q, k, v = step.local_views(dq, dk, tq, tk, tv, full=False)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush = L2Flush(dev, args.flush)
     st = torch.cuda.current_stream()
 
     def barrier():
@@ -430,7 +485,7 @@ def run_sharded(args, world, rank, local):
     t_cap, t_sel, t_att, t_den = [], [], [], []
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
-            flush.zero_()
+            flush()
             barrier()
             e = [ev() for _ in range(3)]
             e[0].record(st)
@@ -438,13 +493,13 @@ def run_sharded(args, world, rank, local):
             e[1].record(st)
             drive(step.build_masks())
             e[2].record(st)
-            flush.zero_()
+            flush()
             barrier()
             e3, e4 = ev(), ev()
             e3.record(st)
             drive(step.attend(q, k, v))
             e4.record(st)
-            flush.zero_()
+            flush()
             barrier()
             e5, e6 = ev(), ev()
             e5.record(st)
@@ -462,7 +517,7 @@ def run_sharded(args, world, rank, local):
     dqe, _, qe, _, _ = step.local_views(d_dq, dk, d_tq, tk, tv, full=False)
     t_e2e = []
     for i in range(args.warmup + args.steps):
-        flush.zero_()
+        flush()
         barrier()
         e0, e1 = ev(), ev()
         e0.record(st)
@@ -499,7 +554,7 @@ def run_sharded(args, world, rank, local):
                                f"{shape.gamma}, sparsity {args.sparsity}, mode S, page_size {args.page_size}",
                    "context": shape.context, "batch": shape.batch, "gamma": shape.gamma, "mode": "S",
                    "page_size": args.page_size, "shard_positions": step.n_loc,
-                   "keys_per_kv_head": round(keys_per_unit, 1), "l2": "flushed (256 MB write) before every timed stage",
+                   "keys_per_kv_head": round(keys_per_unit, 1), "l2": flush.describe(),
                    "parallelism": f"sequence-sharded x{world} (NCCL histogram allreduce + LSE merge)"},
         "dense_us": round(den, 2), "speedup_vs_dense": round(den / att, 3),
         "mask_build_us": {"draft_capture": round(cap, 2), "select": round(sel, 2)},

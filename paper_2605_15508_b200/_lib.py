@@ -13,7 +13,7 @@ from pathlib import Path
 from .errors import raise_for_status
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "_lib" / "libsts_b200.so"
+LIB_PATH = Path(os.environ["STS_B200_LIB"]) if os.environ.get("STS_B200_LIB") else _PKG / "_lib" / "libsts_b200.so"
 HEADER = _PKG.parent / "include" / "sts_b200.h"
 
 STS_DTYPE_F32 = 0

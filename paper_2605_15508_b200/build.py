@@ -53,6 +53,17 @@ def nvcc_path() -> str:
     raise RuntimeError("nvcc not found: cannot build libsts_b200.so")
 
 
+def build_variant(name: str, defines: list[str]) -> Path:
+    """Tuning aid: build a copy of the library with extra -D flags into
+    _lib/variants/libsts_b200_<name>.so (select it with STS_B200_LIB)."""
+    out = LIBDIR / "variants" / f"libsts_b200_{name}.so"
+    out.parent.mkdir(parents=True, exist_ok=True)
+    cmd = [nvcc_path(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", str(out),
+           *[str(p) for p in sorted(CSRC.glob("*.cu"))]]
+    subprocess.run(cmd, check=True)
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     digest = _digest()
     if LIB.exists() and STAMP.exists() and STAMP.read_text().strip() == digest and not force:

@@ -54,6 +54,8 @@ int lse_merge_launch(const float* o_part, const float* lse_part, int nparts, int
                      int out_dtype, void* out, float* lse_out, cudaStream_t st);
 
 int auto_splits(int64_t units, int64_t keys_per_unit);
+// bf16 decode of the stacked verification rows (sts_verify_decode.cu)
+int verify_decode_launch(DecodeParams& p, cudaStream_t st);
 int gather_launch(int mode, DecodeParams& p, cudaStream_t st);
 
 }  // namespace sts

@@ -51,7 +51,7 @@ struct GL {
   static constexpr int SUBB = KEY_TILE * PITCH;   // one 16-key K (or V) block
   static constexpr int KV = KT * PITCH;           // K block -> V block
   static constexpr int STAGE = (K_ONLY ? 1 : 2) * KV;
-  static constexpr int RING = 2 * STAGES;
+  static constexpr int RING = STAGES <= 2 ? 4 : 8;  // index ring (power of 2, >= 2*STAGES)
   static constexpr int IDX_BYTES = RING * KT * 4;
   static constexpr int META_BYTES = RING * 16;
   static constexpr int PROB = MODE == MODE_PROBS ? KT * MP * 4 : 0;
@@ -73,8 +73,16 @@ __device__ __forceinline__ int tiles_of(const DecodeParams& p, int64_t u, int KT
 
 __device__ __forceinline__ int owner_of(int64_t t, int64_t T, int W) { return (int)(((t + 1) * W - 1) / T); }
 
+#ifndef STS_GATHER_MINB3
+#define STS_GATHER_MINB3 5
+#endif
+// resident CTAs the register allocation must allow (NT = 3 is the c2 / c4
+// decode shape: 5 -> 128 registers, 6 -> 112)
+template <int NT>
+constexpr int gather_min_blocks() { return NT == 3 ? STS_GATHER_MINB3 : 16 / NT; }
+
 template <int D, int NT, int MODE, int SUB, int STAGES>
-__global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p) {
+__global__ void __launch_bounds__(NT * 32, gather_min_blocks<NT>()) gather_kernel(DecodeParams p) {
   using L = GL<D, NT, MODE, SUB, STAGES>;
   constexpr int KT = L::KT, MP = L::MP, CH = L::CH, NTH = L::THREADS, PITCH = L::PITCH;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -113,11 +121,35 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
         for (int r = tid; r < M; r += NTH) p.lse[u * M + r] = -INFINITY;
   }
 
-  // ---- tile space and this CTA's range (every warp computes the same) ----
-  int64_t T = 0;
-  for (int64_t u = lane; u < U; u += 32) T += tiles_of(p, u, KT);
+  // ---- tile space and this CTA's range: block-parallel scan of the unit
+  // tile counts (thread t owns units [t*cpt, (t+1)*cpt); its count loads are
+  // independent, so the whole prologue is ~one memory round trip) ----
+  __shared__ long long s_scan[NT + 2];
+  const int64_t cpt = (U + NTH - 1) / NTH;
+  const int64_t ub = (int64_t)tid * cpt, ue = ub + cpt < U ? ub + cpt : U;
+  int64_t mine = 0;
+  for (int64_t u0 = ub; u0 < ue; u0 += 4) {
+    int t4[4];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) T += __shfl_xor_sync(0xffffffffu, T, o);
+    for (int j = 0; j < 4; ++j) t4[j] = u0 + j < ue ? tiles_of(p, u0 + j, KT) : 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) mine += t4[j];
+  }
+  int64_t incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t x = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += x;
+  }
+  if (lane == 31) s_scan[warp] = incl;
+  __syncthreads();
+  int64_t before = 0, T = 0;
+#pragma unroll
+  for (int ww = 0; ww < NT; ++ww) {
+    const int64_t v = s_scan[ww];
+    before += ww < warp ? v : 0;
+    T += v;
+  }
   if (T == 0) return;
   const int W = (int)(T < (int64_t)gridDim.x ? T : (int64_t)gridDim.x);
   const int w = blockIdx.x;
@@ -125,39 +157,29 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
   const int64_t s_w = (int64_t)w * T / W;
   const int64_t e_w = (int64_t)(w + 1) * T / W;
   const int ntile = (int)(e_w - s_w);
-
-  // unit holding tile s_w (warp-cooperative prefix scan over unit tile counts)
-  int64_t iu = 0, iP = 0;
   {
-    int64_t base = 0;
-    for (int64_t u0 = 0; u0 < U; u0 += 32) {
-      const int64_t u = u0 + lane;
-      const int t_u = u < U ? tiles_of(p, u, KT) : 0;
-      int64_t incl = t_u;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int64_t x = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += x;
+    // the thread whose units contain tile s_w finds the unit and its first tile
+    int64_t acc = before + incl - mine;
+    if (acc <= s_w && s_w < acc + mine) {
+      for (int64_t u = ub; u < ue; ++u) {
+        const int t_u = tiles_of(p, u, KT);
+        if (s_w < acc + t_u) {
+          s_scan[NT] = u;
+          s_scan[NT + 1] = acc;
+          break;
+        }
+        acc += t_u;
       }
-      const int64_t tot = __shfl_sync(0xffffffffu, incl, 31);
-      if (base + tot > s_w) {
-        const uint32_t hit = __ballot_sync(0xffffffffu, base + incl > s_w);
-        const int src = __ffs(hit) - 1;
-        iu = u0 + src;
-        iP = base + __shfl_sync(0xffffffffu, incl - t_u, src);
-        break;
-      }
-      base += tot;
     }
   }
+  __syncthreads();
+  int64_t iu = s_scan[NT], iP = s_scan[NT + 1];
   int icnt = p.idx ? p.cnt[iu] : p.n_dense;
   int64_t iPn = iP + (icnt + KT - 1) / KT;
 
   // index cursor: slice of relative tile i -> next ring slot (+ meta)
-  int idx_slot = 0;
   auto issue_idx = [&](int i) {
-    const int slot = idx_slot;
-    idx_slot = idx_slot + 1 == L::RING ? 0 : idx_slot + 1;
+    const int slot = i & (L::RING - 1);
     if (i >= ntile) return;
     const int64_t t = s_w + i;
     while (t >= iPn) {
@@ -189,27 +211,54 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
   };
 
   // K/V gather: thread -> (chunk g_ch, rows g_r0 + GROWS*j); K and V of a
-  // (row, chunk) share the index lookup and the address
+  // (row, chunk) share the index lookup.  Row offsets are 32-bit (a unit spans
+  // < 4 GiB, checked by the host), so each 16-byte copy costs one
+  // IMAD.WIDE.U32 + LDGSTS; full tiles skip the bounds test and the zero-fill.
+  constexpr int GROWS = L::GROWS;
+  constexpr int GJ = (KT + GROWS - 1) / GROWS;
   const int g_ch = tid % CH, g_r0 = tid / CH;
+  const int g_n = (KT - g_r0 + GROWS - 1) / GROWS;  // rows this thread copies per tile
   const uint32_t g_dst = (uint32_t)(g_r0 * PITCH + g_ch * 16);
+  const uint32_t row_bytes = (uint32_t)p.row_stride * 2u;
+  int64_t g_u = -1;
+  const char* g_kb = nullptr;
+  const char* g_vb = nullptr;
   auto issue_data = [&](int i, int slot, int stage) {
     if (i >= ntile) return;
     const int64_t u = s_meta[slot * 4 + 0];
     const int jb = s_meta[slot * 4 + 1], cu = s_meta[slot * 4 + 2];
+    if (u != g_u) {
+      g_u = u;
+      // the math side will load this unit's Q fragments when it gets here:
+      // pull them into L2 now (M*D*2 bytes, one 128-byte line per thread)
+      if (tid * 128 < M * D * 2)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const char*>(p.q) + u * (int64_t)M * D * 2 + tid * 128));
+      g_kb = static_cast<const char*>(p.k) + (u * p.kv_stride + g_ch * 8) * 2;
+      g_vb = MODE == MODE_DECODE ? static_cast<const char*>(p.v) + (u * p.kv_stride + g_ch * 8) * 2 : g_kb;
+    }
     const uint32_t dst0 = stage_base + stage * L::STAGE + g_dst;
-    const __nv_bfloat16* kg = static_cast<const __nv_bfloat16*>(p.k) + u * p.kv_stride + g_ch * 8;
-    const __nv_bfloat16* vg = static_cast<const __nv_bfloat16*>(p.v) + u * p.kv_stride + g_ch * 8;
     const int* ring = s_idx + slot * KT;
+    if (jb + KT <= cu) {
 #pragma unroll
-    for (int j = 0; j < (KT + L::GROWS - 1) / L::GROWS; ++j) {
-      const int r = g_r0 + j * L::GROWS;
-      if (KT % L::GROWS != 0 && r >= KT) break;
-      const bool ok = jb + r < cu;
-      const int pr = ok ? (p.idx ? ring[r] : jb + r) : 0;
-      const int64_t off = (int64_t)pr * p.row_stride;
-      const uint32_t dst = dst0 + j * L::GROWS * PITCH;
-      cp_async_16_zfill(dst, kg + off, ok);
-      if constexpr (MODE == MODE_DECODE) cp_async_16_zfill(dst + L::KV, vg + off, ok);
+      for (int j = 0; j < GJ; ++j) {
+        if (KT % GROWS != 0 && j == GJ - 1 && j >= g_n) break;
+        const int r = g_r0 + j * GROWS;
+        const uint32_t pr = p.idx ? (uint32_t)ring[r] : (uint32_t)(jb + r);
+        const uint32_t dst = dst0 + j * GROWS * PITCH;
+        cp_async_16(dst, g_kb + (uint64_t)pr * row_bytes);
+        if constexpr (MODE == MODE_DECODE) cp_async_16(dst + L::KV, g_vb + (uint64_t)pr * row_bytes);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < GJ; ++j) {
+        if (KT % GROWS != 0 && j == GJ - 1 && j >= g_n) break;
+        const int r = g_r0 + j * GROWS;
+        const bool ok = jb + r < cu;
+        const uint32_t pr = ok ? (p.idx ? (uint32_t)ring[r] : (uint32_t)(jb + r)) : 0u;
+        const uint32_t dst = dst0 + j * GROWS * PITCH;
+        cp_async_16_zfill(dst, g_kb + (uint64_t)pr * row_bytes, ok);
+        if constexpr (MODE == MODE_DECODE) cp_async_16_zfill(dst + L::KV, g_vb + (uint64_t)pr * row_bytes, ok);
+      }
     }
   };
 
@@ -327,43 +376,62 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
       __syncthreads();
       const int last = *s_flag;
       if (!last) return;
-      // merge CTAs wf..wl in order; each warp merges its own 8 rows
+      // merge CTAs wf..wl in order, the whole CTA at once: every load below is
+      // independent of the others (batches of 8 / 4 partials in flight per
+      // thread), so the merge costs ~3 L2 round trips instead of a serial
+      // chain of 2n per row
       const int n = wl - wf + 1;
-      if (lane < 8) {
-        const int r = warp * 8 + lane;
-        float mstar = -INFINITY, tot = 0.f;
-        if (r < M) {
-          for (int ww = 0; ww < n; ++ww) mstar = fmaxf(mstar, __ldcg(p.l_part + ((int64_t)wf + ww + u) * M + r));
-          if (mstar != -INFINITY)
-            for (int ww = 0; ww < n; ++ww) {
-              const float l = __ldcg(p.l_part + ((int64_t)wf + ww + u) * M + r);
-              tot += l == -INFINITY ? 0.f : expf(l - mstar);
-            }
-          if (p.lse) p.lse[u * M + r] = tot > 0.f ? mstar + logf(tot) : -INFINITY;
-          if (MODE == MODE_DECODE && !(tot > 0.f)) set_status(p.status, STS_DEV_EMPTY_ROW);
+      const float* lp = p.l_part + ((int64_t)wf + u) * M;  // partial slot ww at lp + ww*M
+      for (int r = tid; r < M; r += NTH) {
+        float mstar = -INFINITY;
+        for (int w0 = 0; w0 < n; w0 += 8) {
+          float l8[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) l8[j] = w0 + j < n ? __ldcg(lp + (int64_t)(w0 + j) * M + r) : -INFINITY;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) mstar = fmaxf(mstar, l8[j]);
         }
+        float tot = 0.f;
+        if (mstar != -INFINITY)
+          for (int w0 = 0; w0 < n; w0 += 8) {
+            float l8[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) l8[j] = w0 + j < n ? __ldcg(lp + (int64_t)(w0 + j) * M + r) : -INFINITY;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) tot += l8[j] == -INFINITY ? 0.f : expf(l8[j] - mstar);
+          }
+        if (p.lse) p.lse[u * M + r] = tot > 0.f ? mstar + logf(tot) : -INFINITY;
+        if (MODE == MODE_DECODE && !(tot > 0.f)) set_status(p.status, STS_DEV_EMPTY_ROW);
         s_merge[r * 2 + 0] = mstar;
-        s_merge[r * 2 + 1] = tot;
+        s_merge[r * 2 + 1] = tot > 0.f ? 1.f / tot : 0.f;
       }
-      __syncwarp();
       if constexpr (MODE == MODE_DECODE) {
+        __syncthreads();
         constexpr int D4 = D / 4;
-        for (int e = lane; e < 8 * D4; e += 32) {
-          const int r = warp * 8 + e / D4, d4 = e % D4;
-          if (r >= M) continue;
-          const float mstar = s_merge[r * 2], tot = s_merge[r * 2 + 1];
+        const float* op = p.o_part + ((int64_t)wf + u) * M * D;  // slot ww at op + ww*M*D
+        for (int e = tid; e < M * D4; e += NTH) {
+          const int r = e / D4, d4 = e % D4;
+          const float mstar = s_merge[r * 2], inv = s_merge[r * 2 + 1];
           float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (tot > 0.f) {
-#pragma unroll 4
-            for (int ww = 0; ww < n; ++ww) {
-              const int64_t sl = (int64_t)wf + ww + u;
-              const float l = __ldcg(p.l_part + sl * M + r);
-              const float f = l == -INFINITY ? 0.f : expf(l - mstar) / tot;
-              const float4 x = __ldcg(reinterpret_cast<const float4*>(p.o_part + (sl * M + r) * D) + d4);
-              acc.x += f * x.x;
-              acc.y += f * x.y;
-              acc.z += f * x.z;
-              acc.w += f * x.w;
+          if (inv > 0.f) {
+            for (int w0 = 0; w0 < n; w0 += 4) {
+              float l4[4];
+              float4 x4[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const bool ok = w0 + j < n;
+                l4[j] = ok ? __ldcg(lp + (int64_t)(w0 + j) * M + r) : -INFINITY;
+                x4[j] = ok ? __ldcg(reinterpret_cast<const float4*>(op + ((int64_t)(w0 + j) * M + r) * D) + d4)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                const float f = l4[j] == -INFINITY ? 0.f : expf(l4[j] - mstar) * inv;
+                acc.x += f * x4[j].x;
+                acc.y += f * x4[j].y;
+                acc.z += f * x4[j].z;
+                acc.w += f * x4[j].w;
+              }
             }
           }
           if (p.out_f32) {
@@ -375,7 +443,7 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
           }
         }
       }
-      __syncwarp();
+      __syncthreads();  // s_merge / the stage buffers are reused by the caller
     }
   };
 
@@ -391,16 +459,13 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
     cp_async_commit();
   }
 
-  int slot = 0, stage = 0;                        // of tile i
-  int f_slot = STAGES - 1, f_stage = STAGES - 1;  // of tile i + STAGES - 1
   for (int i = 0; i < ntile; ++i) {
+    const int slot = i & (L::RING - 1), stage = i % STAGES;
     cp_async_wait<STAGES - 2>();  // this thread's gathers of tile i landed (and idx of tile i+STAGES-1)
     __syncthreads();              // ... everyone's; everyone is done with tile i-1
-    issue_data(i + STAGES - 1, f_slot, f_stage);  // refill the stage tile i-1 used
+    issue_data(i + STAGES - 1, (i + STAGES - 1) & (L::RING - 1), (i + STAGES - 1) % STAGES);  // refill tile i-1's stage
     issue_idx(i + 2 * STAGES - 1);
     cp_async_commit();
-    f_slot = f_slot + 1 == L::RING ? 0 : f_slot + 1;
-    f_stage = f_stage + 1 == STAGES ? 0 : f_stage + 1;
 
     const int64_t u = s_meta[slot * 4 + 0];
     const int j0 = s_meta[slot * 4 + 1];
@@ -554,8 +619,6 @@ __global__ void __launch_bounds__(NT * 32, 16 / NT) gather_kernel(DecodeParams p
         }
       }
     }
-    slot = slot + 1 == L::RING ? 0 : slot + 1;
-    stage = stage + 1 == STAGES ? 0 : stage + 1;
   }
   cp_async_wait<0>();
   if (cur_u >= 0) flush(cur_u, cur_P, cur_cnt);
@@ -574,10 +637,15 @@ int launch_cfg(DecodeParams& p, cudaStream_t st) {
   using L = GL<D, NT, MODE, SUB, STAGES>;
   static_assert(L::SMEM <= 227 * 1024, "gather kernel shared memory");
   auto kern = gather_kernel<D, NT, MODE, SUB, STAGES>;
-  STS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM));
-  int per_sm = 0;
-  STS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::THREADS, L::SMEM));
-  if (per_sm < 1) per_sm = 1;
+  // attribute + occupancy once per instantiation (thread-safe static init);
+  // the launch path is then a single <<<>>> (cheap enough for per-step calls)
+  static const int per_sm = [&]() {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM) != cudaSuccess) return -1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, L::THREADS, L::SMEM) != cudaSuccess) return -1;
+    return n < 1 ? 1 : n;
+  }();
+  STS_REQUIRE(per_sm > 0, STS_ERR_CUDA, "gather kernel setup failed: %s", cudaGetErrorString(cudaGetLastError()));
   kern<<<num_sms() * per_sm, L::THREADS, L::SMEM, st>>>(p);
   STS_LAUNCH_CHECK();
   return STS_OK;
@@ -632,7 +700,13 @@ int gdispatch_d(DecodeParams& p, cudaStream_t st) {
 }  // namespace
 
 int gather_launch(int mode, DecodeParams& p, cudaStream_t st) {
-  if (mode == MODE_DECODE) return gdispatch_d<MODE_DECODE>(p, st);
+  if (mode == MODE_DECODE) {
+    // product path: sts_verify_decode.cu; STS_DECODE_LEGACY=1 selects the
+    // row-split kernel below (kept for A/B measurements)
+    static const bool legacy = getenv("STS_DECODE_LEGACY") && atoi(getenv("STS_DECODE_LEGACY")) == 1;
+    if (!legacy) return verify_decode_launch(p, st);
+    return gdispatch_d<MODE_DECODE>(p, st);
+  }
   if (mode == MODE_LSE) return gdispatch_d<MODE_LSE>(p, st);
   return gdispatch_d<MODE_PROBS>(p, st);
 }

@@ -638,7 +638,9 @@ extern "C" int sts_select_topk(const float* scores_dev, int64_t ld, const int32_
     p.gbuf_stride = p.buf_bytes;
     grid = (int)slots;
   }
-  STS_CUDA_CHECK(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  static const cudaError_t attr = cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       (int)(sh_bytes + SEL_SMEM_BUDGET));
+  STS_CUDA_CHECK(attr);
   select_kernel<<<grid, SEL_THREADS, smem, static_cast<cudaStream_t>(stream)>>>(p);
   STS_LAUNCH_CHECK();
   return STS_OK;

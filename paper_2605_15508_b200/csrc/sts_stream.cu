@@ -24,6 +24,10 @@ size_t stream_workspace_bytes(int mode, int64_t units, int M, int d) {
 }
 
 int stream_launch(int mode, DecodeParams& p, void* ws, size_t ws_bytes, cudaStream_t st) {
+  // the gather kernels address rows with 32-bit byte offsets inside a unit
+  STS_REQUIRE(p.kv_stride >= 0 && p.kv_stride * 2 <= (int64_t(1) << 32) &&
+                  (int64_t)p.n_dense * p.row_stride * 2 <= (int64_t(1) << 32),
+              STS_ERR_CONTRACT, "one (batch, layer, head) unit of the cache must span < 4 GiB");
   const size_t need = stream_workspace_bytes(mode, p.units, p.M, p.d);
   if (mode != MODE_PROBS) {
     STS_REQUIRE(ws && ws_bytes >= need, STS_ERR_CONTRACT, "gather workspace too small: need %zu, got %zu", need,

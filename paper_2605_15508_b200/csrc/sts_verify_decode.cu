@@ -1,0 +1,675 @@
+// sts_verify_decode.cu — gathered-KV sparse flash-decode of the stacked
+// verification rows (bf16, sm_100a).  The product kernel of sts_sparse_decode.
+//
+// Work decomposition (as the gather kernel of sts_gather.cu): unit = (batch,
+// layer, kv-head); the key tiles of all units form one global tile space cut
+// into equal contiguous ranges, one per CTA (persistent stream-K, grid = SMs x
+// resident CTAs); units split over CTAs are merged by the last CTA to arrive.
+//
+// Math layout: one warp per 16 stacked query rows (M = GQA group x (gamma+1);
+// M = 20 -> 2 warps, M = 40 -> 3), each warp walks ALL keys of the tile:
+//   S (16 rows x 8 keys) = Q (A, registers, loaded once per unit) . K^T
+//     (B fragments: ldmatrix of the gathered K rows, 4 independent n-tiles)
+//   P stays in registers: the S accumulator layout IS the A-fragment layout of
+//     the next MMA (no shared-memory round trip, no transpose)
+//   O (16 rows x D) += P . V  (B fragments: ldmatrix.trans of the gathered V)
+// Softmax statistics are per row, reduced over the 4 lanes of a quad, so a
+// 32-key tile costs each thread 16 exponentials and 2 shuffles per row.
+//
+// Gather: 16-byte cp.async into padded rows (2d+16 bytes: conflict-free
+// ldmatrix), one IMAD.WIDE + LDGSTS per copy (32-bit row offsets), STAGES
+// deep, continuous across unit boundaries; index slices prefetched a ring ahead.
+#include <stdlib.h>
+
+#include "sts_decode.cuh"
+
+namespace sts {
+namespace {
+
+constexpr float LN2 = 0.6931471805599453f;
+
+// Optional per-CTA timeline (tuning builds only: -DSTS_TRACE, read back with
+// sts_debug_trace): entry, first issue, first tile ready, loop end, exit,
+// ns spent in unit flushes, flush count, tiles.
+#ifdef STS_TRACE
+__device__ unsigned long long g_trace[8192 * 8];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define STS_TRACE_AT(k) \
+  if (threadIdx.x == 0 && blockIdx.x < 8192) g_trace[blockIdx.x * 8 + (k)] = gtimer()
+#define STS_TRACE_ADD(k, v) \
+  if (threadIdx.x == 0 && blockIdx.x < 8192) g_trace[blockIdx.x * 8 + (k)] += (v)
+#else
+#define STS_TRACE_AT(k)
+#define STS_TRACE_ADD(k, v)
+#endif
+
+__device__ __forceinline__ void cp_async_4z(uint32_t dst, const void* src, bool valid) {
+  int sz = valid ? 4 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(sz));
+}
+
+__device__ __forceinline__ int unit_tiles(const DecodeParams& p, int64_t u, int KT) {
+  const int c = p.idx ? p.cnt[u] : p.n_dense;
+  return (c + KT - 1) / KT;
+}
+
+__device__ __forceinline__ int tile_owner(int64_t t, int64_t T, int W) { return (int)(((t + 1) * W - 1) / T); }
+
+template <int D, int NW, int KT, int STAGES>
+struct VL {
+  static constexpr int THREADS = NW * 32;
+  static constexpr int CH = D / 8;                // 16-byte chunks per row
+  static constexpr int PITCH = D * 2 + 16;        // padded row
+  static constexpr int KV = KT * PITCH;           // K block -> V block
+  static constexpr int STAGE = 2 * KV;
+  static constexpr int RING = STAGES <= 2 ? 4 : 8;  // index ring (power of 2, >= 2*STAGES)
+  static constexpr int IDX_BYTES = RING * KT * 4;
+  static constexpr int META_BYTES = RING * 16;
+  static constexpr int MERGE = NW * 16 * 2 * 4;
+  static constexpr int SMEM = STAGES * STAGE + 2 * IDX_BYTES + META_BYTES + MERGE + 16;
+  // resident CTAs per SM the register allocation must allow: the shared-memory
+  // limit, capped so a warp keeps ~168 registers (O, Q fragments, S, P)
+  static constexpr int SMEM_CTAS = (227 * 1024) / (SMEM + 1024);
+  static constexpr int REG_CTAS = NW == 1 ? 12 : (NW == 2 ? 6 : 3);
+  static constexpr int MINB = SMEM_CTAS < REG_CTAS ? (SMEM_CTAS < 1 ? 1 : SMEM_CTAS) : REG_CTAS;
+  static constexpr int GROWS = THREADS / CH;      // rows per gather pass
+  static constexpr int GJ = (KT + GROWS - 1) / GROWS;
+  static_assert(THREADS % CH == 0, "gather mapping");
+  static_assert(KT % 16 == 0, "key tile");
+};
+
+template <int D, int NW, int KT, int STAGES>
+__global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES>::MINB)) verify_decode_kernel(DecodeParams p) {
+  using L = VL<D, NW, KT, STAGES>;
+  constexpr int NTH = L::THREADS, PITCH = L::PITCH, CH = L::CH;
+  constexpr int NT = KT / 8;   // 8-key n-tiles of S per tile
+  constexpr int KS = KT / 16;  // 16-key k-steps of P.V per tile
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const int M = p.M;
+  const int64_t U = p.units;
+#ifdef STS_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 8192)
+    for (int k = 0; k < 8; ++k) g_trace[blockIdx.x * 8 + k] = 0;
+#endif
+  STS_TRACE_AT(0);
+
+  uint8_t* s_stage = smem;
+  int* s_idx = reinterpret_cast<int*>(s_stage + STAGES * L::STAGE);
+  uint32_t* s_mem = reinterpret_cast<uint32_t*>(s_idx + L::RING * KT);
+  int* s_meta = reinterpret_cast<int*>(s_mem + L::RING * KT);
+  float* s_merge = reinterpret_cast<float*>(s_meta + L::RING * 4);
+  int* s_flag = reinterpret_cast<int*>(s_merge + L::MERGE / 4);
+  const uint32_t stage_base = smem_u32(s_stage);
+  const uint32_t idx_base = smem_u32(s_idx);
+  const uint32_t mem_base = smem_u32(s_mem);
+
+  // ---- units with no keys (striped over CTAs): zero rows, LSE -inf ----
+  for (int64_t u = blockIdx.x; u < U; u += gridDim.x) {
+    if (unit_tiles(p, u, KT) != 0) continue;
+    if (p.out_f32) {
+      float* og = static_cast<float*>(p.out) + u * (int64_t)M * D;
+      for (int e = tid; e < M * D; e += NTH) og[e] = 0.f;
+    } else {
+      __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + u * (int64_t)M * D;
+      for (int e = tid; e < M * D; e += NTH) og[e] = __float2bfloat16_rn(0.f);
+    }
+    if (tid == 0 && M > 0) set_status(p.status, STS_DEV_EMPTY_ROW);
+    if (p.lse)
+      for (int r = tid; r < M; r += NTH) p.lse[u * M + r] = -INFINITY;
+  }
+
+  // ---- tile space and this CTA's range (block-parallel scan) ----
+  __shared__ long long s_scan[NW + 3];
+  const int64_t cpt = (U + NTH - 1) / NTH;
+  const int64_t ub = (int64_t)tid * cpt, ue = ub + cpt < U ? ub + cpt : U;
+  int64_t mine = 0;
+  for (int64_t u0 = ub; u0 < ue; u0 += 4) {
+    int t4[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) t4[j] = u0 + j < ue ? unit_tiles(p, u0 + j, KT) : 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) mine += t4[j];
+  }
+  int64_t incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t x = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += x;
+  }
+  if (lane == 31) s_scan[warp] = incl;
+  __syncthreads();
+  int64_t before = 0, T = 0;
+#pragma unroll
+  for (int ww = 0; ww < NW; ++ww) {
+    const int64_t v = s_scan[ww];
+    before += ww < warp ? v : 0;
+    T += v;
+  }
+  if (T == 0) return;
+  const int W = (int)(T < (int64_t)gridDim.x ? T : (int64_t)gridDim.x);
+  const int w = blockIdx.x;
+  if (w >= W) return;
+  const int64_t s_w = (int64_t)w * T / W;
+  const int64_t e_w = (int64_t)(w + 1) * T / W;
+  const int ntile = (int)(e_w - s_w);
+  {
+    int64_t acc = before + incl - mine;
+    if (acc <= s_w && s_w < acc + mine) {
+      for (int64_t u = ub; u < ue; ++u) {
+        const int t_u = unit_tiles(p, u, KT);
+        if (s_w < acc + t_u) {
+          s_scan[NW] = u;
+          s_scan[NW + 1] = acc;
+          s_scan[NW + 2] = p.idx ? p.cnt[u] : p.n_dense;  // (an L1 hit: just loaded)
+          break;
+        }
+        acc += t_u;
+      }
+    }
+  }
+  __syncthreads();
+  int64_t iu = s_scan[NW], iP = s_scan[NW + 1];
+  int icnt = (int)s_scan[NW + 2];
+  int64_t iPn = iP + (icnt + KT - 1) / KT;
+
+  // ---- index slices: tile i -> ring slot i & (RING-1) (+ meta) ----
+  auto issue_idx = [&](int i) {
+    const int slot = i & (L::RING - 1);
+    if (i >= ntile) return;
+    const int64_t t = s_w + i;
+    while (t >= iPn) {
+      ++iu;
+      iP = iPn;
+      icnt = p.idx ? p.cnt[iu] : p.n_dense;
+      iPn = iP + (icnt + KT - 1) / KT;
+    }
+    const int j0 = (int)(t - iP) * KT;
+    if (tid == 0) {
+      s_meta[slot * 4 + 0] = (int)iu;
+      s_meta[slot * 4 + 1] = j0;
+      s_meta[slot * 4 + 2] = icnt;
+      s_meta[slot * 4 + 3] = (int)iP;
+    }
+    if (p.idx) {
+      for (int e = tid; e < KT; e += NTH) {
+        const bool ok = j0 + e < icnt;
+        cp_async_4z(idx_base + (slot * KT + e) * 4, p.idx + iu * p.idx_ld + (ok ? j0 + e : 0), ok);
+        if (p.member)
+          cp_async_4z(mem_base + (slot * KT + e) * 4, p.member + iu * p.idx_ld + (ok ? j0 + e : 0), ok);
+      }
+    }
+  };
+
+  // ---- K/V gather (thread -> chunk g_ch of rows g_r0 + GROWS*j) ----
+  constexpr int GROWS = L::GROWS, GJ = L::GJ;
+  const int g_ch = tid % CH, g_r0 = tid / CH;
+  const int g_n = (KT - g_r0 + GROWS - 1) / GROWS;
+  const uint32_t g_dst = (uint32_t)(g_r0 * PITCH + g_ch * 16);
+  const uint32_t row_bytes = (uint32_t)p.row_stride * 2u;
+  int64_t g_u = -1;
+  const char* g_kb = nullptr;
+  const char* g_vb = nullptr;
+  auto issue_data = [&](int i) {
+    if (i >= ntile) return;
+    const int slot = i & (L::RING - 1), stage = i % STAGES;
+    const int64_t u = s_meta[slot * 4 + 0];
+    const int jb = s_meta[slot * 4 + 1], cu = s_meta[slot * 4 + 2];
+    if (u != g_u) {
+      g_u = u;
+      if (tid * 128 < M * D * 2)  // this unit's Q into L2 ahead of the math side
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const char*>(p.q) + u * (int64_t)M * D * 2 + tid * 128));
+      g_kb = static_cast<const char*>(p.k) + (u * p.kv_stride + g_ch * 8) * 2;
+      g_vb = static_cast<const char*>(p.v) + (u * p.kv_stride + g_ch * 8) * 2;
+    }
+    const uint32_t dst0 = stage_base + stage * L::STAGE + g_dst;
+    const int* ring = s_idx + slot * KT;
+    if (jb + KT <= cu) {
+#pragma unroll
+      for (int j = 0; j < GJ; ++j) {
+        if (KT % GROWS != 0 && j == GJ - 1 && j >= g_n) break;
+        const int r = g_r0 + j * GROWS;
+        const uint32_t pr = p.idx ? (uint32_t)ring[r] : (uint32_t)(jb + r);
+        const uint32_t dst = dst0 + j * GROWS * PITCH;
+        cp_async_16(dst, g_kb + (uint64_t)pr * row_bytes);
+        cp_async_16(dst + L::KV, g_vb + (uint64_t)pr * row_bytes);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < GJ; ++j) {
+        if (KT % GROWS != 0 && j == GJ - 1 && j >= g_n) break;
+        const int r = g_r0 + j * GROWS;
+        const bool ok = jb + r < cu;
+        const uint32_t pr = ok ? (p.idx ? (uint32_t)ring[r] : (uint32_t)(jb + r)) : 0u;
+        const uint32_t dst = dst0 + j * GROWS * PITCH;
+        cp_async_16_zfill(dst, g_kb + (uint64_t)pr * row_bytes, ok);
+        cp_async_16_zfill(dst + L::KV, g_vb + (uint64_t)pr * row_bytes, ok);
+      }
+    }
+  };
+
+  // ---- per-warp state: rows rA = 16*warp + lane/4 and rB = rA + 8 ----
+  const int rA = warp * 16 + (lane >> 2), rB = rA + 8;
+  const int rmodA = rA % p.rows_per_head, rmodB = rB % p.rows_per_head;
+  const float sl2 = p.scale * LOG2E;
+  const int causal_shift = p.pos_offset - p.causal_base;
+  const bool causal = p.causal_base >= 0;
+  float o[D / 8][4];
+  float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;
+  uint32_t qa[D / 16][4];
+  // ldmatrix lane offsets: K (B of QK^T, non-trans): key (lane&7), dim block (lane>>3)*8
+  const uint32_t offK = (uint32_t)((lane & 7) * PITCH + (lane >> 3) * 16);
+  // V (B of P.V, trans): key (lane&7) + ((lane>>3)&1)*8, dim block (lane>>4)*8
+  const uint32_t offV = (uint32_t)(((lane & 7) + ((lane >> 3) & 1) * 8) * PITCH + (lane >> 4) * 16);
+  int64_t cur_u = -1;
+  int cur_P = 0, cur_cnt = 0;
+
+  auto reset_state = [&]() {
+#pragma unroll
+    for (int a = 0; a < D / 8; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) o[a][c] = 0.f;
+    m_a = m_b = -INFINITY;
+    l_a = l_b = 0.f;
+  };
+  auto load_q = [&](int64_t u) {
+    const uint32_t* qA = reinterpret_cast<const uint32_t*>(static_cast<const __nv_bfloat16*>(p.q) +
+                                                           (u * M + rA) * (int64_t)D) + (lane & 3);
+    const uint32_t* qB = qA + 8 * D / 2;
+    const bool okA = rA < M, okB = rB < M;
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+      qa[kk][0] = okA ? __ldg(qA + kk * 8) : 0u;
+      qa[kk][1] = okB ? __ldg(qB + kk * 8) : 0u;
+      qa[kk][2] = okA ? __ldg(qA + kk * 8 + 4) : 0u;
+      qa[kk][3] = okB ? __ldg(qB + kk * 8 + 4) : 0u;
+    }
+  };
+
+  // ---- finish unit u for this CTA: final rows, or partial + last-CTA merge ----
+  auto flush = [&](int64_t u, int P_u, int cnt_u) {
+    float la = l_a, lb = l_b;
+    la += __shfl_xor_sync(0xffffffffu, la, 1);
+    la += __shfl_xor_sync(0xffffffffu, la, 2);
+    lb += __shfl_xor_sync(0xffffffffu, lb, 1);
+    lb += __shfl_xor_sync(0xffffffffu, lb, 2);
+    const int64_t tiles = (cnt_u + KT - 1) / KT;
+    const int wf = tile_owner(P_u, T, W);
+    const int wl = tile_owner(P_u + tiles - 1, T, W);
+    const bool single = wf == wl;
+    const int64_t pslot = (int64_t)w + u;
+    const float inv_a = la > 0.f ? 1.f / la : 0.f, inv_b = lb > 0.f ? 1.f / lb : 0.f;
+    const float lse_a = la > 0.f ? (m_a + __log2f(la)) * LN2 : -INFINITY;
+    const float lse_b = lb > 0.f ? (m_b + __log2f(lb)) * LN2 : -INFINITY;
+    const int dc = 2 * (lane & 3);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = h ? rB : rA;
+      if (r >= M) continue;
+      const float inv = h ? inv_b : inv_a;
+      if (single) {
+        if (p.out_f32) {
+          float* og = static_cast<float*>(p.out) + (u * M + r) * (int64_t)D + dc;
+#pragma unroll
+          for (int nt = 0; nt < D / 8; ++nt)
+            *reinterpret_cast<float2*>(og + nt * 8) = make_float2(o[nt][2 * h] * inv, o[nt][2 * h + 1] * inv);
+        } else {
+          __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + (u * M + r) * (int64_t)D + dc;
+#pragma unroll
+          for (int nt = 0; nt < D / 8; ++nt)
+            *reinterpret_cast<__nv_bfloat162*>(og + nt * 8) =
+                __floats2bfloat162_rn(o[nt][2 * h] * inv, o[nt][2 * h + 1] * inv);
+        }
+      } else {
+        float* og = p.o_part + (pslot * M + r) * (int64_t)D + dc;
+#pragma unroll
+        for (int nt = 0; nt < D / 8; ++nt)
+          *reinterpret_cast<float2*>(og + nt * 8) = make_float2(o[nt][2 * h] * inv, o[nt][2 * h + 1] * inv);
+      }
+      if ((lane & 3) == 0) {
+        const float lse = h ? lse_b : lse_a;
+        const bool empty = !((h ? lb : la) > 0.f);
+        if (single) {
+          if (p.lse) p.lse[u * M + r] = lse;
+          if (empty) set_status(p.status, STS_DEV_EMPTY_ROW);
+        } else {
+          p.l_part[pslot * M + r] = lse;
+        }
+      }
+    }
+    if (single) return;  // uniform across the CTA
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      const int old = atomicAdd(p.counters + u, 1);
+      const int last = old == wl - wf;
+      if (last) __threadfence();
+      *s_flag = last;
+    }
+    __syncthreads();
+    const int last = *s_flag;
+    if (!last) return;
+    // merge CTAs wf..wl in order (independent loads, batches of 8 / 4)
+    const int n = wl - wf + 1;
+    const float* lp = p.l_part + ((int64_t)wf + u) * M;
+    for (int r = tid; r < M; r += NTH) {
+      float mstar = -INFINITY;
+      for (int w0 = 0; w0 < n; w0 += 8) {
+        float l8[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) l8[j] = w0 + j < n ? __ldcg(lp + (int64_t)(w0 + j) * M + r) : -INFINITY;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) mstar = fmaxf(mstar, l8[j]);
+      }
+      float tot = 0.f;
+      if (mstar != -INFINITY)
+        for (int w0 = 0; w0 < n; w0 += 8) {
+          float l8[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) l8[j] = w0 + j < n ? __ldcg(lp + (int64_t)(w0 + j) * M + r) : -INFINITY;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) tot += l8[j] == -INFINITY ? 0.f : expf(l8[j] - mstar);
+        }
+      if (p.lse) p.lse[u * M + r] = tot > 0.f ? mstar + logf(tot) : -INFINITY;
+      if (!(tot > 0.f)) set_status(p.status, STS_DEV_EMPTY_ROW);
+      s_merge[r * 2 + 0] = mstar;
+      s_merge[r * 2 + 1] = tot > 0.f ? 1.f / tot : 0.f;
+    }
+    __syncthreads();
+    // O: each thread owns elements e0 + j*NTH (j < EPT); per batch of 4 partials
+    // it issues all EPT*4 float4 + LSE loads before using any of them
+    constexpr int D4 = D / 4, EPT = 2;
+    const float* op = p.o_part + ((int64_t)wf + u) * M * D;
+    for (int e0 = tid; e0 < M * D4; e0 += EPT * NTH) {
+      float4 acc[EPT];
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int w0 = 0; w0 < n; w0 += 4) {
+        float l4[EPT][4];
+        float4 x4[EPT][4];
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) {
+          const int e = e0 + j * NTH;
+          const int r = e / D4, d4 = e % D4;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const bool ok = e < M * D4 && w0 + k < n;
+            l4[j][k] = ok ? __ldcg(lp + (int64_t)(w0 + k) * M + r) : -INFINITY;
+            x4[j][k] = ok ? __ldcg(reinterpret_cast<const float4*>(op + ((int64_t)(w0 + k) * M + r) * D) + d4)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < EPT; ++j) {
+          const int e = e0 + j * NTH;
+          const int r = e < M * D4 ? e / D4 : 0;
+          const float mstar = s_merge[r * 2], inv = s_merge[r * 2 + 1];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const float f = l4[j][k] == -INFINITY ? 0.f : expf(l4[j][k] - mstar) * inv;
+            acc[j].x += f * x4[j][k].x;
+            acc[j].y += f * x4[j][k].y;
+            acc[j].z += f * x4[j][k].z;
+            acc[j].w += f * x4[j][k].w;
+          }
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < EPT; ++j) {
+        const int e = e0 + j * NTH;
+        if (e >= M * D4) continue;
+        const int r = e / D4, d4 = e % D4;
+        if (p.out_f32) {
+          *reinterpret_cast<float4*>(static_cast<float*>(p.out) + (u * M + r) * (int64_t)D + 4 * d4) = acc[j];
+        } else {
+          __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + (u * M + r) * (int64_t)D + 4 * d4;
+          *reinterpret_cast<__nv_bfloat162*>(og) = __floats2bfloat162_rn(acc[j].x, acc[j].y);
+          *reinterpret_cast<__nv_bfloat162*>(og + 2) = __floats2bfloat162_rn(acc[j].z, acc[j].w);
+        }
+      }
+    }
+    __syncthreads();
+  };
+
+  // ---- pipeline: idx slices STAGES tiles ahead, K/V STAGES-1 tiles ahead ----
+  STS_TRACE_AT(1);
+#ifdef STS_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 8192) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_trace[blockIdx.x * 8 + 7] = (unsigned long long)ntile | ((unsigned long long)smid << 32);
+  }
+#endif
+  for (int kk = 0; kk < STAGES; ++kk) issue_idx(kk);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+#pragma unroll
+  for (int s0 = 0; s0 < STAGES - 1; ++s0) {
+    issue_data(s0);
+    issue_idx(s0 + STAGES);
+    cp_async_commit();
+  }
+
+  for (int i = 0; i < ntile; ++i) {
+    const int slot = i & (L::RING - 1), stage = i % STAGES;
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    issue_data(i + STAGES - 1);
+    issue_idx(i + 2 * STAGES - 1);
+    cp_async_commit();
+
+#ifdef STS_TRACE
+    if (i == 0) STS_TRACE_AT(2);
+#endif
+    const int64_t u = s_meta[slot * 4 + 0];
+    const int j0 = s_meta[slot * 4 + 1];
+    if (u != cur_u) {
+#ifdef STS_TRACE
+      const unsigned long long tf0 = gtimer();
+#endif
+      if (cur_u >= 0) flush(cur_u, cur_P, cur_cnt);
+#ifdef STS_TRACE
+      if (cur_u >= 0) {
+        STS_TRACE_ADD(5, gtimer() - tf0);
+        STS_TRACE_ADD(6, 1);
+      }
+#endif
+      cur_u = u;
+      cur_cnt = s_meta[slot * 4 + 2];
+      cur_P = s_meta[slot * 4 + 3];
+      reset_state();
+      load_q(u);
+    }
+    const uint32_t sk = stage_base + stage * L::STAGE;
+    const int* ring = s_idx + slot * KT;
+    const int nvalid = cur_cnt - j0;  // keys of this tile that exist (>= 1)
+    // fast path: all keys valid, no membership bits, tile entirely at or
+    // before the causal base (positions ascending)
+    const int last_pos = p.idx ? ring[KT - 1] : j0 + KT - 1;
+    const bool simple = nvalid >= KT && !p.member && (!causal || last_pos + causal_shift <= 0);
+
+    // S = Q K^T : NT independent 16x8 accumulators
+    float s[NT][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) s[nt][c] = 0.f;
+      const uint32_t ak = sk + nt * 8 * PITCH + offK;
+#pragma unroll
+      for (int kk = 0; kk < D / 16; kk += 2) {
+        uint32_t b[4];
+        ldmatrix_x4(b[0], b[1], b[2], b[3], ak + kk * 32);
+        const uint32_t b0[2] = {b[0], b[1]}, b1[2] = {b[2], b[3]};
+        mma_bf16_16816(s[nt], qa[kk], b0);
+        mma_bf16_16816(s[nt], qa[kk + 1], b1);
+      }
+    }
+    // scale to log2 units; mask when needed
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) s[nt][c] *= sl2;
+    if (!simple) {
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int key = nt * 8 + 2 * (lane & 3) + e;
+          const bool valid = key < nvalid;
+          const int pos = valid ? (p.idx ? ring[key] : j0 + key) : 0;
+          const uint32_t mem = p.member ? s_mem[slot * KT + key] : 0xffffffffu;
+          bool okA = valid && ((mem >> (rA & 31)) & 1u);
+          bool okB = valid && ((mem >> (rB & 31)) & 1u);
+          if (causal) {
+            okA = okA && (pos + causal_shift <= rmodA);
+            okB = okB && (pos + causal_shift <= rmodB);
+          }
+          if (!okA) s[nt][e] = -INFINITY;
+          if (!okB) s[nt][2 + e] = -INFINITY;
+        }
+    }
+    // online softmax (rows rA: s[.][0..1], rB: s[.][2..3])
+    float tA = -INFINITY, tB = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      tA = fmaxf(tA, fmaxf(s[nt][0], s[nt][1]));
+      tB = fmaxf(tB, fmaxf(s[nt][2], s[nt][3]));
+    }
+    tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, 1));
+    tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 1));
+    tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, 2));
+    tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 2));
+    const float nA = fmaxf(m_a, tA), nB = fmaxf(m_b, tB);
+    // rows with no admissible key yet keep everything at zero
+    const float bA = nA == -INFINITY ? 0.f : nA, bB = nB == -INFINITY ? 0.f : nB;
+    const float alA = fast_exp2(m_a - bA), alB = fast_exp2(m_b - bB);
+    m_a = nA;
+    m_b = nB;
+    float sumA = 0.f, sumB = 0.f;
+    uint32_t pa[KS][4];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      const float p0 = fast_exp2(s[nt][0] - bA), p1 = fast_exp2(s[nt][1] - bA);
+      const float p2 = fast_exp2(s[nt][2] - bB), p3 = fast_exp2(s[nt][3] - bB);
+      sumA += p0 + p1;
+      sumB += p2 + p3;
+      pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(p0, p1);
+      pa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(p2, p3);
+    }
+    l_a = l_a * alA + sumA;
+    l_b = l_b * alB + sumB;
+    if (__any_sync(0xffffffffu, alA != 1.f || alB != 1.f)) {
+#pragma unroll
+      for (int nt = 0; nt < D / 8; ++nt) {
+        o[nt][0] *= alA;
+        o[nt][1] *= alA;
+        o[nt][2] *= alB;
+        o[nt][3] *= alB;
+      }
+    }
+    // O += P V
+#pragma unroll
+    for (int ks = 0; ks < KS; ++ks) {
+      const uint32_t av = sk + L::KV + ks * 16 * PITCH + offV;
+#pragma unroll
+      for (int n2 = 0; n2 < D / 16; ++n2) {
+        uint32_t b[4];
+        ldmatrix_x4_trans(b[0], b[1], b[2], b[3], av + n2 * 32);
+        const uint32_t b0[2] = {b[0], b[1]}, b1[2] = {b[2], b[3]};
+        mma_bf16_16816(o[2 * n2], pa[ks], b0);
+        mma_bf16_16816(o[2 * n2 + 1], pa[ks], b1);
+      }
+    }
+  }
+  cp_async_wait<0>();
+  STS_TRACE_AT(3);
+  if (cur_u >= 0) flush(cur_u, cur_P, cur_cnt);
+  STS_TRACE_AT(4);
+}
+
+template <int D, int NW, int KT, int STAGES>
+int launch_verify(DecodeParams& p, cudaStream_t st) {
+  using L = VL<D, NW, KT, STAGES>;
+  static_assert(L::SMEM <= 227 * 1024, "verify decode shared memory");
+  auto kern = verify_decode_kernel<D, NW, KT, STAGES>;
+  static const int per_sm = [&]() {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM) != cudaSuccess) return -1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, L::THREADS, L::SMEM) != cudaSuccess) return -1;
+    return n < 1 ? 1 : n;
+  }();
+  STS_REQUIRE(per_sm > 0, STS_ERR_CUDA, "verify decode kernel setup failed: %s",
+              cudaGetErrorString(cudaGetLastError()));
+  kern<<<num_sms() * per_sm, L::THREADS, L::SMEM, st>>>(p);
+  STS_LAUNCH_CHECK();
+  return STS_OK;
+}
+
+#ifndef STS_VERIFY_KT
+#define STS_VERIFY_KT 32
+#endif
+#ifndef STS_VERIFY_STAGES
+#define STS_VERIFY_STAGES 2
+#endif
+
+// pipeline shape of the d=128, M in (16, 32] decode (the c2 / c4 headline):
+// STS_VERIFY_CFG = 0 (default) 32-key tiles x2 stages, 1: 32x3, 2: 16x4, 3: 16x3, 4: 64x2
+int verify_cfg() {
+  static int cfg = -1;
+  if (cfg < 0) {
+    const char* e = getenv("STS_VERIFY_CFG");
+    cfg = e ? atoi(e) : 0;
+    if (cfg < 0 || cfg > 4) cfg = 0;
+  }
+  return cfg;
+}
+
+template <int D>
+int verify_dispatch(DecodeParams& p, cudaStream_t st) {
+  constexpr int KT = STS_VERIFY_KT, S = STS_VERIFY_STAGES;
+  if constexpr (D == 128) {
+    if ((p.M + 15) / 16 == 2) {
+      switch (verify_cfg()) {
+        case 1: return launch_verify<D, 2, 32, 3>(p, st);
+        case 2: return launch_verify<D, 2, 16, 4>(p, st);
+        case 3: return launch_verify<D, 2, 16, 3>(p, st);
+        case 4: return launch_verify<D, 2, 64, 2>(p, st);
+        default: break;
+      }
+    }
+  }
+  switch ((p.M + 15) / 16) {
+    case 1: return launch_verify<D, 1, KT, S>(p, st);
+    case 2: return launch_verify<D, 2, KT, S>(p, st);
+    case 3: return launch_verify<D, 3, KT, S>(p, st);
+    default:
+      set_error("bf16 sparse decode supports M <= 48 stacked rows, got %d", p.M);
+      return STS_ERR_CONTRACT;
+  }
+}
+
+}  // namespace
+
+#ifdef STS_TRACE
+extern "C" STS_API int sts_debug_trace(void* host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, g_trace, bytes < sizeof(g_trace) ? bytes : sizeof(g_trace)) == cudaSuccess ? 0 : 3;
+}
+#endif
+
+size_t verify_decode_smem_probe() { return VL<128, 2, STS_VERIFY_KT, STS_VERIFY_STAGES>::SMEM; }
+
+int verify_decode_launch(DecodeParams& p, cudaStream_t st) {
+  if (p.d == 128) return verify_dispatch<128>(p, st);
+  if (p.d == 64) return verify_dispatch<64>(p, st);
+  set_error("bf16 sparse decode supports d in {64, 128}, got %d", p.d);
+  return STS_ERR_CONTRACT;
+}
+
+}  // namespace sts
