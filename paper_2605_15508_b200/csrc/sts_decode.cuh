@@ -43,6 +43,16 @@ struct DecodeParams {
   int idx_cap;
   // stream-K bookkeeping (sts_stream.cu)
   int* counters;        // [units], zeroed before each launch
+  // verify kernels: sched[0] = dynamic chunk counter (zeroed per launch);
+  // pieces[u] = (first, last) schedule range holding unit u's tiles, written
+  // by the kernel, read by the piece-merge kernel; pref_units = units whose
+  // tile prefix fits in shared memory (dynamic tail enabled), else 0
+  int* sched;
+  int2* pieces;
+  int pref_units;
+  int nch_max;
+  int dyn_chunk;        // minimum tiles per dynamic chunk
+  float dyn_frac;       // fraction of all tiles scheduled dynamically
 };
 
 // Persistent stream-K launch of the bf16 gather kernel in `mode`.
@@ -54,8 +64,11 @@ int lse_merge_launch(const float* o_part, const float* lse_part, int nparts, int
                      int out_dtype, void* out, float* lse_out, cudaStream_t st);
 
 int auto_splits(int64_t units, int64_t keys_per_unit);
-// bf16 decode of the stacked verification rows (sts_verify_decode.cu)
-int verify_decode_launch(DecodeParams& p, cudaStream_t st);
+// bf16 decode of the stacked verification rows (sts_verify_decode.cu): the
+// main kernel, then the merge of units split over several schedule ranges
+int verify_decode_launch(int mode, DecodeParams& p, cudaStream_t st);
+// shared-memory tile prefix the dynamic tail can afford (units)
+constexpr int VERIFY_PREF_MAX_UNITS = 4095;
 int gather_launch(int mode, DecodeParams& p, cudaStream_t st);
 
 }  // namespace sts

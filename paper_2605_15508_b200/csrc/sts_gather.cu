@@ -700,13 +700,11 @@ int gdispatch_d(DecodeParams& p, cudaStream_t st) {
 }  // namespace
 
 int gather_launch(int mode, DecodeParams& p, cudaStream_t st) {
-  if (mode == MODE_DECODE) {
-    // product path: sts_verify_decode.cu; STS_DECODE_LEGACY=1 selects the
-    // row-split kernel below (kept for A/B measurements)
-    static const bool legacy = getenv("STS_DECODE_LEGACY") && atoi(getenv("STS_DECODE_LEGACY")) == 1;
-    if (!legacy) return verify_decode_launch(p, st);
-    return gdispatch_d<MODE_DECODE>(p, st);
-  }
+  // product path: sts_verify_decode.cu; STS_DECODE_LEGACY=1 selects the
+  // row-split kernels below (kept for A/B measurements)
+  static const bool legacy = getenv("STS_DECODE_LEGACY") && atoi(getenv("STS_DECODE_LEGACY")) == 1;
+  if (!legacy) return verify_decode_launch(mode, p, st);
+  if (mode == MODE_DECODE) return gdispatch_d<MODE_DECODE>(p, st);
   if (mode == MODE_LSE) return gdispatch_d<MODE_LSE>(p, st);
   return gdispatch_d<MODE_PROBS>(p, st);
 }

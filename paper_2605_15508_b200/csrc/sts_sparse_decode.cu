@@ -205,6 +205,11 @@ extern "C" int sts_sparse_decode(int32_t dtype, int32_t out_dtype, const void* q
   p.out_ld = 0;
   p.probs_mode = 0;
   p.counters = nullptr;
+  p.sched = nullptr;
+  p.pieces = nullptr;
+  p.pref_units = 0;
+  p.nch_max = p.dyn_chunk = 0;
+  p.dyn_frac = 0.f;
   if (dtype == STS_DTYPE_BF16) {
     // persistent stream-K kernel; `splits` does not apply
     return stream_launch(MODE_DECODE, p, workspace_dev, workspace_bytes, st);

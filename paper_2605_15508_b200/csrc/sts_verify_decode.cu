@@ -57,24 +57,27 @@ __device__ __forceinline__ int unit_tiles(const DecodeParams& p, int64_t u, int 
   return (c + KT - 1) / KT;
 }
 
-__device__ __forceinline__ int tile_owner(int64_t t, int64_t T, int W) { return (int)(((t + 1) * W - 1) / T); }
 
-template <int D, int NW, int KT, int STAGES>
+template <int D, int NW, int KT, int STAGES, int MODE>
 struct VL {
+  static constexpr bool K_ONLY = MODE != MODE_DECODE;
   static constexpr int THREADS = NW * 32;
   static constexpr int CH = D / 8;                // 16-byte chunks per row
   static constexpr int PITCH = D * 2 + 16;        // padded row
   static constexpr int KV = KT * PITCH;           // K block -> V block
-  static constexpr int STAGE = 2 * KV;
+  static constexpr int STAGE = (K_ONLY ? 1 : 2) * KV;
+  static constexpr int MP = NW * 16;              // padded stacked rows
+  static constexpr int KPS = KT + 4;              // staged probability row pitch (floats)
+  static constexpr int PROB = MODE == MODE_PROBS ? MP * KPS * 4 : 0;  // staged probabilities [row][key]
   static constexpr int RING = STAGES <= 2 ? 4 : 8;  // index ring (power of 2, >= 2*STAGES)
   static constexpr int IDX_BYTES = RING * KT * 4;
-  static constexpr int META_BYTES = RING * 16;
+  static constexpr int META_BYTES = RING * 32;
   static constexpr int MERGE = NW * 16 * 2 * 4;
-  static constexpr int SMEM = STAGES * STAGE + 2 * IDX_BYTES + META_BYTES + MERGE + 16;
+  static constexpr int SMEM = STAGES * STAGE + 2 * IDX_BYTES + META_BYTES + MERGE + PROB + 16;
   // resident CTAs per SM the register allocation must allow: the shared-memory
   // limit, capped so a warp keeps ~168 registers (O, Q fragments, S, P)
   static constexpr int SMEM_CTAS = (227 * 1024) / (SMEM + 1024);
-  static constexpr int REG_CTAS = NW == 1 ? 12 : (NW == 2 ? 6 : 3);
+  static constexpr int REG_CTAS = K_ONLY ? 16 / NW : (NW == 1 ? 12 : (NW == 2 ? 6 : 3));
   static constexpr int MINB = SMEM_CTAS < REG_CTAS ? (SMEM_CTAS < 1 ? 1 : SMEM_CTAS) : REG_CTAS;
   static constexpr int GROWS = THREADS / CH;      // rows per gather pass
   static constexpr int GJ = (KT + GROWS - 1) / GROWS;
@@ -82,9 +85,9 @@ struct VL {
   static_assert(KT % 16 == 0, "key tile");
 };
 
-template <int D, int NW, int KT, int STAGES>
-__global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES>::MINB)) verify_decode_kernel(DecodeParams p) {
-  using L = VL<D, NW, KT, STAGES>;
+template <int D, int NW, int KT, int STAGES, int MODE>
+__global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) verify_decode_kernel(DecodeParams p) {
+  using L = VL<D, NW, KT, STAGES, MODE>;
   constexpr int NTH = L::THREADS, PITCH = L::PITCH, CH = L::CH;
   constexpr int NT = KT / 8;   // 8-key n-tiles of S per tile
   constexpr int KS = KT / 16;  // 16-key k-steps of P.V per tile
@@ -104,8 +107,9 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES>::MINB)) verify
   int* s_idx = reinterpret_cast<int*>(s_stage + STAGES * L::STAGE);
   uint32_t* s_mem = reinterpret_cast<uint32_t*>(s_idx + L::RING * KT);
   int* s_meta = reinterpret_cast<int*>(s_mem + L::RING * KT);
-  float* s_merge = reinterpret_cast<float*>(s_meta + L::RING * 4);
-  int* s_flag = reinterpret_cast<int*>(s_merge + L::MERGE / 4);
+  float* s_merge = reinterpret_cast<float*>(s_meta + L::RING * 8);
+  float* s_prob = s_merge + L::MERGE / 4;
+  int* s_flag = reinterpret_cast<int*>(s_prob + L::PROB / 4);
   const uint32_t stage_base = smem_u32(s_stage);
   const uint32_t idx_base = smem_u32(s_idx);
   const uint32_t mem_base = smem_u32(s_mem);
@@ -113,14 +117,17 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES>::MINB)) verify
   // ---- units with no keys (striped over CTAs): zero rows, LSE -inf ----
   for (int64_t u = blockIdx.x; u < U; u += gridDim.x) {
     if (unit_tiles(p, u, KT) != 0) continue;
-    if (p.out_f32) {
-      float* og = static_cast<float*>(p.out) + u * (int64_t)M * D;
-      for (int e = tid; e < M * D; e += NTH) og[e] = 0.f;
-    } else {
-      __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + u * (int64_t)M * D;
-      for (int e = tid; e < M * D; e += NTH) og[e] = __float2bfloat16_rn(0.f);
+    if constexpr (MODE == MODE_PROBS) continue;
+    if constexpr (MODE == MODE_DECODE) {
+      if (p.out_f32) {
+        float* og = static_cast<float*>(p.out) + u * (int64_t)M * D;
+        for (int e = tid; e < M * D; e += NTH) og[e] = 0.f;
+      } else {
+        __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + u * (int64_t)M * D;
+        for (int e = tid; e < M * D; e += NTH) og[e] = __float2bfloat16_rn(0.f);
+      }
+      if (tid == 0 && M > 0) set_status(p.status, STS_DEV_EMPTY_ROW);
     }
-    if (tid == 0 && M > 0) set_status(p.status, STS_DEV_EMPTY_ROW);
     if (p.lse)
       for (int r = tid; r < M; r += NTH) p.lse[u * M + r] = -INFINITY;
   }
@@ -153,57 +160,159 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES>::MINB)) verify
     T += v;
   }
   if (T == 0) return;
-  const int W = (int)(T < (int64_t)gridDim.x ? T : (int64_t)gridDim.x);
+
+  // ---- schedule: a static head (one contiguous range per CTA, stream-K) and
+  // a dynamic tail of fixed chunks claimed through an atomic counter, so
+  // CTAs on faster SMs take more of the tail.  Ranges are ordered by tile
+  // position (static ranges 0..W_s-1, then chunks), a piece of a unit is
+  // (range, unit) and its partial slot is range + unit: merges run in range
+  // order, so results do not depend on which CTA claimed which chunk.
+  // The schedule and the tile cursor live in shared memory and only thread 0
+  // moves the cursor (keeps them out of every thread's registers).
+  struct Cursor {
+    long long T_s, C, NCH, W_s;      // schedule
+    long long t, end, range;         // current range [t, end)
+    long long iu, iP, iPn;           // unit walk
+    int icnt, done;
+  };
+  __shared__ Cursor cs;
   const int w = blockIdx.x;
-  if (w >= W) return;
-  const int64_t s_w = (int64_t)w * T / W;
-  const int64_t e_w = (int64_t)(w + 1) * T / W;
-  const int ntile = (int)(e_w - s_w);
-  {
+  // tile prefix of every unit in shared memory (after the pipeline buffers),
+  // so thread 0 maps a claimed chunk to its unit with a binary search
+  int* s_pref = reinterpret_cast<int*>(smem + L::SMEM);
+  const bool use_pref = p.pref_units == U && U > 0;
+  if (tid == 0) {
+    const bool dyn = use_pref && p.sched != nullptr && p.dyn_frac > 0.f && T > 1;
+    const long long T_d = dyn ? (long long)((double)T * (double)p.dyn_frac) : 0;
+    cs.T_s = T - T_d;
+    cs.C = T_d > 0 ? max((long long)p.dyn_chunk, (T_d + p.nch_max - 1) / p.nch_max) : 1;
+    cs.NCH = T_d > 0 ? (T_d + cs.C - 1) / cs.C : 0;
+    cs.W_s = cs.T_s < (long long)gridDim.x ? cs.T_s : (long long)gridDim.x;
+    cs.done = 0;
+    if (use_pref) s_pref[U] = (int)T;
+  }
+  if (use_pref) {
+    int64_t b = before + incl - mine;
+    for (int64_t u = ub; u < ue; ++u) {
+      s_pref[u] = (int)b;
+      b += unit_tiles(p, u, KT);
+    }
+  }
+  __syncthreads();
+  if (w >= cs.W_s && cs.NCH == 0) return;
+  // range id of global tile t (static ranges, then chunks)
+  auto owner = [&](int64_t t) -> int64_t {
+    return t < cs.T_s ? ((t + 1) * cs.W_s - 1) / cs.T_s : cs.W_s + (t - cs.T_s) / cs.C;
+  };
+
+  // thread 0: claim of the next range, overlapped with the current one.  The
+  // claimed chunk, its unit and the unit's count stay in registers until the
+  // range ends, so the atomic's and the load's latencies are not waited on.
+  int nx_state = 0;  // 0 none, 1 claim issued, 2 unit found + count requested
+  unsigned nx_c = 0;
+  int nx_u = 0, nx_cnt = 0;
+  auto claim_step = [&]() {
+    if (cs.NCH == 0) return;
+    if (nx_state == 0) {
+      nx_c = atomicAdd(reinterpret_cast<unsigned*>(p.sched), 1u);
+      nx_state = 1;
+    } else if (nx_state == 1) {
+      if (nx_c < (unsigned)cs.NCH) {
+        const int t = (int)(cs.T_s + (long long)nx_c * cs.C);
+        int lo = 0, hi = (int)U;  // largest u with s_pref[u] <= t (a unit with tiles)
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (s_pref[mid] <= t) lo = mid;
+          else hi = mid;
+        }
+        nx_u = lo;
+        nx_cnt = p.idx ? __ldg(p.cnt + lo) : p.n_dense;
+      }
+      nx_state = 2;
+    }
+  };
+  auto enter_next = [&]() {  // thread 0
+    if (cs.NCH == 0) {  // static schedule only: the CTA's range was its work
+      cs.done = 1;
+      return;
+    }
+    while (nx_state < 2) claim_step();
+    if (nx_c >= (unsigned)cs.NCH) {
+      cs.done = 1;
+      return;
+    }
+    cs.range = cs.W_s + nx_c;
+    cs.t = cs.T_s + (long long)nx_c * cs.C;
+    cs.end = cs.t + cs.C < T ? cs.t + cs.C : T;
+    cs.iu = nx_u;
+    cs.iP = s_pref[nx_u];
+    cs.icnt = nx_cnt;
+    cs.iPn = cs.iP + (cs.icnt + KT - 1) / KT;
+    nx_state = 0;
+  };
+  if (w < cs.W_s) {
+    const long long s0 = (long long)w * cs.T_s / cs.W_s;
     int64_t acc = before + incl - mine;
-    if (acc <= s_w && s_w < acc + mine) {
+    if (acc <= s0 && s0 < acc + mine) {
       for (int64_t u = ub; u < ue; ++u) {
         const int t_u = unit_tiles(p, u, KT);
-        if (s_w < acc + t_u) {
-          s_scan[NW] = u;
-          s_scan[NW + 1] = acc;
-          s_scan[NW + 2] = p.idx ? p.cnt[u] : p.n_dense;  // (an L1 hit: just loaded)
+        if (s0 < acc + t_u) {
+          cs.t = s0;
+          cs.end = (long long)(w + 1) * cs.T_s / cs.W_s;
+          cs.range = w;
+          cs.iu = u;
+          cs.iP = acc;
+          cs.icnt = p.idx ? p.cnt[u] : p.n_dense;  // (an L1 hit: just loaded)
+          cs.iPn = acc + t_u;
           break;
         }
         acc += t_u;
       }
     }
+  } else if (tid == 0) {
+    enter_next();  // no static range: claim the first chunk now
   }
   __syncthreads();
-  int64_t iu = s_scan[NW], iP = s_scan[NW + 1];
-  int icnt = (int)s_scan[NW + 2];
-  int64_t iPn = iP + (icnt + KT - 1) / KT;
 
-  // ---- index slices: tile i -> ring slot i & (RING-1) (+ meta) ----
+  // ---- index slices: tile i of this CTA -> ring slot i & (RING-1) (+ meta).
+  // Thread 0 moves the cursor and writes the slot's meta; warp 0 copies the
+  // slot's indices (callers order consecutive calls with a barrier).
   auto issue_idx = [&](int i) {
     const int slot = i & (L::RING - 1);
-    if (i >= ntile) return;
-    const int64_t t = s_w + i;
-    while (t >= iPn) {
-      ++iu;
-      iP = iPn;
-      icnt = p.idx ? p.cnt[iu] : p.n_dense;
-      iPn = iP + (icnt + KT - 1) / KT;
-    }
-    const int j0 = (int)(t - iP) * KT;
-    if (tid == 0) {
-      s_meta[slot * 4 + 0] = (int)iu;
-      s_meta[slot * 4 + 1] = j0;
-      s_meta[slot * 4 + 2] = icnt;
-      s_meta[slot * 4 + 3] = (int)iP;
-    }
-    if (p.idx) {
-      for (int e = tid; e < KT; e += NTH) {
-        const bool ok = j0 + e < icnt;
-        cp_async_4z(idx_base + (slot * KT + e) * 4, p.idx + iu * p.idx_ld + (ok ? j0 + e : 0), ok);
-        if (p.member)
-          cp_async_4z(mem_base + (slot * KT + e) * 4, p.member + iu * p.idx_ld + (ok ? j0 + e : 0), ok);
+    int* meta = s_meta + slot * 8;
+    if (warp != 0) return;
+    if (lane == 0) {
+      if (!cs.done && cs.t == cs.end) enter_next();
+      if (cs.done) {
+        meta[0] = -1;
+      } else {
+        const long long t = cs.t;
+        while (t >= cs.iPn && cs.iu + 1 < U) {
+          ++cs.iu;
+          cs.iP = cs.iPn;
+          cs.icnt = p.idx ? p.cnt[cs.iu] : p.n_dense;
+          cs.iPn = cs.iP + (cs.icnt + KT - 1) / KT;
+        }
+        meta[0] = (int)cs.iu;
+        meta[1] = (int)(t - cs.iP) * KT;
+        meta[2] = cs.icnt;
+        meta[3] = (int)cs.iP;
+        meta[4] = (int)cs.range;
+        ++cs.t;
+        // claim the next range only near the end of this one (claims made
+        // early would hand out the dynamic tail before anyone knows who is fast)
+        if (cs.end - cs.t <= 3) claim_step();
       }
+    }
+    __syncwarp();
+    const int u = meta[0];
+    if (u < 0 || !p.idx) return;
+    const int j0 = meta[1], cu = meta[2];
+    for (int e = lane; e < KT; e += 32) {
+      const bool ok = j0 + e < cu;
+      cp_async_4z(idx_base + (slot * KT + e) * 4, p.idx + (int64_t)u * p.idx_ld + (ok ? j0 + e : 0), ok);
+      if (p.member)
+        cp_async_4z(mem_base + (slot * KT + e) * 4, p.member + (int64_t)u * p.idx_ld + (ok ? j0 + e : 0), ok);
     }
   };
 
@@ -217,16 +326,16 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES>::MINB)) verify
   const char* g_kb = nullptr;
   const char* g_vb = nullptr;
   auto issue_data = [&](int i) {
-    if (i >= ntile) return;
     const int slot = i & (L::RING - 1), stage = i % STAGES;
-    const int64_t u = s_meta[slot * 4 + 0];
-    const int jb = s_meta[slot * 4 + 1], cu = s_meta[slot * 4 + 2];
+    const int64_t u = s_meta[slot * 8 + 0];
+    if (u < 0) return;
+    const int jb = s_meta[slot * 8 + 1], cu = s_meta[slot * 8 + 2];
     if (u != g_u) {
       g_u = u;
       if (tid * 128 < M * D * 2)  // this unit's Q into L2 ahead of the math side
         asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const char*>(p.q) + u * (int64_t)M * D * 2 + tid * 128));
       g_kb = static_cast<const char*>(p.k) + (u * p.kv_stride + g_ch * 8) * 2;
-      g_vb = static_cast<const char*>(p.v) + (u * p.kv_stride + g_ch * 8) * 2;
+      if constexpr (MODE == MODE_DECODE) g_vb = static_cast<const char*>(p.v) + (u * p.kv_stride + g_ch * 8) * 2;
     }
     const uint32_t dst0 = stage_base + stage * L::STAGE + g_dst;
     const int* ring = s_idx + slot * KT;
@@ -238,7 +347,7 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES>::MINB)) verify
         const uint32_t pr = p.idx ? (uint32_t)ring[r] : (uint32_t)(jb + r);
         const uint32_t dst = dst0 + j * GROWS * PITCH;
         cp_async_16(dst, g_kb + (uint64_t)pr * row_bytes);
-        cp_async_16(dst + L::KV, g_vb + (uint64_t)pr * row_bytes);
+        if constexpr (MODE == MODE_DECODE) cp_async_16(dst + L::KV, g_vb + (uint64_t)pr * row_bytes);
       }
     } else {
 #pragma unroll
@@ -249,7 +358,7 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES>::MINB)) verify
         const uint32_t pr = ok ? (p.idx ? (uint32_t)ring[r] : (uint32_t)(jb + r)) : 0u;
         const uint32_t dst = dst0 + j * GROWS * PITCH;
         cp_async_16_zfill(dst, g_kb + (uint64_t)pr * row_bytes, ok);
-        cp_async_16_zfill(dst + L::KV, g_vb + (uint64_t)pr * row_bytes, ok);
+        if constexpr (MODE == MODE_DECODE) cp_async_16_zfill(dst + L::KV, g_vb + (uint64_t)pr * row_bytes, ok);
       }
     }
   };
@@ -260,8 +369,9 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES>::MINB)) verify
   const float sl2 = p.scale * LOG2E;
   const int causal_shift = p.pos_offset - p.causal_base;
   const bool causal = p.causal_base >= 0;
-  float o[D / 8][4];
+  float o[MODE == MODE_DECODE ? D / 8 : 1][4];
   float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;
+  float lse2A = 0.f, lse2B = 0.f;  // MODE_PROBS: the rows' LSE in log2 units
   uint32_t qa[D / 16][4];
   // ldmatrix lane offsets: K (B of QK^T, non-trans): key (lane&7), dim block (lane>>3)*8
   const uint32_t offK = (uint32_t)((lane & 7) * PITCH + (lane >> 3) * 16);
@@ -272,7 +382,7 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES>::MINB)) verify
 
   auto reset_state = [&]() {
 #pragma unroll
-    for (int a = 0; a < D / 8; ++a)
+    for (int a = 0; a < (MODE == MODE_DECODE ? D / 8 : 1); ++a)
 #pragma unroll
       for (int c = 0; c < 4; ++c) o[a][c] = 0.f;
     m_a = m_b = -INFINITY;
@@ -290,20 +400,25 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES>::MINB)) verify
       qa[kk][2] = okA ? __ldg(qA + kk * 8 + 4) : 0u;
       qa[kk][3] = okB ? __ldg(qB + kk * 8 + 4) : 0u;
     }
+    if constexpr (MODE == MODE_PROBS) {
+      lse2A = okA ? p.lse_in[u * M + rA] * LOG2E : 0.f;
+      lse2B = okB ? p.lse_in[u * M + rB] * LOG2E : 0.f;
+    }
   };
 
   // ---- finish unit u for this CTA: final rows, or partial + last-CTA merge ----
-  auto flush = [&](int64_t u, int P_u, int cnt_u) {
+  auto flush = [&](int64_t u, int P_u, int cnt_u, int64_t range) {
+    if constexpr (MODE == MODE_PROBS) return;  // probabilities are written per tile
     float la = l_a, lb = l_b;
     la += __shfl_xor_sync(0xffffffffu, la, 1);
     la += __shfl_xor_sync(0xffffffffu, la, 2);
     lb += __shfl_xor_sync(0xffffffffu, lb, 1);
     lb += __shfl_xor_sync(0xffffffffu, lb, 2);
     const int64_t tiles = (cnt_u + KT - 1) / KT;
-    const int wf = tile_owner(P_u, T, W);
-    const int wl = tile_owner(P_u + tiles - 1, T, W);
+    const int64_t wf = owner(P_u);
+    const int64_t wl = owner(P_u + tiles - 1);
     const bool single = wf == wl;
-    const int64_t pslot = (int64_t)w + u;
+    const int64_t pslot = range + u;
     const float inv_a = la > 0.f ? 1.f / la : 0.f, inv_b = lb > 0.f ? 1.f / lb : 0.f;
     const float lse_a = la > 0.f ? (m_a + __log2f(la)) * LN2 : -INFINITY;
     const float lse_b = lb > 0.f ? (m_b + __log2f(lb)) * LN2 : -INFINITY;
@@ -313,7 +428,9 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES>::MINB)) verify
       const int r = h ? rB : rA;
       if (r >= M) continue;
       const float inv = h ? inv_b : inv_a;
-      if (single) {
+      if constexpr (MODE != MODE_DECODE) {
+        (void)inv;
+      } else if (single) {
         if (p.out_f32) {
           float* og = static_cast<float*>(p.out) + (u * M + r) * (int64_t)D + dc;
 #pragma unroll
@@ -337,104 +454,15 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES>::MINB)) verify
         const bool empty = !((h ? lb : la) > 0.f);
         if (single) {
           if (p.lse) p.lse[u * M + r] = lse;
-          if (empty) set_status(p.status, STS_DEV_EMPTY_ROW);
+          if (MODE == MODE_DECODE && empty) set_status(p.status, STS_DEV_EMPTY_ROW);
         } else {
           p.l_part[pslot * M + r] = lse;
         }
       }
     }
-    if (single) return;  // uniform across the CTA
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) {
-      const int old = atomicAdd(p.counters + u, 1);
-      const int last = old == wl - wf;
-      if (last) __threadfence();
-      *s_flag = last;
-    }
-    __syncthreads();
-    const int last = *s_flag;
-    if (!last) return;
-    // merge CTAs wf..wl in order (independent loads, batches of 8 / 4)
-    const int n = wl - wf + 1;
-    const float* lp = p.l_part + ((int64_t)wf + u) * M;
-    for (int r = tid; r < M; r += NTH) {
-      float mstar = -INFINITY;
-      for (int w0 = 0; w0 < n; w0 += 8) {
-        float l8[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) l8[j] = w0 + j < n ? __ldcg(lp + (int64_t)(w0 + j) * M + r) : -INFINITY;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) mstar = fmaxf(mstar, l8[j]);
-      }
-      float tot = 0.f;
-      if (mstar != -INFINITY)
-        for (int w0 = 0; w0 < n; w0 += 8) {
-          float l8[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j) l8[j] = w0 + j < n ? __ldcg(lp + (int64_t)(w0 + j) * M + r) : -INFINITY;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) tot += l8[j] == -INFINITY ? 0.f : expf(l8[j] - mstar);
-        }
-      if (p.lse) p.lse[u * M + r] = tot > 0.f ? mstar + logf(tot) : -INFINITY;
-      if (!(tot > 0.f)) set_status(p.status, STS_DEV_EMPTY_ROW);
-      s_merge[r * 2 + 0] = mstar;
-      s_merge[r * 2 + 1] = tot > 0.f ? 1.f / tot : 0.f;
-    }
-    __syncthreads();
-    // O: each thread owns elements e0 + j*NTH (j < EPT); per batch of 4 partials
-    // it issues all EPT*4 float4 + LSE loads before using any of them
-    constexpr int D4 = D / 4, EPT = 2;
-    const float* op = p.o_part + ((int64_t)wf + u) * M * D;
-    for (int e0 = tid; e0 < M * D4; e0 += EPT * NTH) {
-      float4 acc[EPT];
-#pragma unroll
-      for (int j = 0; j < EPT; ++j) acc[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int w0 = 0; w0 < n; w0 += 4) {
-        float l4[EPT][4];
-        float4 x4[EPT][4];
-#pragma unroll
-        for (int j = 0; j < EPT; ++j) {
-          const int e = e0 + j * NTH;
-          const int r = e / D4, d4 = e % D4;
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const bool ok = e < M * D4 && w0 + k < n;
-            l4[j][k] = ok ? __ldcg(lp + (int64_t)(w0 + k) * M + r) : -INFINITY;
-            x4[j][k] = ok ? __ldcg(reinterpret_cast<const float4*>(op + ((int64_t)(w0 + k) * M + r) * D) + d4)
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < EPT; ++j) {
-          const int e = e0 + j * NTH;
-          const int r = e < M * D4 ? e / D4 : 0;
-          const float mstar = s_merge[r * 2], inv = s_merge[r * 2 + 1];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float f = l4[j][k] == -INFINITY ? 0.f : expf(l4[j][k] - mstar) * inv;
-            acc[j].x += f * x4[j][k].x;
-            acc[j].y += f * x4[j][k].y;
-            acc[j].z += f * x4[j][k].z;
-            acc[j].w += f * x4[j][k].w;
-          }
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < EPT; ++j) {
-        const int e = e0 + j * NTH;
-        if (e >= M * D4) continue;
-        const int r = e / D4, d4 = e % D4;
-        if (p.out_f32) {
-          *reinterpret_cast<float4*>(static_cast<float*>(p.out) + (u * M + r) * (int64_t)D + 4 * d4) = acc[j];
-        } else {
-          __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + (u * M + r) * (int64_t)D + 4 * d4;
-          *reinterpret_cast<__nv_bfloat162*>(og) = __floats2bfloat162_rn(acc[j].x, acc[j].y);
-          *reinterpret_cast<__nv_bfloat162*>(og + 2) = __floats2bfloat162_rn(acc[j].z, acc[j].w);
-        }
-      }
-    }
-    __syncthreads();
+    // the piece holding the unit's first tile records the unit's range span;
+    // split units are merged by merge_pieces_kernel after this kernel
+    if (range == wf && tid == 0) p.pieces[u] = make_int2((int)wf, (int)wl);
   };
 
   // ---- pipeline: idx slices STAGES tiles ahead, K/V STAGES-1 tiles ahead ----
@@ -443,21 +471,26 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES>::MINB)) verify
   if (threadIdx.x == 0 && blockIdx.x < 8192) {
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    g_trace[blockIdx.x * 8 + 7] = (unsigned long long)ntile | ((unsigned long long)smid << 32);
+    g_trace[blockIdx.x * 8 + 7] = (unsigned long long)(cs.end - cs.t) | ((unsigned long long)smid << 32);
   }
 #endif
-  for (int kk = 0; kk < STAGES; ++kk) issue_idx(kk);
+  for (int kk = 0; kk < STAGES; ++kk) {
+    if (kk) __syncthreads();
+    issue_idx(kk);
+  }
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
 #pragma unroll
   for (int s0 = 0; s0 < STAGES - 1; ++s0) {
+    if (s0) __syncthreads();
     issue_data(s0);
     issue_idx(s0 + STAGES);
     cp_async_commit();
   }
 
-  for (int i = 0; i < ntile; ++i) {
+  int64_t cur_range = -1;
+  for (int i = 0;; ++i) {
     const int slot = i & (L::RING - 1), stage = i % STAGES;
     cp_async_wait<STAGES - 2>();
     __syncthreads();
@@ -468,24 +501,28 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES>::MINB)) verify
 #ifdef STS_TRACE
     if (i == 0) STS_TRACE_AT(2);
 #endif
-    const int64_t u = s_meta[slot * 4 + 0];
-    const int j0 = s_meta[slot * 4 + 1];
-    if (u != cur_u) {
+    const int64_t u = s_meta[slot * 8 + 0];
+    if (u < 0) break;
+    const int j0 = s_meta[slot * 8 + 1];
+    const int64_t range = s_meta[slot * 8 + 4];
+    if (u != cur_u || range != cur_range) {
 #ifdef STS_TRACE
       const unsigned long long tf0 = gtimer();
 #endif
-      if (cur_u >= 0) flush(cur_u, cur_P, cur_cnt);
+      if (cur_u >= 0) flush(cur_u, cur_P, cur_cnt, cur_range);
 #ifdef STS_TRACE
       if (cur_u >= 0) {
         STS_TRACE_ADD(5, gtimer() - tf0);
         STS_TRACE_ADD(6, 1);
       }
 #endif
+      const bool new_unit = u != cur_u;
       cur_u = u;
-      cur_cnt = s_meta[slot * 4 + 2];
-      cur_P = s_meta[slot * 4 + 3];
+      cur_range = range;
+      cur_cnt = s_meta[slot * 8 + 2];
+      cur_P = s_meta[slot * 8 + 3];
       reset_state();
-      load_q(u);
+      if (new_unit) load_q(u);
     }
     const uint32_t sk = stage_base + stage * L::STAGE;
     const int* ring = s_idx + slot * KT;
@@ -511,104 +548,237 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES>::MINB)) verify
         mma_bf16_16816(s[nt], qa[kk + 1], b1);
       }
     }
-    // scale to log2 units; mask when needed
+    // scale to log2 units
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
       for (int c = 0; c < 4; ++c) s[nt][c] *= sl2;
-    if (!simple) {
+
+    if constexpr (MODE == MODE_PROBS) {
+      // p = 2^(s - lse) staged as s_prob[row][key], then written per row
+      // (mode R) or summed over each head's speculative rows in row order
+      // (mode S, committed positions only); one thread per key, no divides
+      constexpr int KPS = L::KPS;
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int key = nt * 8 + 2 * (lane & 3) + e;
-          const bool valid = key < nvalid;
-          const int pos = valid ? (p.idx ? ring[key] : j0 + key) : 0;
-          const uint32_t mem = p.member ? s_mem[slot * KT + key] : 0xffffffffu;
-          bool okA = valid && ((mem >> (rA & 31)) & 1u);
-          bool okB = valid && ((mem >> (rB & 31)) & 1u);
-          if (causal) {
-            okA = okA && (pos + causal_shift <= rmodA);
-            okB = okB && (pos + causal_shift <= rmodB);
-          }
-          if (!okA) s[nt][e] = -INFINITY;
-          if (!okB) s[nt][2 + e] = -INFINITY;
-        }
-    }
-    // online softmax (rows rA: s[.][0..1], rB: s[.][2..3])
-    float tA = -INFINITY, tB = -INFINITY;
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      tA = fmaxf(tA, fmaxf(s[nt][0], s[nt][1]));
-      tB = fmaxf(tB, fmaxf(s[nt][2], s[nt][3]));
-    }
-    tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, 1));
-    tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 1));
-    tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, 2));
-    tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 2));
-    const float nA = fmaxf(m_a, tA), nB = fmaxf(m_b, tB);
-    // rows with no admissible key yet keep everything at zero
-    const float bA = nA == -INFINITY ? 0.f : nA, bB = nB == -INFINITY ? 0.f : nB;
-    const float alA = fast_exp2(m_a - bA), alB = fast_exp2(m_b - bB);
-    m_a = nA;
-    m_b = nB;
-    float sumA = 0.f, sumB = 0.f;
-    uint32_t pa[KS][4];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      const float p0 = fast_exp2(s[nt][0] - bA), p1 = fast_exp2(s[nt][1] - bA);
-      const float p2 = fast_exp2(s[nt][2] - bB), p3 = fast_exp2(s[nt][3] - bB);
-      sumA += p0 + p1;
-      sumB += p2 + p3;
-      pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(p0, p1);
-      pa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(p2, p3);
-    }
-    l_a = l_a * alA + sumA;
-    l_b = l_b * alB + sumB;
-    if (__any_sync(0xffffffffu, alA != 1.f || alB != 1.f)) {
-#pragma unroll
-      for (int nt = 0; nt < D / 8; ++nt) {
-        o[nt][0] *= alA;
-        o[nt][1] *= alA;
-        o[nt][2] *= alB;
-        o[nt][3] *= alB;
+      for (int nt = 0; nt < NT; ++nt) {
+        const int key = nt * 8 + 2 * (lane & 3);
+        *reinterpret_cast<float2*>(s_prob + rA * KPS + key) =
+            make_float2(fast_exp2(s[nt][0] - lse2A), fast_exp2(s[nt][1] - lse2A));
+        *reinterpret_cast<float2*>(s_prob + rB * KPS + key) =
+            make_float2(fast_exp2(s[nt][2] - lse2B), fast_exp2(s[nt][3] - lse2B));
       }
-    }
-    // O += P V
+      __syncthreads();
+      const int R = p.rows_per_head;
+      const int G = M / R;
+      const int lim = p.causal_base - p.pos_offset;  // committed: pos < lim
+      for (int key = tid; key < KT; key += NTH) {
+        if (key >= nvalid) continue;
+        const int pos = p.idx ? ring[key] : j0 + key;
+        if (p.probs_mode == 0) {
+          if (pos >= lim) continue;
+          float* outp = p.probs_out + (u * G) * p.out_ld + j0 + key;
+          for (int hh = 0; hh < G; ++hh) {
+            const float* sp = s_prob + hh * R * KPS + key;
+            float acc = sp[0];
+            for (int ii = 1; ii < R; ++ii) acc = __fadd_rn(acc, sp[ii * KPS]);
+            outp[hh * p.out_ld] = acc;
+          }
+        } else {
+          float* outp = p.probs_out + (u * M) * p.out_ld + j0 + key;
+          for (int r = 0; r < M; ++r)
+            if (pos <= lim + r % R) outp[r * p.out_ld] = s_prob[r * KPS + key];
+        }
+      }
+      // the next iteration's loop-top barrier orders these reads before reuse
+    } else {
+      if (!simple) {
 #pragma unroll
-    for (int ks = 0; ks < KS; ++ks) {
-      const uint32_t av = sk + L::KV + ks * 16 * PITCH + offV;
+        for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int n2 = 0; n2 < D / 16; ++n2) {
-        uint32_t b[4];
-        ldmatrix_x4_trans(b[0], b[1], b[2], b[3], av + n2 * 32);
-        const uint32_t b0[2] = {b[0], b[1]}, b1[2] = {b[2], b[3]};
-        mma_bf16_16816(o[2 * n2], pa[ks], b0);
-        mma_bf16_16816(o[2 * n2 + 1], pa[ks], b1);
+          for (int e = 0; e < 2; ++e) {
+            const int key = nt * 8 + 2 * (lane & 3) + e;
+            const bool valid = key < nvalid;
+            const int pos = valid ? (p.idx ? ring[key] : j0 + key) : 0;
+            const uint32_t mem = p.member ? s_mem[slot * KT + key] : 0xffffffffu;
+            bool okA = valid && ((mem >> (rA & 31)) & 1u);
+            bool okB = valid && ((mem >> (rB & 31)) & 1u);
+            if (causal) {
+              okA = okA && (pos + causal_shift <= rmodA);
+              okB = okB && (pos + causal_shift <= rmodB);
+            }
+            if (!okA) s[nt][e] = -INFINITY;
+            if (!okB) s[nt][2 + e] = -INFINITY;
+          }
+      }
+      // online softmax (rows rA: s[.][0..1], rB: s[.][2..3])
+      float tA = -INFINITY, tB = -INFINITY;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        tA = fmaxf(tA, fmaxf(s[nt][0], s[nt][1]));
+        tB = fmaxf(tB, fmaxf(s[nt][2], s[nt][3]));
+      }
+      tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, 1));
+      tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 1));
+      tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, 2));
+      tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 2));
+      const float nA = fmaxf(m_a, tA), nB = fmaxf(m_b, tB);
+      // rows with no admissible key yet keep everything at zero
+      const float bA = nA == -INFINITY ? 0.f : nA, bB = nB == -INFINITY ? 0.f : nB;
+      const float alA = fast_exp2(m_a - bA), alB = fast_exp2(m_b - bB);
+      m_a = nA;
+      m_b = nB;
+      float sumA = 0.f, sumB = 0.f;
+      uint32_t pa[KS][4];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        const float p0 = fast_exp2(s[nt][0] - bA), p1 = fast_exp2(s[nt][1] - bA);
+        const float p2 = fast_exp2(s[nt][2] - bB), p3 = fast_exp2(s[nt][3] - bB);
+        sumA += p0 + p1;
+        sumB += p2 + p3;
+        if constexpr (MODE == MODE_DECODE) {
+          pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(p0, p1);
+          pa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(p2, p3);
+        }
+      }
+      l_a = l_a * alA + sumA;
+      l_b = l_b * alB + sumB;
+      if constexpr (MODE == MODE_DECODE) {
+        if (__any_sync(0xffffffffu, alA != 1.f || alB != 1.f)) {
+#pragma unroll
+          for (int nt = 0; nt < D / 8; ++nt) {
+            o[nt][0] *= alA;
+            o[nt][1] *= alA;
+            o[nt][2] *= alB;
+            o[nt][3] *= alB;
+          }
+        }
+        // O += P V
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const uint32_t av = sk + L::KV + ks * 16 * PITCH + offV;
+#pragma unroll
+          for (int n2 = 0; n2 < D / 16; ++n2) {
+            uint32_t b[4];
+            ldmatrix_x4_trans(b[0], b[1], b[2], b[3], av + n2 * 32);
+            const uint32_t b0[2] = {b[0], b[1]}, b1[2] = {b[2], b[3]};
+            mma_bf16_16816(o[2 * n2], pa[ks], b0);
+            mma_bf16_16816(o[2 * n2 + 1], pa[ks], b1);
+          }
+        }
       }
     }
   }
   cp_async_wait<0>();
   STS_TRACE_AT(3);
-  if (cur_u >= 0) flush(cur_u, cur_P, cur_cnt);
+  if (cur_u >= 0) flush(cur_u, cur_P, cur_cnt, cur_range);
   STS_TRACE_AT(4);
 }
 
-template <int D, int NW, int KT, int STAGES>
+// Merge of the units whose tiles were split over several schedule ranges: one
+// CTA per unit, pieces in range order (deterministic), every load of a row's
+// pieces issued before any is used.
+constexpr int MERGE_THREADS = 128;
+
+template <int D, int MODE>
+__global__ void __launch_bounds__(MERGE_THREADS) merge_pieces_kernel(DecodeParams p) {
+  __shared__ float s_row[48 * 2];
+  const int64_t u = blockIdx.x;
+  const int M = p.M;
+  if ((p.idx ? p.cnt[u] : p.n_dense) <= 0) return;
+  const int2 pr = p.pieces[u];
+  const int n = pr.y - pr.x + 1;
+  if (n <= 1) return;
+  const float* lp = p.l_part + ((int64_t)pr.x + u) * M;  // piece k at lp + k*M
+  for (int r = threadIdx.x; r < M; r += MERGE_THREADS) {
+    float mstar = -INFINITY, tot = 0.f;
+    for (int k0 = 0; k0 < n; k0 += 8) {
+      float l8[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) l8[j] = k0 + j < n ? __ldcg(lp + (int64_t)(k0 + j) * M + r) : -INFINITY;
+      float m8 = mstar;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) m8 = fmaxf(m8, l8[j]);
+      if (m8 != -INFINITY) {
+        tot = mstar == -INFINITY ? 0.f : tot * expf(mstar - m8);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) tot += l8[j] == -INFINITY ? 0.f : expf(l8[j] - m8);
+        mstar = m8;
+      }
+    }
+    if (p.lse) p.lse[u * M + r] = tot > 0.f ? mstar + logf(tot) : -INFINITY;
+    if (MODE == MODE_DECODE && !(tot > 0.f)) set_status(p.status, STS_DEV_EMPTY_ROW);
+    s_row[r * 2 + 0] = mstar;
+    s_row[r * 2 + 1] = tot > 0.f ? 1.f / tot : 0.f;
+  }
+  if constexpr (MODE != MODE_DECODE) return;
+  __syncthreads();
+  constexpr int D4 = D / 4;
+  const float* op = p.o_part + ((int64_t)pr.x + u) * M * D;
+  for (int e = threadIdx.x; e < M * D4; e += MERGE_THREADS) {
+    const int r = e / D4, d4 = e % D4;
+    const float mstar = s_row[r * 2], inv = s_row[r * 2 + 1];
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (inv > 0.f) {
+      for (int k0 = 0; k0 < n; k0 += 8) {
+        float l8[8];
+        float4 x8[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const bool ok = k0 + j < n;
+          l8[j] = ok ? __ldcg(lp + (int64_t)(k0 + j) * M + r) : -INFINITY;
+          x8[j] = ok ? __ldcg(reinterpret_cast<const float4*>(op + ((int64_t)(k0 + j) * M + r) * D) + d4)
+                     : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float f = l8[j] == -INFINITY ? 0.f : expf(l8[j] - mstar) * inv;
+          acc.x += f * x8[j].x;
+          acc.y += f * x8[j].y;
+          acc.z += f * x8[j].z;
+          acc.w += f * x8[j].w;
+        }
+      }
+    }
+    if (p.out_f32) {
+      *reinterpret_cast<float4*>(static_cast<float*>(p.out) + (u * M + r) * (int64_t)D + 4 * d4) = acc;
+    } else {
+      __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + (u * M + r) * (int64_t)D + 4 * d4;
+      *reinterpret_cast<__nv_bfloat162*>(og) = __floats2bfloat162_rn(acc.x, acc.y);
+      *reinterpret_cast<__nv_bfloat162*>(og + 2) = __floats2bfloat162_rn(acc.z, acc.w);
+    }
+  }
+}
+
+template <int D, int NW, int KT, int STAGES, int MODE>
 int launch_verify(DecodeParams& p, cudaStream_t st) {
-  using L = VL<D, NW, KT, STAGES>;
-  static_assert(L::SMEM <= 227 * 1024, "verify decode shared memory");
-  auto kern = verify_decode_kernel<D, NW, KT, STAGES>;
-  static const int per_sm = [&]() {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM) != cudaSuccess) return -1;
-    int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, L::THREADS, L::SMEM) != cudaSuccess) return -1;
-    return n < 1 ? 1 : n;
-  }();
-  STS_REQUIRE(per_sm > 0, STS_ERR_CUDA, "verify decode kernel setup failed: %s",
-              cudaGetErrorString(cudaGetLastError()));
-  kern<<<num_sms() * per_sm, L::THREADS, L::SMEM, st>>>(p);
+  using L = VL<D, NW, KT, STAGES, MODE>;
+  constexpr int PREF_MAX = ((VERIFY_PREF_MAX_UNITS + 1) * 4 + 15) & ~15;
+  static_assert(L::SMEM + PREF_MAX <= 227 * 1024, "verify decode shared memory");
+  auto kern = verify_decode_kernel<D, NW, KT, STAGES, MODE>;
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM + PREF_MAX);
+  STS_CUDA_CHECK(attr);
+  if (MODE == MODE_PROBS || !p.pieces) p.pref_units = 0;
+  const int smem = L::SMEM + (p.pref_units > 0 ? ((p.pref_units + 1) * 4 + 15) & ~15 : 0);
+  // resident CTAs for this shared-memory size (host-side query, cached per size)
+  static int cache_smem[4] = {-1, -1, -1, -1}, cache_n[4];
+  int per_sm = -1;
+  for (int k = 0; k < 4; ++k)
+    if (cache_smem[k] == smem) per_sm = cache_n[k];
+  if (per_sm < 0) {
+    STS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::THREADS, smem));
+    if (per_sm < 1) per_sm = 1;
+    static int next = 0;
+    cache_smem[next & 3] = smem;
+    cache_n[next & 3] = per_sm;
+    ++next;
+  }
+  kern<<<num_sms() * per_sm, L::THREADS, smem, st>>>(p);
   STS_LAUNCH_CHECK();
+  if (MODE != MODE_PROBS && p.pieces) {
+    merge_pieces_kernel<D, MODE><<<(unsigned)p.units, MERGE_THREADS, 0, st>>>(p);
+    STS_LAUNCH_CHECK();
+  }
   return STS_OK;
 }
 
@@ -617,6 +787,13 @@ int launch_verify(DecodeParams& p, cudaStream_t st) {
 #endif
 #ifndef STS_VERIFY_STAGES
 #define STS_VERIFY_STAGES 2
+#endif
+// draft capture (K only, contiguous keys): bigger tiles, deeper pipeline
+#ifndef STS_DRAFT_KT
+#define STS_DRAFT_KT 64
+#endif
+#ifndef STS_DRAFT_STAGES
+#define STS_DRAFT_STAGES 4
 #endif
 
 // pipeline shape of the d=128, M in (16, 32] decode (the c2 / c4 headline):
@@ -631,28 +808,37 @@ int verify_cfg() {
   return cfg;
 }
 
-template <int D>
+template <int D, int MODE>
 int verify_dispatch(DecodeParams& p, cudaStream_t st) {
-  constexpr int KT = STS_VERIFY_KT, S = STS_VERIFY_STAGES;
-  if constexpr (D == 128) {
+  constexpr bool DEC = MODE == MODE_DECODE;
+  constexpr int KT = DEC ? STS_VERIFY_KT : STS_DRAFT_KT, S = DEC ? STS_VERIFY_STAGES : STS_DRAFT_STAGES;
+  if constexpr (D == 128 && DEC) {
     if ((p.M + 15) / 16 == 2) {
       switch (verify_cfg()) {
-        case 1: return launch_verify<D, 2, 32, 3>(p, st);
-        case 2: return launch_verify<D, 2, 16, 4>(p, st);
-        case 3: return launch_verify<D, 2, 16, 3>(p, st);
-        case 4: return launch_verify<D, 2, 64, 2>(p, st);
+        case 1: return launch_verify<D, 2, 32, 3, MODE>(p, st);
+        case 2: return launch_verify<D, 2, 16, 4, MODE>(p, st);
+        case 3: return launch_verify<D, 2, 16, 3, MODE>(p, st);
+        case 4: return launch_verify<D, 2, 64, 2, MODE>(p, st);
         default: break;
       }
     }
   }
   switch ((p.M + 15) / 16) {
-    case 1: return launch_verify<D, 1, KT, S>(p, st);
-    case 2: return launch_verify<D, 2, KT, S>(p, st);
-    case 3: return launch_verify<D, 3, KT, S>(p, st);
+    case 1: return launch_verify<D, 1, KT, S, MODE>(p, st);
+    case 2: return launch_verify<D, 2, KT, S, MODE>(p, st);
+    case 3: return launch_verify<D, 3, KT, S, MODE>(p, st);
     default:
-      set_error("bf16 sparse decode supports M <= 48 stacked rows, got %d", p.M);
+      set_error("bf16 gather kernels support M <= 48 stacked rows, got %d", p.M);
       return STS_ERR_CONTRACT;
   }
+}
+
+template <int MODE>
+int verify_dispatch_d(DecodeParams& p, cudaStream_t st) {
+  if (p.d == 128) return verify_dispatch<128, MODE>(p, st);
+  if (p.d == 64) return verify_dispatch<64, MODE>(p, st);
+  set_error("bf16 gather kernels support d in {64, 128}, got %d", p.d);
+  return STS_ERR_CONTRACT;
 }
 
 }  // namespace
@@ -663,13 +849,10 @@ extern "C" STS_API int sts_debug_trace(void* host, size_t bytes) {
 }
 #endif
 
-size_t verify_decode_smem_probe() { return VL<128, 2, STS_VERIFY_KT, STS_VERIFY_STAGES>::SMEM; }
-
-int verify_decode_launch(DecodeParams& p, cudaStream_t st) {
-  if (p.d == 128) return verify_dispatch<128>(p, st);
-  if (p.d == 64) return verify_dispatch<64>(p, st);
-  set_error("bf16 sparse decode supports d in {64, 128}, got %d", p.d);
-  return STS_ERR_CONTRACT;
+int verify_decode_launch(int mode, DecodeParams& p, cudaStream_t st) {
+  if (mode == MODE_DECODE) return verify_dispatch_d<MODE_DECODE>(p, st);
+  if (mode == MODE_LSE) return verify_dispatch_d<MODE_LSE>(p, st);
+  return verify_dispatch_d<MODE_PROBS>(p, st);
 }
 
 }  // namespace sts

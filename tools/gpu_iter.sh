@@ -4,10 +4,8 @@ timeout 900 python -m pytest tests -m gpu -x -q -p no:cacheprovider > gpurun_out
 B="python bench.py --steps 10 --warmup 3 --no-cpu-baseline"
 : > gpurun_out/iter.log
 for ctx in 32768; do echo "== ctx $ctx" >> gpurun_out/iter.log; timeout 300 $B --context $ctx >> gpurun_out/iter.log 2>&1; done
-echo "== eager" >> gpurun_out/iter.log; timeout 300 $B --eager >> gpurun_out/iter.log 2>&1
-for v in paper_2605_15508_b200/_lib/variants/*.so; do [ -f "$v" ] || continue; echo "== $v" >> gpurun_out/iter.log; STS_B200_LIB=$PWD/$v timeout 300 $B >> gpurun_out/iter.log 2>&1; done
-P="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --eager"
 echo "== legacy" >> gpurun_out/iter.log; STS_DECODE_LEGACY=1 timeout 300 $B >> gpurun_out/iter.log 2>&1
+P="python bench.py --steps 1 --warmup 3 --no-cpu-baseline --eager"
 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:verify_decode|gather_kernel" -s 12 -c 4 -o gpurun_out/prof_gather $P > gpurun_out/ncu_gather.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/ncu_gather.log
 tail -2 gpurun_out/pytest_gpu.log
