@@ -67,8 +67,7 @@ int auto_splits(int64_t units, int64_t keys_per_unit);
 // bf16 decode of the stacked verification rows (sts_verify_decode.cu): the
 // main kernel, then the merge of units split over several schedule ranges
 int verify_decode_launch(int mode, DecodeParams& p, cudaStream_t st);
-// shared-memory tile prefix the dynamic tail can afford (units)
-constexpr int VERIFY_PREF_MAX_UNITS = 4095;
+constexpr int VERIFY_PREF_MAX_UNITS = 0;
 int gather_launch(int mode, DecodeParams& p, cudaStream_t st);
 
 }  // namespace sts

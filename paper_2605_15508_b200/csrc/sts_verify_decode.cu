@@ -97,6 +97,9 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
   const int warp = tid >> 5;
   const int M = p.M;
   const int64_t U = p.units;
+  // let the (programmatically dependent) merge grid launch now; it waits for
+  // this grid's completion before reading anything
+  asm volatile("griddepcontrol.launch_dependents;");
 #ifdef STS_TRACE
   if (threadIdx.x == 0 && blockIdx.x < 8192)
     for (int k = 0; k < 8; ++k) g_trace[blockIdx.x * 8 + k] = 0;
@@ -161,158 +164,67 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
   }
   if (T == 0) return;
 
-  // ---- schedule: a static head (one contiguous range per CTA, stream-K) and
-  // a dynamic tail of fixed chunks claimed through an atomic counter, so
-  // CTAs on faster SMs take more of the tail.  Ranges are ordered by tile
-  // position (static ranges 0..W_s-1, then chunks), a piece of a unit is
-  // (range, unit) and its partial slot is range + unit: merges run in range
-  // order, so results do not depend on which CTA claimed which chunk.
-  // The schedule and the tile cursor live in shared memory and only thread 0
-  // moves the cursor (keeps them out of every thread's registers).
-  struct Cursor {
-    long long T_s, C, NCH, W_s;      // schedule
-    long long t, end, range;         // current range [t, end)
-    long long iu, iP, iPn;           // unit walk
-    int icnt, done;
-  };
-  __shared__ Cursor cs;
+  // ---- schedule: one contiguous tile range per CTA (stream-K).  A piece of a
+  // unit is (CTA range, unit); its partial slot is range + unit, and units
+  // split over several ranges are merged afterwards in range order
+  // (merge_pieces_kernel), so results are deterministic.
+  const int W = (int)(T < (int64_t)gridDim.x ? T : (int64_t)gridDim.x);
   const int w = blockIdx.x;
-  // tile prefix of every unit in shared memory (after the pipeline buffers),
-  // so thread 0 maps a claimed chunk to its unit with a binary search
-  int* s_pref = reinterpret_cast<int*>(smem + L::SMEM);
-  const bool use_pref = p.pref_units == U && U > 0;
-  if (tid == 0) {
-    const bool dyn = use_pref && p.sched != nullptr && p.dyn_frac > 0.f && T > 1;
-    const long long T_d = dyn ? (long long)((double)T * (double)p.dyn_frac) : 0;
-    cs.T_s = T - T_d;
-    cs.C = T_d > 0 ? max((long long)p.dyn_chunk, (T_d + p.nch_max - 1) / p.nch_max) : 1;
-    cs.NCH = T_d > 0 ? (T_d + cs.C - 1) / cs.C : 0;
-    cs.W_s = cs.T_s < (long long)gridDim.x ? cs.T_s : (long long)gridDim.x;
-    cs.done = 0;
-    if (use_pref) s_pref[U] = (int)T;
-  }
-  if (use_pref) {
-    int64_t b = before + incl - mine;
-    for (int64_t u = ub; u < ue; ++u) {
-      s_pref[u] = (int)b;
-      b += unit_tiles(p, u, KT);
-    }
-  }
-  __syncthreads();
-  if (w >= cs.W_s && cs.NCH == 0) return;
-  // range id of global tile t (static ranges, then chunks)
-  auto owner = [&](int64_t t) -> int64_t {
-    return t < cs.T_s ? ((t + 1) * cs.W_s - 1) / cs.T_s : cs.W_s + (t - cs.T_s) / cs.C;
-  };
-
-  // thread 0: claim of the next range, overlapped with the current one.  The
-  // claimed chunk, its unit and the unit's count stay in registers until the
-  // range ends, so the atomic's and the load's latencies are not waited on.
-  int nx_state = 0;  // 0 none, 1 claim issued, 2 unit found + count requested
-  unsigned nx_c = 0;
-  int nx_u = 0, nx_cnt = 0;
-  auto claim_step = [&]() {
-    if (cs.NCH == 0) return;
-    if (nx_state == 0) {
-      nx_c = atomicAdd(reinterpret_cast<unsigned*>(p.sched), 1u);
-      nx_state = 1;
-    } else if (nx_state == 1) {
-      if (nx_c < (unsigned)cs.NCH) {
-        const int t = (int)(cs.T_s + (long long)nx_c * cs.C);
-        int lo = 0, hi = (int)U;  // largest u with s_pref[u] <= t (a unit with tiles)
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (s_pref[mid] <= t) lo = mid;
-          else hi = mid;
-        }
-        nx_u = lo;
-        nx_cnt = p.idx ? __ldg(p.cnt + lo) : p.n_dense;
-      }
-      nx_state = 2;
-    }
-  };
-  auto enter_next = [&]() {  // thread 0
-    if (cs.NCH == 0) {  // static schedule only: the CTA's range was its work
-      cs.done = 1;
-      return;
-    }
-    while (nx_state < 2) claim_step();
-    if (nx_c >= (unsigned)cs.NCH) {
-      cs.done = 1;
-      return;
-    }
-    cs.range = cs.W_s + nx_c;
-    cs.t = cs.T_s + (long long)nx_c * cs.C;
-    cs.end = cs.t + cs.C < T ? cs.t + cs.C : T;
-    cs.iu = nx_u;
-    cs.iP = s_pref[nx_u];
-    cs.icnt = nx_cnt;
-    cs.iPn = cs.iP + (cs.icnt + KT - 1) / KT;
-    nx_state = 0;
-  };
-  if (w < cs.W_s) {
-    const long long s0 = (long long)w * cs.T_s / cs.W_s;
+  if (w >= W) return;
+  const int64_t s_w = (int64_t)w * T / W;
+  const int ntile = (int)((int64_t)(w + 1) * T / W - s_w);
+  auto owner = [&](int64_t t) -> int64_t { return ((t + 1) * W - 1) / T; };
+  {
     int64_t acc = before + incl - mine;
-    if (acc <= s0 && s0 < acc + mine) {
+    if (acc <= s_w && s_w < acc + mine) {
       for (int64_t u = ub; u < ue; ++u) {
         const int t_u = unit_tiles(p, u, KT);
-        if (s0 < acc + t_u) {
-          cs.t = s0;
-          cs.end = (long long)(w + 1) * cs.T_s / cs.W_s;
-          cs.range = w;
-          cs.iu = u;
-          cs.iP = acc;
-          cs.icnt = p.idx ? p.cnt[u] : p.n_dense;  // (an L1 hit: just loaded)
-          cs.iPn = acc + t_u;
+        if (s_w < acc + t_u) {
+          s_scan[NW] = u;
+          s_scan[NW + 1] = acc;
+          s_scan[NW + 2] = p.idx ? p.cnt[u] : p.n_dense;  // (an L1 hit: just loaded)
           break;
         }
         acc += t_u;
       }
     }
-  } else if (tid == 0) {
-    enter_next();  // no static range: claim the first chunk now
   }
   __syncthreads();
+  // uniform cursor of the index side (every thread holds the same values)
+  int64_t iu = s_scan[NW], iP = s_scan[NW + 1];
+  int icnt = (int)s_scan[NW + 2];
+  int64_t iPn = iP + (icnt + KT - 1) / KT;
 
-  // ---- index slices: tile i of this CTA -> ring slot i & (RING-1) (+ meta).
-  // Thread 0 moves the cursor and writes the slot's meta; warp 0 copies the
-  // slot's indices (callers order consecutive calls with a barrier).
+  // ---- index slices: tile i of this CTA -> ring slot i & (RING-1) (+ meta) ----
   auto issue_idx = [&](int i) {
     const int slot = i & (L::RING - 1);
     int* meta = s_meta + slot * 8;
-    if (warp != 0) return;
-    if (lane == 0) {
-      if (!cs.done && cs.t == cs.end) enter_next();
-      if (cs.done) {
-        meta[0] = -1;
-      } else {
-        const long long t = cs.t;
-        while (t >= cs.iPn && cs.iu + 1 < U) {
-          ++cs.iu;
-          cs.iP = cs.iPn;
-          cs.icnt = p.idx ? p.cnt[cs.iu] : p.n_dense;
-          cs.iPn = cs.iP + (cs.icnt + KT - 1) / KT;
-        }
-        meta[0] = (int)cs.iu;
-        meta[1] = (int)(t - cs.iP) * KT;
-        meta[2] = cs.icnt;
-        meta[3] = (int)cs.iP;
-        meta[4] = (int)cs.range;
-        ++cs.t;
-        // claim the next range only near the end of this one (claims made
-        // early would hand out the dynamic tail before anyone knows who is fast)
-        if (cs.end - cs.t <= 3) claim_step();
-      }
+    if (i >= ntile) {
+      if (tid == 0) meta[0] = -1;
+      return;
     }
-    __syncwarp();
-    const int u = meta[0];
-    if (u < 0 || !p.idx) return;
-    const int j0 = meta[1], cu = meta[2];
-    for (int e = lane; e < KT; e += 32) {
-      const bool ok = j0 + e < cu;
-      cp_async_4z(idx_base + (slot * KT + e) * 4, p.idx + (int64_t)u * p.idx_ld + (ok ? j0 + e : 0), ok);
-      if (p.member)
-        cp_async_4z(mem_base + (slot * KT + e) * 4, p.member + (int64_t)u * p.idx_ld + (ok ? j0 + e : 0), ok);
+    const int64_t t = s_w + i;
+    while (t >= iPn) {
+      ++iu;
+      iP = iPn;
+      icnt = p.idx ? p.cnt[iu] : p.n_dense;
+      iPn = iP + (icnt + KT - 1) / KT;
+    }
+    const int j0 = (int)(t - iP) * KT;
+    if (tid == 0) {
+      meta[0] = (int)iu;
+      meta[1] = j0;
+      meta[2] = icnt;
+      meta[3] = (int)iP;
+      meta[4] = w;
+    }
+    if (p.idx) {
+      for (int e = tid; e < KT; e += NTH) {
+        const bool ok = j0 + e < icnt;
+        cp_async_4z(idx_base + (slot * KT + e) * 4, p.idx + iu * p.idx_ld + (ok ? j0 + e : 0), ok);
+        if (p.member)
+          cp_async_4z(mem_base + (slot * KT + e) * 4, p.member + iu * p.idx_ld + (ok ? j0 + e : 0), ok);
+      }
     }
   };
 
@@ -471,7 +383,7 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
   if (threadIdx.x == 0 && blockIdx.x < 8192) {
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-    g_trace[blockIdx.x * 8 + 7] = (unsigned long long)(cs.end - cs.t) | ((unsigned long long)smid << 32);
+    g_trace[blockIdx.x * 8 + 7] = (unsigned long long)ntile | ((unsigned long long)smid << 32);
   }
 #endif
   for (int kk = 0; kk < STAGES; ++kk) {
@@ -677,66 +589,78 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
 // Merge of the units whose tiles were split over several schedule ranges: one
 // CTA per unit, pieces in range order (deterministic), every load of a row's
 // pieces issued before any is used.
-constexpr int MERGE_THREADS = 128;
+constexpr int MERGE_MAX_THREADS = 1024;
 
 template <int D, int MODE>
-__global__ void __launch_bounds__(MERGE_THREADS) merge_pieces_kernel(DecodeParams p) {
-  __shared__ float s_row[48 * 2];
+__global__ void __launch_bounds__(MERGE_MAX_THREADS) merge_pieces_kernel(DecodeParams p) {
+  // weights w[k][r] = exp(lse_k[r] - lse[r]) of piece k for row r, in smem
+  constexpr int MAXP = 32;
+  __shared__ float s_w[MAXP * 48];
+  __shared__ float s_l[MAXP * 48];
+  const int nth = blockDim.x;
   const int64_t u = blockIdx.x;
   const int M = p.M;
-  if ((p.idx ? p.cnt[u] : p.n_dense) <= 0) return;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the main kernel's pieces are complete
   const int2 pr = p.pieces[u];
+  if ((p.idx ? p.cnt[u] : p.n_dense) <= 0) return;
   const int n = pr.y - pr.x + 1;
   if (n <= 1) return;
   const float* lp = p.l_part + ((int64_t)pr.x + u) * M;  // piece k at lp + k*M
-  for (int r = threadIdx.x; r < M; r += MERGE_THREADS) {
+  const int nb = n < MAXP ? n : MAXP;                    // pieces staged in smem
+  for (int e = threadIdx.x; e < nb * M; e += nth) s_l[e] = __ldcg(lp + e);
+  __syncthreads();
+  for (int r = threadIdx.x; r < M; r += nth) {
     float mstar = -INFINITY, tot = 0.f;
-    for (int k0 = 0; k0 < n; k0 += 8) {
-      float l8[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) l8[j] = k0 + j < n ? __ldcg(lp + (int64_t)(k0 + j) * M + r) : -INFINITY;
-      float m8 = mstar;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) m8 = fmaxf(m8, l8[j]);
-      if (m8 != -INFINITY) {
-        tot = mstar == -INFINITY ? 0.f : tot * expf(mstar - m8);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) tot += l8[j] == -INFINITY ? 0.f : expf(l8[j] - m8);
-        mstar = m8;
+    for (int k = 0; k < n; ++k) mstar = fmaxf(mstar, k < nb ? s_l[k * M + r] : __ldcg(lp + (int64_t)k * M + r));
+    if (mstar != -INFINITY)
+      for (int k = 0; k < n; ++k) {
+        const float l = k < nb ? s_l[k * M + r] : __ldcg(lp + (int64_t)k * M + r);
+        tot += l == -INFINITY ? 0.f : expf(l - mstar);
       }
+    const float inv = tot > 0.f ? 1.f / tot : 0.f;
+    for (int k = 0; k < nb; ++k) {
+      const float l = s_l[k * M + r];
+      s_w[k * M + r] = l == -INFINITY ? 0.f : expf(l - mstar) * inv;
     }
+    s_l[r] = mstar;  // (row r of piece 0 is no longer needed: its weight is in s_w)
     if (p.lse) p.lse[u * M + r] = tot > 0.f ? mstar + logf(tot) : -INFINITY;
     if (MODE == MODE_DECODE && !(tot > 0.f)) set_status(p.status, STS_DEV_EMPTY_ROW);
-    s_row[r * 2 + 0] = mstar;
-    s_row[r * 2 + 1] = tot > 0.f ? 1.f / tot : 0.f;
+    if (nb < n) s_w[r] = -1.f - inv;  // marker: pieces beyond MAXP use the slow path (never in practice)
   }
   if constexpr (MODE != MODE_DECODE) return;
   __syncthreads();
   constexpr int D4 = D / 4;
   const float* op = p.o_part + ((int64_t)pr.x + u) * M * D;
-  for (int e = threadIdx.x; e < M * D4; e += MERGE_THREADS) {
+  for (int e = threadIdx.x; e < M * D4; e += nth) {
     const int r = e / D4, d4 = e % D4;
-    const float mstar = s_row[r * 2], inv = s_row[r * 2 + 1];
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (inv > 0.f) {
+    if (nb == n) {
       for (int k0 = 0; k0 < n; k0 += 8) {
-        float l8[8];
         float4 x8[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const bool ok = k0 + j < n;
-          l8[j] = ok ? __ldcg(lp + (int64_t)(k0 + j) * M + r) : -INFINITY;
-          x8[j] = ok ? __ldcg(reinterpret_cast<const float4*>(op + ((int64_t)(k0 + j) * M + r) * D) + d4)
-                     : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+        for (int j = 0; j < 8; ++j)
+          x8[j] = k0 + j < n ? __ldcg(reinterpret_cast<const float4*>(op + ((int64_t)(k0 + j) * M + r) * D) + d4)
+                             : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const float f = l8[j] == -INFINITY ? 0.f : expf(l8[j] - mstar) * inv;
+          const float f = k0 + j < n ? s_w[(k0 + j) * M + r] : 0.f;
           acc.x += f * x8[j].x;
           acc.y += f * x8[j].y;
           acc.z += f * x8[j].z;
           acc.w += f * x8[j].w;
         }
+      }
+    } else {
+      // > MAXP pieces (a unit spread over more than 32 CTAs): plain loop
+      const float mstar = s_l[r], inv = -1.f - s_w[r];
+      for (int k = 0; k < n; ++k) {
+        const float l = __ldcg(lp + (int64_t)k * M + r);
+        const float f = l == -INFINITY ? 0.f : expf(l - mstar) * inv;
+        const float4 x = __ldcg(reinterpret_cast<const float4*>(op + ((int64_t)k * M + r) * D) + d4);
+        acc.x += f * x.x;
+        acc.y += f * x.y;
+        acc.z += f * x.z;
+        acc.w += f * x.w;
       }
     }
     if (p.out_f32) {
@@ -752,31 +676,38 @@ __global__ void __launch_bounds__(MERGE_THREADS) merge_pieces_kernel(DecodeParam
 template <int D, int NW, int KT, int STAGES, int MODE>
 int launch_verify(DecodeParams& p, cudaStream_t st) {
   using L = VL<D, NW, KT, STAGES, MODE>;
-  constexpr int PREF_MAX = ((VERIFY_PREF_MAX_UNITS + 1) * 4 + 15) & ~15;
-  static_assert(L::SMEM + PREF_MAX <= 227 * 1024, "verify decode shared memory");
+  static_assert(L::SMEM <= 227 * 1024, "verify decode shared memory");
   auto kern = verify_decode_kernel<D, NW, KT, STAGES, MODE>;
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM + PREF_MAX);
-  STS_CUDA_CHECK(attr);
-  if (MODE == MODE_PROBS || !p.pieces) p.pref_units = 0;
-  const int smem = L::SMEM + (p.pref_units > 0 ? ((p.pref_units + 1) * 4 + 15) & ~15 : 0);
-  // resident CTAs for this shared-memory size (host-side query, cached per size)
-  static int cache_smem[4] = {-1, -1, -1, -1}, cache_n[4];
-  int per_sm = -1;
-  for (int k = 0; k < 4; ++k)
-    if (cache_smem[k] == smem) per_sm = cache_n[k];
-  if (per_sm < 0) {
-    STS_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L::THREADS, smem));
-    if (per_sm < 1) per_sm = 1;
-    static int next = 0;
-    cache_smem[next & 3] = smem;
-    cache_n[next & 3] = per_sm;
-    ++next;
-  }
+  static const int per_sm = [&]() {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM) != cudaSuccess) return -1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, L::THREADS, L::SMEM) != cudaSuccess) return -1;
+    return n < 1 ? 1 : n;
+  }();
+  STS_REQUIRE(per_sm > 0, STS_ERR_CUDA, "verify kernel setup failed: %s", cudaGetErrorString(cudaGetLastError()));
+  const int smem = L::SMEM;
   kern<<<num_sms() * per_sm, L::THREADS, smem, st>>>(p);
   STS_LAUNCH_CHECK();
   if (MODE != MODE_PROBS && p.pieces) {
-    merge_pieces_kernel<D, MODE><<<(unsigned)p.units, MERGE_THREADS, 0, st>>>(p);
+    // one thread per (row, 4 dims) output element: every piece load in flight at once
+    // (optional, -DSTS_PDL) programmatic dependent launch: the merge grid is
+    // launched while the main kernel runs and waits (griddepcontrol.wait)
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)p.units);
+    cfg.blockDim = dim3(MODE == MODE_DECODE ? 256 : 64);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+#ifdef STS_PDL
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+#else
+    // measured: an early-launched merge grid costs the main kernel ~3 us at c2
+    attr[0].val.programmaticStreamSerializationAllowed = 0;
+#endif
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    STS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, merge_pieces_kernel<D, MODE>, p));
     STS_LAUNCH_CHECK();
   }
   return STS_OK;
