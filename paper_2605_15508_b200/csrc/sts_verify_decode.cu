@@ -724,7 +724,7 @@ int launch_verify(DecodeParams& p, cudaStream_t st) {
 #define STS_DRAFT_KT 64
 #endif
 #ifndef STS_DRAFT_STAGES
-#define STS_DRAFT_STAGES 4
+#define STS_DRAFT_STAGES 2
 #endif
 
 // pipeline shape of the d=128, M in (16, 32] decode (the c2 / c4 headline):
@@ -739,10 +739,35 @@ int verify_cfg() {
   return cfg;
 }
 
+// pipeline shape of the d=64 draft capture (LSE / probability passes):
+// STS_DRAFT_CFG = 0 (default) 64-key tiles x2 stages, 1: 64x3, 2: 32x3, 3: 32x2, 4: 64x4
+// (measured at c2, LSE + probability passes: 64x2 247 us < 64x3 270 < 64x4 296
+//  < 32x4 297 < 32x3 306 < 128x2 316 < 128x3 415)
+int draft_cfg() {
+  static int cfg = -1;
+  if (cfg < 0) {
+    const char* e = getenv("STS_DRAFT_CFG");
+    cfg = e ? atoi(e) : 0;
+    if (cfg < 0 || cfg > 4) cfg = 0;
+  }
+  return cfg;
+}
+
 template <int D, int MODE>
 int verify_dispatch(DecodeParams& p, cudaStream_t st) {
   constexpr bool DEC = MODE == MODE_DECODE;
   constexpr int KT = DEC ? STS_VERIFY_KT : STS_DRAFT_KT, S = DEC ? STS_VERIFY_STAGES : STS_DRAFT_STAGES;
+  if constexpr (D == 64 && !DEC) {
+    if ((p.M + 15) / 16 == 2) {
+      switch (draft_cfg()) {
+        case 1: return launch_verify<D, 2, 64, 3, MODE>(p, st);
+        case 2: return launch_verify<D, 2, 32, 3, MODE>(p, st);
+        case 3: return launch_verify<D, 2, 32, 2, MODE>(p, st);
+        case 4: return launch_verify<D, 2, 64, 4, MODE>(p, st);
+        default: break;
+      }
+    }
+  }
   if constexpr (D == 128 && DEC) {
     if ((p.M + 15) / 16 == 2) {
       switch (verify_cfg()) {
