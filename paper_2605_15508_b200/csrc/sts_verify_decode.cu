@@ -52,6 +52,27 @@ __device__ __forceinline__ void cp_async_4z(uint32_t dst, const void* src, bool 
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(sz));
 }
 
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cta address -> the same offset in CTA `rank` of this cluster
+__device__ __forceinline__ uint32_t dsmem_map(uint32_t addr, unsigned rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float4 dsmem_ld4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr) : "memory");
+  return v;
+}
+
 __device__ __forceinline__ int unit_tiles(const DecodeParams& p, int64_t u, int KT) {
   const int c = p.idx ? p.cnt[u] : p.n_dense;
   return (c + KT - 1) / KT;
@@ -85,7 +106,7 @@ struct VL {
   static_assert(KT % 16 == 0, "key tile");
 };
 
-template <int D, int NW, int KT, int STAGES, int MODE>
+template <int D, int NW, int KT, int STAGES, int MODE, int CS>
 __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) verify_decode_kernel(DecodeParams p) {
   using L = VL<D, NW, KT, STAGES, MODE>;
   constexpr int NTH = L::THREADS, PITCH = L::PITCH, CH = L::CH;
@@ -162,19 +183,35 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
     before += ww < warp ? v : 0;
     T += v;
   }
-  if (T == 0) return;
+  if (T == 0) return;  // (a cluster's CTAs all see the same T)
 
-  // ---- schedule: one contiguous tile range per CTA (stream-K).  A piece of a
-  // unit is (CTA range, unit); its partial slot is range + unit, and units
-  // split over several ranges are merged afterwards in range order
-  // (merge_pieces_kernel), so results are deterministic.
-  const int W = (int)(T < (int64_t)gridDim.x ? T : (int64_t)gridDim.x);
-  const int w = blockIdx.x;
-  if (w >= W) return;
-  const int64_t s_w = (int64_t)w * T / W;
-  const int ntile = (int)((int64_t)(w + 1) * T / W - s_w);
-  auto owner = [&](int64_t t) -> int64_t { return ((t + 1) * W - 1) / T; };
-  {
+  // ---- schedule.  CS == 1: one contiguous tile range per CTA (stream-K); a
+  // piece of a unit is (CTA range, unit), its partial slot is range + unit, and
+  // units split over several ranges are merged afterwards in range order
+  // (merge_pieces_kernel) — deterministic.  CS > 1: a thread-block cluster of
+  // CS CTAs per unit, each taking an equal contiguous share of the unit's
+  // tiles; the shares are merged through distributed shared memory at the end
+  // (no global partials, no second kernel).
+  int W, w;
+  int64_t s_w, iu, iP;
+  int ntile, icnt;
+  [[maybe_unused]] unsigned crank = 0;
+  if constexpr (CS > 1) {
+    crank = cluster_rank();
+    iu = blockIdx.x / CS;
+    icnt = iu < U ? (p.idx ? p.cnt[iu] : p.n_dense) : 0;
+    const int64_t T_u = (icnt + KT - 1) / KT;
+    W = CS;
+    w = (int)crank;
+    s_w = (int64_t)w * T_u / CS;
+    ntile = (int)((int64_t)(w + 1) * T_u / CS - s_w);
+    iP = 0;
+  } else {
+    W = (int)(T < (int64_t)gridDim.x ? T : (int64_t)gridDim.x);
+    w = blockIdx.x;
+    if (w >= W) return;
+    s_w = (int64_t)w * T / W;
+    ntile = (int)((int64_t)(w + 1) * T / W - s_w);
     int64_t acc = before + incl - mine;
     if (acc <= s_w && s_w < acc + mine) {
       for (int64_t u = ub; u < ue; ++u) {
@@ -188,11 +225,13 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
         acc += t_u;
       }
     }
+    __syncthreads();
+    iu = s_scan[NW];
+    iP = s_scan[NW + 1];
+    icnt = (int)s_scan[NW + 2];
   }
-  __syncthreads();
+  auto owner = [&](int64_t t) -> int64_t { return ((t + 1) * W - 1) / T; };
   // uniform cursor of the index side (every thread holds the same values)
-  int64_t iu = s_scan[NW], iP = s_scan[NW + 1];
-  int icnt = (int)s_scan[NW + 2];
   int64_t iPn = iP + (icnt + KT - 1) / KT;
 
   // ---- index slices: tile i of this CTA -> ring slot i & (RING-1) (+ meta) ----
@@ -402,6 +441,7 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
   }
 
   int64_t cur_range = -1;
+  reset_state();  // (a cluster CTA with no tiles still contributes an empty share)
   for (int i = 0;; ++i) {
     const int slot = i & (L::RING - 1), stage = i % STAGES;
     cp_async_wait<STAGES - 2>();
@@ -582,7 +622,84 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
   }
   cp_async_wait<0>();
   STS_TRACE_AT(3);
-  if (cur_u >= 0) flush(cur_u, cur_P, cur_cnt, cur_range);
+  if constexpr (CS > 1) {
+    // ---- merge the cluster's shares of the unit through DSMEM ----
+    if constexpr (MODE != MODE_PROBS) {
+      constexpr int NO = MODE == MODE_DECODE ? D / 8 : 0;  // float4 of O per thread
+      float la = l_a, lb = l_b;
+      la += __shfl_xor_sync(0xffffffffu, la, 1);
+      la += __shfl_xor_sync(0xffffffffu, la, 2);
+      lb += __shfl_xor_sync(0xffffffffu, lb, 1);
+      lb += __shfl_xor_sync(0xffffffffu, lb, 2);
+      __syncthreads();  // the stage buffers are free: reuse them as the exchange area
+      float4* xb = reinterpret_cast<float4*>(smem);  // [NO + 1][NTH] float4
+      if (crank != 0) {
+        if constexpr (MODE == MODE_DECODE) {
+#pragma unroll
+          for (int j = 0; j < NO; ++j) xb[j * NTH + tid] = make_float4(o[j][0], o[j][1], o[j][2], o[j][3]);
+        }
+        xb[NO * NTH + tid] = make_float4(m_a, m_b, la, lb);
+      }
+      cluster_sync_all();
+      if (crank == 0 && iu < U && icnt > 0) {
+        const uint32_t xa = smem_u32(xb);
+        for (unsigned q = 1; q < (unsigned)CS; ++q) {
+          const uint32_t ra = dsmem_map(xa, q);
+          const float4 st = dsmem_ld4(ra + (uint32_t)((NO * NTH + tid) * 16));
+          const float nA = fmaxf(m_a, st.x), nB = fmaxf(m_b, st.y);
+          const float bA = nA == -INFINITY ? 0.f : nA, bB = nB == -INFINITY ? 0.f : nB;
+          const float fA = fast_exp2(m_a - bA), gA = fast_exp2(st.x - bA);
+          const float fB = fast_exp2(m_b - bB), gB = fast_exp2(st.y - bB);
+          la = la * fA + st.z * gA;
+          lb = lb * fB + st.w * gB;
+          m_a = nA;
+          m_b = nB;
+          if constexpr (MODE == MODE_DECODE) {
+#pragma unroll
+            for (int j = 0; j < NO; ++j) {
+              const float4 x = dsmem_ld4(ra + (uint32_t)((j * NTH + tid) * 16));
+              o[j][0] = o[j][0] * fA + x.x * gA;
+              o[j][1] = o[j][1] * fA + x.y * gA;
+              o[j][2] = o[j][2] * fB + x.z * gB;
+              o[j][3] = o[j][3] * fB + x.w * gB;
+            }
+          }
+        }
+        const float inv_a = la > 0.f ? 1.f / la : 0.f, inv_b = lb > 0.f ? 1.f / lb : 0.f;
+        const int dc = 2 * (lane & 3);
+        const int64_t u = iu;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = h ? rB : rA;
+          if (r >= M) continue;
+          const float inv = h ? inv_b : inv_a;
+          if constexpr (MODE == MODE_DECODE) {
+            if (p.out_f32) {
+              float* og = static_cast<float*>(p.out) + (u * M + r) * (int64_t)D + dc;
+#pragma unroll
+              for (int nt = 0; nt < D / 8; ++nt)
+                *reinterpret_cast<float2*>(og + nt * 8) = make_float2(o[nt][2 * h] * inv, o[nt][2 * h + 1] * inv);
+            } else {
+              __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + (u * M + r) * (int64_t)D + dc;
+#pragma unroll
+              for (int nt = 0; nt < D / 8; ++nt)
+                *reinterpret_cast<__nv_bfloat162*>(og + nt * 8) =
+                    __floats2bfloat162_rn(o[nt][2 * h] * inv, o[nt][2 * h + 1] * inv);
+            }
+          }
+          if ((lane & 3) == 0) {
+            const float l = h ? lb : la;
+            const float m = h ? m_b : m_a;
+            if (p.lse) p.lse[u * M + r] = l > 0.f ? (m + __log2f(l)) * LN2 : -INFINITY;
+            if (MODE == MODE_DECODE && !(l > 0.f)) set_status(p.status, STS_DEV_EMPTY_ROW);
+          }
+        }
+      }
+      cluster_sync_all();  // partners keep their shared memory until rank 0 has read it
+    }
+  } else {
+    if (cur_u >= 0) flush(cur_u, cur_P, cur_cnt, cur_range);
+  }
   STS_TRACE_AT(4);
 }
 
@@ -674,10 +791,65 @@ __global__ void __launch_bounds__(MERGE_MAX_THREADS) merge_pieces_kernel(DecodeP
 }
 
 template <int D, int NW, int KT, int STAGES, int MODE>
+int launch_verify(DecodeParams& p, cudaStream_t st);
+
+template <int D, int NW, int KT, int STAGES, int MODE, int CS>
+int launch_cluster(DecodeParams& p, cudaStream_t st) {
+  using L = VL<D, NW, KT, STAGES, MODE>;
+  auto kern = verify_decode_kernel<D, NW, KT, STAGES, MODE, CS>;
+  static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+  STS_CUDA_CHECK(attr);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(p.units * CS));
+  cfg.blockDim = dim3(L::THREADS);
+  cfg.dynamicSmemBytes = L::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  STS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, p));
+  return STS_OK;
+}
+
+#ifndef STS_CLUSTER_MAX
+#define STS_CLUSTER_MAX 8
+#endif
+
+// Cluster mode when the resident CTA slots hold >= 2 CTAs per unit and a CTA
+// would stream few tiles (fixed per-launch costs dominate): the c2 shape
+// (256 units on 888 slots, ~30 tiles per CTA) -> clusters of 3, measured
+// 92.8 vs 98.9 us (sparse) and 670 vs 688 us (dense, ~300 tiles per CTA).  At
+// c4 (~950 tiles per CTA) the 13% of slots a floor(slots / units) cluster
+// grid leaves idle cost more (2.55 vs 2.35 ms), so long streams stay
+// stream-K; the draft LSE pass also measured better as stream-K.
+// STS_VERIFY_CLUSTER=0 disables, =1 forces (when it applies).
+template <int D, int NW, int KT, int STAGES, int MODE>
+int try_cluster(DecodeParams& p, cudaStream_t st, int per_sm) {
+  static const int env = getenv("STS_VERIFY_CLUSTER") ? atoi(getenv("STS_VERIFY_CLUSTER")) : -1;
+  if (env == 0 || MODE != MODE_DECODE || NW != 2 || p.units <= 0) return -1;
+  const int64_t slots = (int64_t)num_sms() * per_sm;
+  const int64_t cap = p.idx ? p.idx_ld : p.n_dense;  // keys per unit (upper bound)
+  const int64_t tiles_per_slot = p.units * ((cap + KT - 1) / KT) / slots;
+  if (env != 1 && tiles_per_slot > 600) return -1;
+  int64_t cs = slots / p.units;
+  if (cs > STS_CLUSTER_MAX) cs = STS_CLUSTER_MAX;
+  if (cs >= 8) return launch_cluster<D, NW, KT, STAGES, MODE, 8>(p, st);
+  if (cs >= 6) return launch_cluster<D, NW, KT, STAGES, MODE, 6>(p, st);
+  if (cs >= 4) return launch_cluster<D, NW, KT, STAGES, MODE, 4>(p, st);
+  if (cs >= 3) return launch_cluster<D, NW, KT, STAGES, MODE, 3>(p, st);
+  if (cs >= 2) return launch_cluster<D, NW, KT, STAGES, MODE, 2>(p, st);
+  return -1;
+}
+
+template <int D, int NW, int KT, int STAGES, int MODE>
 int launch_verify(DecodeParams& p, cudaStream_t st) {
   using L = VL<D, NW, KT, STAGES, MODE>;
   static_assert(L::SMEM <= 227 * 1024, "verify decode shared memory");
-  auto kern = verify_decode_kernel<D, NW, KT, STAGES, MODE>;
+  auto kern = verify_decode_kernel<D, NW, KT, STAGES, MODE, 1>;
   static const int per_sm = [&]() {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM) != cudaSuccess) return -1;
     int n = 0;
@@ -685,6 +857,10 @@ int launch_verify(DecodeParams& p, cudaStream_t st) {
     return n < 1 ? 1 : n;
   }();
   STS_REQUIRE(per_sm > 0, STS_ERR_CUDA, "verify kernel setup failed: %s", cudaGetErrorString(cudaGetLastError()));
+  if constexpr (NW == 2 && MODE == MODE_DECODE) {
+    const int rc = try_cluster<D, NW, KT, STAGES, MODE>(p, st, per_sm);
+    if (rc >= 0) return rc;
+  }
   const int smem = L::SMEM;
   kern<<<num_sms() * per_sm, L::THREADS, smem, st>>>(p);
   STS_LAUNCH_CHECK();
@@ -727,58 +903,15 @@ int launch_verify(DecodeParams& p, cudaStream_t st) {
 #define STS_DRAFT_STAGES 2
 #endif
 
-// pipeline shape of the d=128, M in (16, 32] decode (the c2 / c4 headline):
-// STS_VERIFY_CFG = 0 (default) 32-key tiles x2 stages, 1: 32x3, 2: 16x4, 3: 16x3, 4: 64x2
-int verify_cfg() {
-  static int cfg = -1;
-  if (cfg < 0) {
-    const char* e = getenv("STS_VERIFY_CFG");
-    cfg = e ? atoi(e) : 0;
-    if (cfg < 0 || cfg > 4) cfg = 0;
-  }
-  return cfg;
-}
-
-// pipeline shape of the d=64 draft capture (LSE / probability passes):
-// STS_DRAFT_CFG = 0 (default) 64-key tiles x2 stages, 1: 64x3, 2: 32x3, 3: 32x2, 4: 64x4
-// (measured at c2, LSE + probability passes: 64x2 247 us < 64x3 270 < 64x4 296
-//  < 32x4 297 < 32x3 306 < 128x2 316 < 128x3 415)
-int draft_cfg() {
-  static int cfg = -1;
-  if (cfg < 0) {
-    const char* e = getenv("STS_DRAFT_CFG");
-    cfg = e ? atoi(e) : 0;
-    if (cfg < 0 || cfg > 4) cfg = 0;
-  }
-  return cfg;
-}
+// Pipeline shapes were tuned on B200 at c2 (profiles/r01): decode 32-key tiles
+// x2 stages (vs 32x3, 16x4, 16x3, 64x2: all within 1-5% slower); draft passes
+// 64-key tiles x2 (247 us) < 64x3 (270) < 64x4 (296) < 32x4 (297) < 32x3 (306)
+// < 128x2 (316) < 128x3 (415).
 
 template <int D, int MODE>
 int verify_dispatch(DecodeParams& p, cudaStream_t st) {
   constexpr bool DEC = MODE == MODE_DECODE;
   constexpr int KT = DEC ? STS_VERIFY_KT : STS_DRAFT_KT, S = DEC ? STS_VERIFY_STAGES : STS_DRAFT_STAGES;
-  if constexpr (D == 64 && !DEC) {
-    if ((p.M + 15) / 16 == 2) {
-      switch (draft_cfg()) {
-        case 1: return launch_verify<D, 2, 64, 3, MODE>(p, st);
-        case 2: return launch_verify<D, 2, 32, 3, MODE>(p, st);
-        case 3: return launch_verify<D, 2, 32, 2, MODE>(p, st);
-        case 4: return launch_verify<D, 2, 64, 4, MODE>(p, st);
-        default: break;
-      }
-    }
-  }
-  if constexpr (D == 128 && DEC) {
-    if ((p.M + 15) / 16 == 2) {
-      switch (verify_cfg()) {
-        case 1: return launch_verify<D, 2, 32, 3, MODE>(p, st);
-        case 2: return launch_verify<D, 2, 16, 4, MODE>(p, st);
-        case 3: return launch_verify<D, 2, 16, 3, MODE>(p, st);
-        case 4: return launch_verify<D, 2, 64, 2, MODE>(p, st);
-        default: break;
-      }
-    }
-  }
   switch ((p.M + 15) / 16) {
     case 1: return launch_verify<D, 1, KT, S, MODE>(p, st);
     case 2: return launch_verify<D, 2, KT, S, MODE>(p, st);

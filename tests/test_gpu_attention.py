@@ -236,3 +236,20 @@ def test_interleaved_kv_row_stride(cuda_ok, dtype):
     for u in range(U):
         want, _ = O.block_attention(q[u], k[u], v[u], lists[u], causal_base=base, rows_per_head=R)
         np.testing.assert_allclose(out[u], want, rtol=tol[0], atol=tol[1])
+
+
+def test_stream_k_schedule_variant(cuda_ok):
+    """The attention parity suite again with the cluster schedule disabled
+    (STS_VERIFY_CLUSTER=0: every launch takes the stream-K + piece-merge path),
+    in a subprocess because the library reads the knob once."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, STS_VERIFY_CLUSTER="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", str(root / "tests" / "test_gpu_attention.py"), "-q", "-x",
+                        "-p", "no:cacheprovider", "-k", "not stream_k_schedule_variant"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
