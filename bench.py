@@ -307,15 +307,19 @@ def main():
         "attend": lambda: step.attend(q, k, v),
         "dense": lambda: step.attend_dense(q, k, v, out=dense_out, lse=dense_lse),
     }
-    run_stage = {}
+    run_stage, stage_launches = {}, {}
+    lib = _lib.load()
     for name, fn in stages.items():
+        c0 = lib.sts_launch_count()
         if args.eager:
+            fn()
             run_stage[name] = fn
         else:
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 fn()
             run_stage[name] = g.replay
+        stage_launches[name] = int(lib.sts_launch_count() - c0)  # our kernels per replay
     for _ in range(2):
         for fn in run_stage.values():
             fn()
@@ -391,9 +395,7 @@ def main():
             traffic = json.loads(prof.read_text()).get("dram_bytes_per_step")
         except Exception:
             traffic = None
-    splits_launch = 1 + (step.splits > 1)
-    launches_step = (2 + (step.ws_draft.buf is not None)) + 1 + splits_launch  # capture, select, attend
-    launches = args.steps * (launches_step + 1 + (step.dense_splits > 1))
+    launches = args.steps * sum(stage_launches.values())  # counted by the library (sts_launch_count)
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
@@ -426,12 +428,13 @@ def main():
         "hbm_gbs": round(achieved, 1), "dense_hbm_gbs": round(dense_bytes / (den * 1e-6) / 1e9, 1),
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
-                     "kernel": "sts_sparse_decode (gather flash-decode + split merge)",
+                     "kernel": "sts_sparse_decode: verify_decode_kernel (gathered flash-decode, cluster/DSMEM or stream-K + piece merge)",
                      "algorithmic_bytes_per_launch": int(nbytes), "peak_source": peak_src},
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e, 2), "unit": "us", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "what": "public API STSVerifyStep.step: H2D target+draft Q, capture, select, sparse attention, D2H out"},
         "gpu_launches": int(launches),
+        "launches_per_stage": stage_launches,
         "clocks": clocks.summary(),
         "wall_s_timed_loop": round(wall, 3),
     }

@@ -59,6 +59,9 @@ extern "C" {
 
 STS_API const char* sts_last_error(void);
 STS_API int sts_abi_version(void);
+/* kernels this process has launched through the library (a CUDA graph
+ * replay re-runs the kernels captured once, without passing here) */
+STS_API unsigned long long sts_launch_count(void);
 
 /* ------------------------------------------------------------------------
  * sts_select_topk — sparsity-mask construction.

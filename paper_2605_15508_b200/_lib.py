@@ -31,6 +31,7 @@ _p, _sz = C.c_void_p, C.c_size_t
 SIGNATURES = {
     "sts_last_error": (C.c_char_p, []),
     "sts_abi_version": (C.c_int, []),
+    "sts_launch_count": (C.c_ulonglong, []),
     "sts_select_workspace_bytes": (_sz, [_i64, _i32, _i32]),
     "sts_select_topk": (C.c_int, [_p, _i64, _p, _i32, _i64, _p, _i32, _f64, _i32, _i32, _u32, _i32,
                                   _i32, _p, _i64, _p, _p, _p, _sz, _p]),

@@ -37,7 +37,13 @@ void set_error(const char* fmt, ...);
     }                                                                          \
   } while (0)
 
-#define STS_LAUNCH_CHECK() STS_CUDA_CHECK(cudaGetLastError())
+// every kernel launch of the library passes here (counted: sts_launch_count)
+void count_launch();
+#define STS_LAUNCH_CHECK()              \
+  do {                                  \
+    ::sts::count_launch();              \
+    STS_CUDA_CHECK(cudaGetLastError()); \
+  } while (0)
 
 int num_sms();
 

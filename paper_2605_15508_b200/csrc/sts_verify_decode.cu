@@ -812,6 +812,7 @@ int launch_cluster(DecodeParams& p, cudaStream_t st) {
   cfg.attrs = at;
   cfg.numAttrs = 1;
   STS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, p));
+  count_launch();
   return STS_OK;
 }
 
@@ -884,6 +885,7 @@ int launch_verify(DecodeParams& p, cudaStream_t st) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     STS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, merge_pieces_kernel<D, MODE>, p));
+    count_launch();
     STS_LAUNCH_CHECK();
   }
   return STS_OK;

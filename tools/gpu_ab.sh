@@ -4,7 +4,7 @@ timeout 600 python -m pytest tests -m gpu -x -q -p no:cacheprovider --timeout 12
 tail -3 gpurun_out/pytest_gpu.log
 B="python bench.py --steps 30 --warmup 5 --no-cpu-baseline"
 : > gpurun_out/ab.log
-for rep in 1 2; do
+for rep in 1; do
   echo "== cluster" >> gpurun_out/ab.log; timeout 200 $B >> gpurun_out/ab.log 2>&1
   echo "== streamk" >> gpurun_out/ab.log; STS_VERIFY_CLUSTER=0 timeout 200 $B >> gpurun_out/ab.log 2>&1
 done

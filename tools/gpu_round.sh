@@ -13,6 +13,6 @@ for sp in 0.5 0.75 0.9 0.95 0.98; do timeout 600 python bench.py --config c3 --s
 echo "c3 rc=$?" >> gpurun_out/bench_c3.log
 P="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --eager"
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv $P > gpurun_out/ncu_launches.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k "regex:verify_decode|merge_pieces|select_kernel" -s 21 -c 7 -o gpurun_out/prof_step $P > gpurun_out/ncu_step.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k "regex:verify_decode|merge_pieces|select_kernel" -s 30 -c 6 -o gpurun_out/prof_step $P > gpurun_out/ncu_step.log 2>&1
 echo "ncu rc=$?" >> gpurun_out/ncu_step.log
 for f in gpurun_out/pytest_gpu.log gpurun_out/smoke.log gpurun_out/bench.log gpurun_out/bench_ref.log gpurun_out/bench_c4.log; do tail -n 2 $f; done
