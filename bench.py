@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--eager", action="store_true", help="time stages as eager launches instead of CUDA graphs")
     ap.add_argument("--flush", default="clean", choices=["clean", "write", "none"], help="L2 flush between stages")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="collective backend for N > 1 (gloo + --one-gpu: functional check on a single GPU)")
+    ap.add_argument("--one-gpu", action="store_true", help="map every rank to cuda:0 (functional checks only)")
     ap.add_argument("--context", type=int, default=None, help="override the config's context length")
     ap.add_argument("--batch", type=int, default=None, help="override the config's batch")
     return ap.parse_args()
@@ -455,11 +458,15 @@ def run_sharded(args, world, rank, local):
     from paper_2605_15508_b200 import SparsityConfig, _lib, sharded
     from paper_2605_15508_b200.verify import algorithmic_bytes, config_shape, random_mapping_table
 
+    local = 0 if args.one_gpu else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
         drive = lambda proto: sharded.run(proto)  # noqa: E731
     else:
         drive = sharded.run_single
@@ -558,7 +565,7 @@ def run_sharded(args, world, rank, local):
                    "context": shape.context, "batch": shape.batch, "gamma": shape.gamma, "mode": "S",
                    "page_size": args.page_size, "shard_positions": step.n_loc,
                    "keys_per_kv_head": round(keys_per_unit, 1), "l2": flush.describe(),
-                   "parallelism": f"sequence-sharded x{world} (NCCL histogram allreduce + LSE merge)"},
+                   "parallelism": f"sequence-sharded x{world} ({args.dist_backend} histogram allreduce + LSE merge)"},
         "dense_us": round(den, 2), "speedup_vs_dense": round(den / att, 3),
         "mask_build_us": {"draft_capture": round(cap, 2), "select": round(sel, 2)},
         "sts_step_us": round(cap + sel + att, 2), "step_speedup_vs_dense": round(den / (cap + sel + att), 3),
