@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
   const int rA = warp * 16 + (lane >> 2), rB = rA + 8;
   const int rmodA = rA % p.rows_per_head, rmodB = rB % p.rows_per_head;
   const float sl2 = p.scale * LOG2E;
+  [[maybe_unused]] const int probs_G = M / p.rows_per_head;  // q-heads per unit (MODE_PROBS)
   const int causal_shift = p.pos_offset - p.causal_base;
   const bool causal = p.causal_base >= 0;
   float o[MODE == MODE_DECODE ? D / 8 : 1][4];
@@ -521,7 +522,7 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
       }
       __syncthreads();
       const int R = p.rows_per_head;
-      const int G = M / R;
+      const int G = probs_G;
       const int lim = p.causal_base - p.pos_offset;  // committed: pos < lim
       for (int key = tid; key < KT; key += NTH) {
         if (key >= nvalid) continue;
@@ -529,11 +530,19 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
         if (p.probs_mode == 0) {
           if (pos >= lim) continue;
           float* outp = p.probs_out + (u * G) * p.out_ld + j0 + key;
-          for (int hh = 0; hh < G; ++hh) {
-            const float* sp = s_prob + hh * R * KPS + key;
-            float acc = sp[0];
-            for (int ii = 1; ii < R; ++ii) acc = __fadd_rn(acc, sp[ii * KPS]);
-            outp[hh * p.out_ld] = acc;
+          if (R == 5) {  // gamma = 4: all five loads issued before the in-order sum
+            for (int hh = 0; hh < G; ++hh) {
+              const float* sp = s_prob + hh * 5 * KPS + key;
+              const float x0 = sp[0], x1 = sp[KPS], x2 = sp[2 * KPS], x3 = sp[3 * KPS], x4 = sp[4 * KPS];
+              outp[hh * p.out_ld] = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(x0, x1), x2), x3), x4);
+            }
+          } else {
+            for (int hh = 0; hh < G; ++hh) {
+              const float* sp = s_prob + hh * R * KPS + key;
+              float acc = sp[0];
+              for (int ii = 1; ii < R; ++ii) acc = __fadd_rn(acc, sp[ii * KPS]);
+              outp[hh * p.out_ld] = acc;
+            }
           }
         } else {
           float* outp = p.probs_out + (u * M) * p.out_ld + j0 + key;

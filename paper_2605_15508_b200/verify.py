@@ -199,6 +199,53 @@ class STSVerifyStep:
         self.build_masks(stream)
         return self.attend(target_q, target_k, target_v, stream)
 
+    # -- host-buffer API (queries in from pinned host memory, output back out) --
+    def _graph(self, key, fn):
+        """CUDA graph of ``fn`` (captured once per key; replays launch no Python)."""
+        if not hasattr(self, "_graphs"):
+            self._graphs = {}
+        g = self._graphs.get(key)
+        if g is None:
+            fn()  # warm-up outside capture (workspace allocations happen here)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                fn()
+            self._graphs[key] = g
+        return g
+
+    def _host_buffers(self, h_dq, h_tq):
+        if getattr(self, "_d_tq", None) is None or self._d_tq.shape != h_tq.shape:
+            self._d_tq = torch.empty(h_tq.shape, dtype=h_tq.dtype, device=self.device)
+            self._d_dq = torch.empty(h_dq.shape, dtype=h_dq.dtype, device=self.device) if h_dq is not None else None
+        return self._d_dq, self._d_tq
+
+    def attend_host(self, h_tq, target_k, target_v, h_out):
+        """Target attention with host queries: H2D copy of Q [B, L, Hq, R, d]
+        (pinned), the attention graph, D2H copy of the output into ``h_out``.
+        The masks are the ones the last ``build_masks`` produced."""
+        _, d_tq = self._host_buffers(None, h_tq)
+        d_tq.copy_(h_tq, non_blocking=True)
+        q, k, v = self.target_views(d_tq, target_k, target_v)
+        key = ("attend", target_k.data_ptr(), target_v.data_ptr(),
+               self.idx.data_ptr() if self.idx is not None else 0)
+        self._graph(key, lambda: self.attend(q, k, v)).replay()
+        h_out.copy_(self.out, non_blocking=True)
+        return h_out
+
+    def step_host(self, h_dq, draft_k, h_tq, target_k, target_v, h_out):
+        """The whole verify step with host queries (draft Q [B, Ld, Hqd, R, dd]
+        and target Q), replayed as one CUDA graph; output copied to ``h_out``."""
+        d_dq, d_tq = self._host_buffers(h_dq, h_tq)
+        d_dq.copy_(h_dq, non_blocking=True)
+        d_tq.copy_(h_tq, non_blocking=True)
+        dq, dk = self.draft_views(d_dq, draft_k)
+        q, k, v = self.target_views(d_tq, target_k, target_v)
+        key = ("step", draft_k.data_ptr(), target_k.data_ptr(), target_v.data_ptr())
+        self._graph(key, lambda: self.step(dq, dk, q, k, v)).replay()
+        h_out.copy_(self.out, non_blocking=True)
+        return h_out
+
     # -- layouts ------------------------------------------------------------------
     def target_views(self, q, k, v):
         """[B, L, Hq, R, d] q and [B, L, Hkv, N, d] caches -> kernel unit views."""

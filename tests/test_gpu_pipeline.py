@@ -122,3 +122,29 @@ def test_verify_step_mode_r_reference_masks(cuda_ok):
                     np.testing.assert_array_equal(lst[(mem[u, : cnt[u]] >> r) & 1 == 1], mask)
                     want = O.sparse_attention(qf[u, r], kf[u], vf[u], mask)
                     np.testing.assert_allclose(out[u, r], want, rtol=2e-2, atol=2e-2)
+
+
+def test_host_buffer_api_matches_device_path(cuda_ok):
+    """STSVerifyStep.step_host / attend_host (pinned host queries in, host output
+    out, CUDA-graph replays) give the device path's result bit for bit."""
+    import torch
+
+    from paper_2605_15508_b200 import SparsityConfig
+    from paper_2605_15508_b200.verify import STSVerifyStep, random_mapping_table, synthetic_inputs
+
+    s = _small_shape()
+    step = STSVerifyStep(s, SparsityConfig(budget=0.1), random_mapping_table(s, seed=2), mode="S")
+    dq, dk, tq, tk, tv = synthetic_inputs(s, "cuda", seed=3)
+    q, k, v = step.target_views(tq, tk, tv)
+    out, _ = step.step(*step.draft_views(dq, dk), q, k, v)
+    want = out.clone()
+    h_out = torch.empty(want.shape, dtype=want.dtype).pin_memory()
+    for _ in range(2):  # first call captures the graph, second replays it
+        h_out.zero_()
+        step.step_host(dq.cpu().pin_memory(), dk, tq.cpu().pin_memory(), tk, tv, h_out)
+        torch.cuda.synchronize()
+        assert torch.equal(h_out, want.cpu())
+    h_out.zero_()
+    step.attend_host(tq.cpu().pin_memory(), tk, tv, h_out)
+    torch.cuda.synchronize()
+    assert torch.equal(h_out, want.cpu())
