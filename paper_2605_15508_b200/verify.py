@@ -215,10 +215,12 @@ class STSVerifyStep:
         return g
 
     def _host_buffers(self, h_dq, h_tq):
+        """Device staging buffers for host queries (allocated once per shape)."""
         if getattr(self, "_d_tq", None) is None or self._d_tq.shape != h_tq.shape:
             self._d_tq = torch.empty(h_tq.shape, dtype=h_tq.dtype, device=self.device)
-            self._d_dq = torch.empty(h_dq.shape, dtype=h_dq.dtype, device=self.device) if h_dq is not None else None
-        return self._d_dq, self._d_tq
+        if h_dq is not None and (getattr(self, "_d_dq", None) is None or self._d_dq.shape != h_dq.shape):
+            self._d_dq = torch.empty(h_dq.shape, dtype=h_dq.dtype, device=self.device)
+        return getattr(self, "_d_dq", None), self._d_tq
 
     def attend_host(self, h_tq, target_k, target_v, h_out):
         """Target attention with host queries: H2D copy of Q [B, L, Hq, R, d]
