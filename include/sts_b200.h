@@ -137,6 +137,25 @@ STS_API int sts_sparse_decode(int32_t dtype, int32_t out_dtype, const void* q_de
                       void* stream);
 
 /* ------------------------------------------------------------------------
+ * sts_sparse_prefill — sparse prefill attention (STS-PD):
+ * every query row has its own key list.  Replaces the masked prefill of
+ * toymodel._run_block (src/toymodel.py:315-348 reached through
+ * forward_prefill(masks=...) :370-399, masks from draft_masks_prefill
+ * src/sparsity.py:122-130) and a per-row loop of sparse_attention.
+ * Unit (g, t) = g*rows + t: queries q[(g*rows+t)][M][d] (M = the heads that
+ * share g's K/V and the mask, 1 for MHA), keys idx_dev[(g*rows+t)*idx_ld + j],
+ * j < cnt_dev[g*rows+t], positions into K/V block g (k_cache + g*kv_unit_stride);
+ * every listed key is attended (lists are causal by construction).
+ * out[(g*rows+t)][M][d] (out_dtype), lse (nullable).  Workspace:
+ * sts_sparse_decode_workspace_bytes(kv_units*rows, M, d, 1).
+ * ---------------------------------------------------------------------- */
+STS_API int sts_sparse_prefill(int32_t dtype, int32_t out_dtype, const void* q_dev, const void* k_cache_dev,
+                               const void* v_cache_dev, int64_t kv_unit_stride, int64_t kv_row_stride,
+                               int64_t kv_units, int32_t rows, int32_t M, int32_t d, const int32_t* idx_dev,
+                               int64_t idx_ld, const int32_t* cnt_dev, float scale, void* out_dev, float* lse_dev,
+                               int32_t* status_dev, void* workspace_dev, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------------------------------
  * sts_draft_scores — draft-score capture (ForwardRecord.attention of the
  * draft's decode, src/toymodel.py:349-350 via specdec.propose
  * src/specdec.py:150-167), computed for the R speculative rows at once.

@@ -28,6 +28,7 @@ from .sparsity import (
     page_aggregate,
     remap_masks,
     sparse_attention,
+    sparse_prefill_attention,
     verification_masks,
 )
 
@@ -50,5 +51,6 @@ __all__ = [
     "page_aggregate",
     "remap_masks",
     "sparse_attention",
+    "sparse_prefill_attention",
     "verification_masks",
 ]

@@ -40,6 +40,8 @@ SIGNATURES = {
     "sts_auto_splits": (_i32, [_i64, _i64]),
     "sts_sparse_decode": (C.c_int, [_i32, _i32, _p, _p, _p, _i64, _i64, _i64, _i32, _i32, _p, _i64, _p, _i32, _p,
                                     _i32, _i32, _i32, _f32, _p, _p, _i32, _p, _p, _sz, _p]),
+    "sts_sparse_prefill": (C.c_int, [_i32, _i32, _p, _p, _p, _i64, _i64, _i64, _i32, _i32, _i32, _p, _i64, _p,
+                                     _f32, _p, _p, _p, _p, _sz, _p]),
     "sts_draft_workspace_bytes": (_sz, [_i64, _i32, _i32]),
     "sts_draft_lse": (C.c_int, [_i32, _p, _p, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _i32, _f32,
                                 _p, _p, _sz, _p]),

@@ -17,6 +17,7 @@ struct DecodeParams {
   int64_t kv_stride;
   int64_t row_stride;  // elements between consecutive K (V) rows
   int64_t units;
+  int64_t kv_div;       // units per K/V unit (prefill: query rows share their head's cache); <= 1: one each
   int M;
   int d;
   const int32_t* idx;

@@ -233,8 +233,8 @@ __global__ void __launch_bounds__(NT * 32, gather_min_blocks<NT>()) gather_kerne
       // pull them into L2 now (M*D*2 bytes, one 128-byte line per thread)
       if (tid * 128 < M * D * 2)
         asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const char*>(p.q) + u * (int64_t)M * D * 2 + tid * 128));
-      g_kb = static_cast<const char*>(p.k) + (u * p.kv_stride + g_ch * 8) * 2;
-      g_vb = MODE == MODE_DECODE ? static_cast<const char*>(p.v) + (u * p.kv_stride + g_ch * 8) * 2 : g_kb;
+      g_kb = static_cast<const char*>(p.k) + ((p.kv_div > 1 ? u / p.kv_div : u) * p.kv_stride + g_ch * 8) * 2;
+      g_vb = MODE == MODE_DECODE ? static_cast<const char*>(p.v) + ((p.kv_div > 1 ? u / p.kv_div : u) * p.kv_stride + g_ch * 8) * 2 : g_kb;
     }
     const uint32_t dst0 = stage_base + stage * L::STAGE + g_dst;
     const int* ring = s_idx + slot * KT;

@@ -39,8 +39,9 @@ __global__ void __launch_bounds__(F32_WARPS * 32) sparse_decode_f32_kernel(Decod
   const int cnt = unit_count(p, u);
   const int c0 = (int)((int64_t)split * cnt / p.splits);
   const int c1 = (int)((int64_t)(split + 1) * cnt / p.splits);
-  const float* kg = static_cast<const float*>(p.k) + u * p.kv_stride;
-  const float* vg = static_cast<const float*>(p.v) + u * p.kv_stride;
+  const int64_t ukv = p.kv_div > 1 ? u / p.kv_div : u;
+  const float* kg = static_cast<const float*>(p.k) + ukv * p.kv_stride;
+  const float* vg = static_cast<const float*>(p.v) + ukv * p.kv_stride;
   const int32_t* idxg = p.idx ? p.idx + u * p.idx_ld : nullptr;
   const uint32_t* memg = p.member ? p.member + u * p.idx_ld : nullptr;
 
@@ -150,7 +151,7 @@ extern "C" size_t sts_sparse_decode_workspace_bytes(int64_t units, int32_t M, in
   return f32 > bf16 ? f32 : bf16;
 }
 
-extern "C" int sts_sparse_decode(int32_t dtype, int32_t out_dtype, const void* q_dev, const void* k_cache_dev,
+static int sparse_decode_impl(int32_t dtype, int32_t out_dtype, const void* q_dev, const void* k_cache_dev,
                                  const void* v_cache_dev, int64_t kv_unit_stride, int64_t kv_row_stride,
                                  int64_t units,
                                  int32_t M, int32_t d, const int32_t* idx_dev, int64_t idx_ld,
@@ -159,7 +160,7 @@ extern "C" int sts_sparse_decode(int32_t dtype, int32_t out_dtype, const void* q
                                  int32_t rows_per_head, int32_t pos_offset, float scale,
                                  void* out_dev, float* lse_dev, int32_t splits,
                                  int32_t* status_dev, void* workspace_dev,
-                                 size_t workspace_bytes, void* stream) {
+                                 size_t workspace_bytes, void* stream, int64_t kv_div) {
   STS_REQUIRE(units >= 0, STS_ERR_CONTRACT, "units must be >= 0");
   if (units == 0) return STS_OK;
   STS_REQUIRE(q_dev && k_cache_dev && v_cache_dev && out_dev, STS_ERR_CONTRACT, "null buffer");
@@ -169,7 +170,7 @@ extern "C" int sts_sparse_decode(int32_t dtype, int32_t out_dtype, const void* q
   STS_REQUIRE(idx_dev ? (cnt_dev != nullptr) : (n_dense >= 0), STS_ERR_CONTRACT,
               "index list needs counts / dense needs n_dense");
   STS_REQUIRE(splits >= 1 && splits <= 4096, STS_ERR_CONTRACT, "splits must be in [1, 4096]");
-  STS_REQUIRE(units <= 65535, STS_ERR_CONTRACT, "units must be <= 65535 (grid.y)");
+  STS_REQUIRE(dtype != STS_DTYPE_F32 || units <= 65535, STS_ERR_CONTRACT, "f32 path: units must be <= 65535 (grid.y)");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 
   DecodeParams p;
@@ -177,6 +178,7 @@ extern "C" int sts_sparse_decode(int32_t dtype, int32_t out_dtype, const void* q
   p.k = k_cache_dev;
   p.v = v_cache_dev;
   p.kv_stride = kv_unit_stride;
+  p.kv_div = kv_div;
   p.row_stride = kv_row_stride > 0 ? kv_row_stride : d;
   STS_REQUIRE(p.row_stride >= d, STS_ERR_CONTRACT, "kv_row_stride must be >= d");
   p.units = units;
@@ -235,6 +237,33 @@ extern "C" int sts_sparse_decode(int32_t dtype, int32_t out_dtype, const void* q
   }
   if (rc != STS_OK || splits == 1) return rc;
   return lse_merge_launch(p.o_part, p.l_part, splits, units * M, d, dtype, out_dev, lse_dev, st);
+}
+
+extern "C" int sts_sparse_decode(int32_t dtype, int32_t out_dtype, const void* q_dev, const void* k_cache_dev,
+                                 const void* v_cache_dev, int64_t kv_unit_stride, int64_t kv_row_stride,
+                                 int64_t units, int32_t M, int32_t d, const int32_t* idx_dev, int64_t idx_ld,
+                                 const int32_t* cnt_dev, int32_t n_dense, const uint32_t* member_dev,
+                                 int32_t causal_base, int32_t rows_per_head, int32_t pos_offset, float scale,
+                                 void* out_dev, float* lse_dev, int32_t splits, int32_t* status_dev,
+                                 void* workspace_dev, size_t workspace_bytes, void* stream) {
+  return sparse_decode_impl(dtype, out_dtype, q_dev, k_cache_dev, v_cache_dev, kv_unit_stride, kv_row_stride, units,
+                            M, d, idx_dev, idx_ld, cnt_dev, n_dense, member_dev, causal_base, rows_per_head,
+                            pos_offset, scale, out_dev, lse_dev, splits, status_dev, workspace_dev, workspace_bytes,
+                            stream, 1);
+}
+
+extern "C" int sts_sparse_prefill(int32_t dtype, int32_t out_dtype, const void* q_dev, const void* k_cache_dev,
+                                  const void* v_cache_dev, int64_t kv_unit_stride, int64_t kv_row_stride,
+                                  int64_t kv_units, int32_t rows, int32_t M, int32_t d, const int32_t* idx_dev,
+                                  int64_t idx_ld, const int32_t* cnt_dev, float scale, void* out_dev, float* lse_dev,
+                                  int32_t* status_dev, void* workspace_dev, size_t workspace_bytes, void* stream) {
+  STS_REQUIRE(kv_units >= 0 && rows >= 0, STS_ERR_CONTRACT, "kv_units and rows must be >= 0");
+  STS_REQUIRE(idx_dev && cnt_dev, STS_ERR_CONTRACT, "sparse prefill needs per-row index lists");
+  // unit (g, t) = g*rows + t attends exactly its list (already causal); its
+  // K/V block is g's: kv_div = rows
+  return sparse_decode_impl(dtype, out_dtype, q_dev, k_cache_dev, v_cache_dev, kv_unit_stride, kv_row_stride,
+                            kv_units * rows, M, d, idx_dev, idx_ld, cnt_dev, 0, nullptr, -1, 1, 0, scale, out_dev,
+                            lse_dev, 1, status_dev, workspace_dev, workspace_bytes, stream, rows > 1 ? rows : 1);
 }
 
 extern "C" int32_t sts_auto_splits(int64_t units, int64_t keys_per_unit) {

@@ -285,8 +285,9 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
       g_u = u;
       if (tid * 128 < M * D * 2)  // this unit's Q into L2 ahead of the math side
         asm volatile("prefetch.global.L2 [%0];" ::"l"(static_cast<const char*>(p.q) + u * (int64_t)M * D * 2 + tid * 128));
-      g_kb = static_cast<const char*>(p.k) + (u * p.kv_stride + g_ch * 8) * 2;
-      if constexpr (MODE == MODE_DECODE) g_vb = static_cast<const char*>(p.v) + (u * p.kv_stride + g_ch * 8) * 2;
+      const int64_t ukv = p.kv_div > 1 ? u / p.kv_div : u;  // the unit's K/V block
+      g_kb = static_cast<const char*>(p.k) + (ukv * p.kv_stride + g_ch * 8) * 2;
+      if constexpr (MODE == MODE_DECODE) g_vb = static_cast<const char*>(p.v) + (ukv * p.kv_stride + g_ch * 8) * 2;
     }
     const uint32_t dst0 = stage_base + stage * L::STAGE + g_dst;
     const int* ring = s_idx + slot * KT;

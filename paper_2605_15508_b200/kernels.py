@@ -164,6 +164,42 @@ def sparse_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
     return out, lse
 
 
+def sparse_prefill(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, *, idx, cnt, scale=None,
+                   out=None, lse=None, out_dtype=None, status=None, workspace: Workspace | None = None, stream=None):
+    """Sparse prefill attention (STS-PD): every query row has its own key list.
+
+    q: [G, n, M, d] (G K/V blocks, n query rows, M heads sharing block g and
+    the row's mask; M = 1 for MHA); k_cache/v_cache: [G, N, d] views (unit
+    inner stride); idx/cnt: int32 [G*n, ld] / [G*n] per-row key lists (causal
+    by construction).  Returns (out [G, n, M, d], lse fp32 [G, n, M]).
+    Semantics: include/sts_b200.h sts_sparse_prefill.
+    """
+    _require_cuda(q, k_cache, v_cache, idx, cnt)
+    if q.dtype not in STS_DTYPE or k_cache.dtype != q.dtype or v_cache.dtype != q.dtype:
+        raise ValueError("q, k_cache, v_cache must share dtype float32 or bfloat16")
+    G, n, M, d = q.shape
+    q = q.contiguous()
+    if k_cache.stride(-1) != 1 or v_cache.stride() != k_cache.stride():
+        raise ValueError("k_cache/v_cache must be [G, N, d] views with unit inner stride and equal strides")
+    if idx.shape[0] != G * n or cnt.shape[0] != G * n:
+        raise ValueError("idx/cnt need one row per (block, query row)")
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    out_dtype = q.dtype if out_dtype is None else out_dtype
+    dev = q.device
+    if out is None:
+        out = torch.empty((G, n, M, d), dtype=out_dtype, device=dev)
+    if lse is None:
+        lse = torch.empty((G, n, M), dtype=torch.float32, device=dev)
+    lib = _lib.load()
+    wbytes = lib.sts_sparse_decode_workspace_bytes(G * n, M, d, 1)
+    ws = workspace or _ws("decode", dev)
+    wbuf, wlen = ws.get(wbytes)
+    call("sts_sparse_prefill", STS_DTYPE[q.dtype], STS_DTYPE[out_dtype], ptr(q), ptr(k_cache), ptr(v_cache),
+         k_cache.stride(0), k_cache.stride(1), G, n, M, d, ptr(idx), idx.stride(0), ptr(cnt), scale, ptr(out),
+         ptr(lse), ptr(status), ptr(wbuf), wlen, stream_handle(stream))
+    return out, lse
+
+
 def draft_lse(q: torch.Tensor, k_cache: torch.Tensor, *, G: int, R: int, base: int, n_keys=None,
               pos_offset: int = 0, scale=None, out=None, workspace: Workspace | None = None,
               stream=None):

@@ -178,6 +178,43 @@ def sparse_attention(q, keys, values, mask) -> np.ndarray:
     return out[0, 0].cpu().numpy()
 
 
+def sparse_prefill_attention(q, keys, values, row_masks, positions=None) -> np.ndarray:
+    """Masked prefill attention of one head: row r (at position ``positions[r]``,
+    default r) attends exactly ``row_masks[r]`` — the masked path of
+    toymodel._run_block (src/toymodel.py:315-348, row validation
+    ``_row_allowed`` :257-272) reached through forward_prefill(masks=...)
+    with masks from draft_masks_prefill.  One fp32 kernel launch for all rows.
+    Returns float32 [m, d]."""
+    m = len(row_masks)
+    n = keys.shape[0]
+    pos = np.arange(m) if positions is None else np.asarray(positions, dtype=np.int64)
+    lists = []
+    for r, mr in enumerate(row_masks):
+        idx = np.asarray(mr, dtype=np.int64).ravel()
+        if idx.size == 0:
+            raise ContractViolation(f"empty mask row at position {int(pos[r])}")
+        if idx.min() < 0 or idx.max() > pos[r] or idx.max() >= n:
+            raise ContractViolation(f"mask at position {int(pos[r])} escapes the causal prefix")
+        lists.append(idx)
+    dev = _device()
+    width = max(len(x) for x in lists) if lists else 1
+    idx_t = torch.zeros((m, width), dtype=torch.int32)
+    cnt_t = torch.zeros((m,), dtype=torch.int32)
+    for r, x in enumerate(lists):
+        idx_t[r, : x.size] = torch.from_numpy(x.astype(np.int32))
+        cnt_t[r] = x.size
+
+    def dev32(x):
+        t = x if isinstance(x, torch.Tensor) else torch.from_numpy(np.asarray(x, dtype=np.float32))
+        return t.to(device=dev, dtype=torch.float32).contiguous()
+
+    qd = dev32(q).reshape(1, m, 1, -1)
+    kd = dev32(keys).reshape(1, n, -1)
+    vd = dev32(values).reshape(1, n, -1)
+    out, _ = kernels.sparse_prefill(qd, kd, vd, idx=idx_t.to(dev), cnt=cnt_t.to(dev))
+    return out[0, :, 0].cpu().numpy()
+
+
 def dump_masks(fh, step: int, masks: dict) -> None:
     """Append one JSON document describing a step's masks (src/sparsity.py:176-185)."""
     heads = {}
