@@ -15,6 +15,8 @@
 //
 // Keys live in shared memory when the row fits (<= SEL_SMEM_MAX_LEN), else in
 // a per-CTA slot of the global workspace (persistent grid over rows).
+#include <stdlib.h>
+
 #include "sts_common.cuh"
 
 namespace sts {
@@ -541,6 +543,274 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(SelectParams p) 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Cluster select (token mode): a thread-block cluster of C CTAs per row, CTA c
+// holding the keys of positions [c*n/C, (c+1)*n/C) in its shared memory.  The
+// radix passes exchange 256-bin histograms through distributed shared memory
+// (every CTA sums the same C histograms, so every CTA picks the same digit);
+// after the threshold is known each CTA publishes its tie and selection
+// counts, derives its tie share (ties go to the lowest global index) and its
+// output offset, and emits its range.  Rows are spread over C SMs instead of
+// one: the per-row latency of the single-CTA kernel is what bounds it.
+// ---------------------------------------------------------------------------
+constexpr int CSEL_THREADS = 512;
+constexpr int CSEL_WARPS = CSEL_THREADS / 32;
+constexpr int CSEL_BITS = 8;
+constexpr int CSEL_BINS = 1 << CSEL_BITS;
+constexpr int CSEL_KEYS = 16384;  // keys per CTA held in shared memory (64 KB)
+
+struct CSelShared {
+  uint32_t hist[CSEL_BINS];
+  int xch[8];          // values published to the cluster
+  int warp_tot[CSEL_WARPS];
+  int bcast[4];
+};
+
+__device__ __forceinline__ unsigned csel_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void csel_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t csel_ld(const void* local, unsigned rank) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(local), ra, v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(ra) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ int csel_block_scan(int v, int* warp_tot, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int x = lane < CSEL_WARPS ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    if (lane < CSEL_WARPS) warp_tot[lane] = x;
+  }
+  __syncthreads();
+  const int before = warp > 0 ? warp_tot[warp - 1] : 0;
+  total = warp_tot[CSEL_WARPS - 1];
+  __syncthreads();
+  return before + incl - v;
+}
+
+template <int C>
+__global__ void __launch_bounds__(CSEL_THREADS) select_cluster_kernel(SelectParams p) {
+  __shared__ CSelShared sh;
+  extern __shared__ __align__(16) uint32_t csel_keys[];  // CSEL_KEYS keys (dynamic shared memory)
+  const unsigned c = csel_rank();
+  const int64_t r = blockIdx.x / C;
+  const int tid = threadIdx.x;
+  const int n = p.row_len ? p.row_len[r] : p.n_common;
+  int32_t* out = p.idx_out + r * p.idx_ld;
+  int32_t srcs[8];
+  if (p.row_src) {
+    for (int q = 0; q < p.nsrc && q < 8; ++q) srcs[q] = p.row_src[r * p.nsrc + q];
+  } else {
+    srcs[0] = (int32_t)r;
+  }
+  int b;
+  if (p.budget_is_fraction) {
+    const double cc = ceil(p.budget * (double)n);
+    b = cc < 1.0 ? 1 : (int)cc;
+  } else {
+    b = (int)p.budget;
+  }
+  const int lo = (int)((int64_t)c * (n > 0 ? n : 0) / C), hi = (int)((int64_t)(c + 1) * (n > 0 ? n : 0) / C);
+  const int len = hi - lo;
+  const bool dense = n > 0 && b >= n;
+  const bool cur = (p.flags & STS_SEL_CURRENT) != 0, sink = (p.flags & STS_SEL_SINK) != 0;
+  const int lo_extra = p.recent_window > 0 ? n - p.recent_window : n;
+  auto extra = [&](int g) { return g >= lo_extra || (sink && g == 0) || (cur && g == n - 1); };
+
+  // 1. keys of this CTA's positions (+ OR / AND of the varying bits)
+  uint32_t k_or = 0u, k_and = 0xffffffffu;
+  if (!dense)
+    for (int j = tid; j < len; j += CSEL_THREADS) {
+      const uint32_t key = f32_key(row_value(p, srcs, lo + j));
+      csel_keys[j] = key;
+      k_or |= key;
+      k_and &= key;
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    k_or |= __shfl_xor_sync(0xffffffffu, k_or, o);
+    k_and &= __shfl_xor_sync(0xffffffffu, k_and, o);
+  }
+  if (tid < CSEL_BINS) sh.hist[tid] = 0;
+  if (tid == 0) {
+    sh.bcast[0] = 0;
+    sh.bcast[1] = -1;
+  }
+  __syncthreads();
+  if ((tid & 31) == 0) {
+    atomicOr(reinterpret_cast<unsigned*>(&sh.bcast[0]), k_or);
+    atomicAnd(reinterpret_cast<unsigned*>(&sh.bcast[1]), k_and);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    sh.xch[0] = sh.bcast[0];
+    sh.xch[1] = sh.bcast[1];
+  }
+  csel_sync();
+  uint32_t g_or = 0u, g_and = 0xffffffffu;
+  for (unsigned q = 0; q < (unsigned)C; ++q) {
+    g_or |= csel_ld(&sh.xch[0], q);
+    g_and &= csel_ld(&sh.xch[1], q);
+  }
+
+  // 2. radix passes over the varying bits, 8 bits per pass, histograms summed
+  //    over the cluster
+  uint32_t prefix = 0u, pmask = 0u;
+  int krem = b, ties_g = 0;
+  bool resolved = dense || n <= 0;
+  const uint32_t diff = g_or ^ g_and;
+  if (!resolved && diff == 0u) {  // every committed key equal: all ties
+    prefix = g_and;
+    pmask = 0xffffffffu;
+    ties_g = n;
+    resolved = true;
+  }
+  int top = resolved ? -1 : 31 - __clz((int)diff);
+  if (!resolved) {
+    pmask = top >= 31 ? 0u : ~((2u << top) - 1u);
+    prefix = g_and & pmask;
+  }
+  while (!resolved) {
+    const int s0 = top - CSEL_BITS + 1 < 0 ? 0 : top - CSEL_BITS + 1;
+    const int width = top - s0 + 1;
+    const uint32_t dm = (1u << width) - 1u;
+    csel_sync();  // every CTA is done reading the previous pass's histograms
+    if (tid < CSEL_BINS) sh.hist[tid] = 0;
+    __syncthreads();
+    for (int j = tid; j < len; j += CSEL_THREADS) {
+      const uint32_t key = csel_keys[j];
+      if ((key & pmask) == prefix) atomicAdd(&sh.hist[(key >> s0) & dm], 1u);
+    }
+    csel_sync();
+    // every CTA sums the same C histograms and finds the same digit
+    int cnt = 0;
+    if (tid < CSEL_BINS)
+      for (unsigned q = 0; q < (unsigned)C; ++q) cnt += (int)csel_ld(&sh.hist[tid], q);
+    // descending inclusive scan over bins (bin 255 first): thread tid holds bin 255 - tid
+    int v = tid < CSEL_BINS ? 0 : 0;
+    __shared__ int s_cnt[CSEL_BINS];
+    if (tid < CSEL_BINS) s_cnt[tid] = cnt;
+    __syncthreads();
+    v = tid < CSEL_BINS ? s_cnt[CSEL_BINS - 1 - tid] : 0;
+    int tot;
+    const int excl = csel_block_scan(v, sh.warp_tot, tot);
+    if (tid < CSEL_BINS && excl < krem && krem <= excl + v) {
+      sh.bcast[2] = CSEL_BINS - 1 - tid;
+      sh.bcast[3] = excl;
+      sh.xch[7] = v;
+    }
+    __syncthreads();
+    const int digit = sh.bcast[2], above = sh.bcast[3], inbin = sh.xch[7];
+    prefix |= (uint32_t)digit << s0;
+    pmask |= dm << s0;
+    krem -= above;
+    if (s0 == 0 || krem == inbin) {
+      ties_g = inbin;
+      resolved = true;
+    }
+    top = s0 - 1;
+  }
+
+  // 3. round A: this CTA's threshold ties -> its share of them (ties go to the
+  //    lowest global index, i.e. to the lower CTAs first)
+  const bool all_ties = krem >= ties_g;  // every key of the final bin is taken
+  int t_loc = 0;
+  if (!dense && n > 0)
+    for (int j = tid; j < len; j += CSEL_THREADS) t_loc += (csel_keys[j] & pmask) == prefix ? 1 : 0;
+  int tt;
+  csel_block_scan(t_loc, sh.warp_tot, tt);
+  if (tid == 0) sh.xch[2] = tt;
+  csel_sync();
+  int tie_before = 0;
+  for (unsigned q = 0; q < c; ++q) tie_before += (int)csel_ld(&sh.xch[2], q);
+  const int need = all_ties ? 0x7fffffff : krem - tie_before;  // ties this CTA takes, by local rank
+
+  // selection flags of 4 consecutive local positions (block-wide tie ranks)
+  auto flags4 = [&](int j0, int& run_tie) -> uint32_t {
+    uint32_t sel = 0, eq = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = j0 + q;
+      if (j >= len) break;
+      const uint32_t mk = csel_keys[j] & pmask;
+      if (mk > prefix) sel |= 1u << q;
+      else if (mk == prefix) eq |= 1u << q;
+    }
+    int tie_tot;
+    int rank = run_tie + csel_block_scan(__popc(eq), sh.warp_tot, tie_tot);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if ((eq >> q) & 1u) {
+        if (rank < need) sel |= 1u << q;
+        ++rank;
+      }
+      if (j0 + q < len && extra(lo + j0 + q)) sel |= 1u << q;
+    }
+    run_tie += tie_tot;
+    return sel;
+  };
+
+  // round B: this CTA's selection count -> its output offset
+  int sel_loc = 0;
+  if (dense) {
+    sel_loc = len;
+  } else if (n > 0) {
+    int run_tie = 0, cnt_acc = 0;
+    for (int base = 0; base < len; base += 4 * CSEL_THREADS) cnt_acc += __popc(flags4(base + 4 * tid, run_tie));
+    csel_block_scan(cnt_acc, sh.warp_tot, sel_loc);
+  }
+  if (tid == 0) sh.xch[3] = sel_loc;
+  csel_sync();
+  int out_off = 0, total = 0;
+  for (unsigned q = 0; q < (unsigned)C; ++q) {
+    const int sq = (int)csel_ld(&sh.xch[3], q);
+    out_off += q < c ? sq : 0;
+    total += sq;
+  }
+  csel_sync();  // published counts read by everyone (a CTA may now exit)
+
+  // 4. emit this CTA's positions in ascending order
+  if (dense) {
+    for (int j = tid; j < len; j += CSEL_THREADS) write_idx(p, out, out_off + j, lo + j);
+  } else if (n > 0) {
+    int run_sel = 0, run_tie = 0;
+    for (int base = 0; base < len; base += 4 * CSEL_THREADS) {
+      const int j0 = base + 4 * tid;
+      const uint32_t sel = flags4(j0, run_tie);
+      int sel_tot;
+      int pos = out_off + run_sel + csel_block_scan(__popc(sel), sh.warp_tot, sel_tot);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if ((sel >> q) & 1u) write_idx(p, out, pos++, lo + j0 + q);
+      run_sel += sel_tot;
+    }
+  }
+  // 5. in-block tail and the count (last CTA of the cluster)
+  if (c == (unsigned)(C - 1)) {
+    for (int t = tid; t < p.tail_len; t += CSEL_THREADS) write_idx(p, out, total + t, (n > 0 ? n : 0) + t);
+    if (tid == 0) p.cnt_out[r] = total + p.tail_len;
+  }
+}
+
 // page_aggregate as a standalone op (src/sparsity.py:72-83): one thread per page
 __global__ void page_aggregate_kernel(SelectParams p, double* out, int64_t out_ld) {
   const int64_t r = blockIdx.y;
@@ -621,6 +891,46 @@ extern "C" int sts_select_topk(const float* scores_dev, int64_t ld, const int32_
   p.status = status_dev;
   p.buf_bytes = key_buf_bytes(max_len, page_size);
 
+  // experimental (STS_SELECT_CLUSTER=1): token-mode rows that fit C x 16K keys
+  // through one thread-block cluster per row.  Measured slower than the
+  // single-CTA kernel at c2 (150 vs 63 us: 8-bit digits without candidate
+  // compaction serialise on hot shared-memory histogram bins), so off by default.
+  {
+    static const int env = getenv("STS_SELECT_CLUSTER") ? atoi(getenv("STS_SELECT_CLUSTER")) : 0;
+    const int64_t per = CSEL_KEYS;
+    if (env == 1 && page_size == 1 && max_len > 0 && max_len <= 8 * per && rows * 2 <= (int64_t)1 << 30) {
+      int C = (int)((max_len + per - 1) / per);
+      C = C < 2 ? 2 : (C <= 2 ? 2 : (C <= 4 ? 4 : 8));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(rows * C));
+      cfg.blockDim = dim3(CSEL_THREADS);
+      cfg.dynamicSmemBytes = CSEL_KEYS * 4;
+      cfg.stream = static_cast<cudaStream_t>(stream);
+      static const bool attr_ok =
+          cudaFuncSetAttribute(select_cluster_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, CSEL_KEYS * 4) ==
+              cudaSuccess &&
+          cudaFuncSetAttribute(select_cluster_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, CSEL_KEYS * 4) ==
+              cudaSuccess &&
+          cudaFuncSetAttribute(select_cluster_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, CSEL_KEYS * 4) ==
+              cudaSuccess;
+      STS_REQUIRE(attr_ok, STS_ERR_CUDA, "cluster select setup failed");
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = C;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      p.gbuf = nullptr;
+      cudaError_t e;
+      if (C == 2) e = cudaLaunchKernelEx(&cfg, select_cluster_kernel<2>, p);
+      else if (C == 4) e = cudaLaunchKernelEx(&cfg, select_cluster_kernel<4>, p);
+      else e = cudaLaunchKernelEx(&cfg, select_cluster_kernel<8>, p);
+      STS_CUDA_CHECK(e);
+      count_launch();
+      return STS_OK;
+    }
+  }
   const size_t sh_bytes = (sizeof(SelShared) + 15) & ~size_t(15);
   size_t smem = sh_bytes;
   int grid;

@@ -184,3 +184,21 @@ def test_capacity_status_flag(cuda_ok):
     kernels.select_topk(x, budget=50, include_current=False, idx_ld=10, status=status)
     torch.cuda.synchronize()
     assert status.item() & 0x1
+
+
+def test_cluster_select_variant(cuda_ok):
+    """The selection parity suite again through the experimental cluster select
+    (STS_SELECT_CLUSTER=1: token-mode rows split over a thread-block cluster,
+    histograms exchanged through DSMEM), in a subprocess because the library
+    reads the knob once."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, STS_SELECT_CLUSTER="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", str(root / "tests" / "test_gpu_select.py"), "-q", "-x",
+                        "-p", "no:cacheprovider", "-k", "not cluster_select_variant"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
