@@ -24,6 +24,19 @@ def _require_cuda(*ts):
             raise ValueError("tensor must live on a CUDA device (no CPU path exists)")
 
 
+def _require_kv(*ts, host_kv=False):
+    """K/V caches live in HBM, or (host_kv=True, the offload tier) in pinned,
+    device-mapped host memory that the kernels read over the host link."""
+    for t in ts:
+        if t is None:
+            continue
+        if t.is_cuda:
+            continue
+        if host_kv and t.is_pinned():
+            continue
+        raise ValueError("K/V must be CUDA tensors (or pinned host tensors with host_kv=True)")
+
+
 class Workspace:
     """Grow-only device scratch buffer (allocate once, reuse every step)."""
 
@@ -118,7 +131,8 @@ def select_topk(scores: torch.Tensor, *, budget, page_size: int = 1, include_cur
 def sparse_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, *, idx=None,
                   cnt=None, n_dense: int = 0, member=None, causal_base: int = -1,
                   rows_per_head: int = 1, pos_offset: int = 0, scale=None, splits=None, out=None,
-                  lse=None, status=None, out_dtype=None, workspace: Workspace | None = None, stream=None):
+                  lse=None, status=None, out_dtype=None, host_kv: bool = False, workspace: Workspace | None = None,
+                  stream=None):
     """Gathered-KV sparse flash-decode.
 
     q: [U, M, d] (bf16 or fp32); k_cache/v_cache: [U, N, d] views of the same
@@ -126,8 +140,11 @@ def sparse_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
     [U, N, 2, d] passes kv[..., 0, :] and kv[..., 1, :]).  idx/cnt: int32 [U, ld] / [U] key lists
     (None => dense keys 0..n_dense-1).  Returns (out [U, M, d] q.dtype,
     lse fp32 [U, M]).  Semantics: include/sts_b200.h sts_sparse_decode.
+    ``host_kv``: the caches may be pinned host tensors (KV offload tier): the
+    same kernel then gathers only the selected rows over the host link.
     """
-    _require_cuda(q, k_cache, v_cache, idx, cnt, member)
+    _require_cuda(q, idx, cnt, member)
+    _require_kv(k_cache, v_cache, host_kv=host_kv)
     if q.dtype not in STS_DTYPE or k_cache.dtype != q.dtype or v_cache.dtype != q.dtype:
         raise ValueError("q, k_cache, v_cache must share dtype float32 or bfloat16")
     U, M, d = q.shape

@@ -253,3 +253,28 @@ def test_stream_k_schedule_variant(cuda_ok):
                         "-p", "no:cacheprovider", "-k", "not stream_k_schedule_variant"],
                        env=env, cwd=root, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_host_resident_kv_offload(cuda_ok):
+    """KV offload tier: the caches in pinned host memory, read by the same
+    kernel over the host link (only the selected rows cross it) — results
+    identical to the HBM-resident run."""
+    import torch
+
+    from paper_2605_15508_b200 import kernels
+
+    rng = np.random.default_rng(9)
+    U, M, d, N = 6, 20, 128, 2000
+    q = torch.from_numpy(rng.standard_normal((U, M, d)).astype(np.float32)).bfloat16().cuda()
+    k = torch.from_numpy(rng.standard_normal((U, N, d)).astype(np.float32)).bfloat16()
+    v = torch.from_numpy(rng.standard_normal((U, N, d)).astype(np.float32)).bfloat16()
+    sel = np.stack([np.sort(rng.choice(N, 300, replace=False)) for _ in range(U)]).astype(np.int32)
+    idx = torch.from_numpy(sel).cuda()
+    cnt = torch.full((U,), 300, dtype=torch.int32, device="cuda")
+    dev_out, dev_lse = kernels.sparse_decode(q, k.cuda(), v.cuda(), idx=idx, cnt=cnt)
+    kh, vh = k.pin_memory(), v.pin_memory()
+    host_out, host_lse = kernels.sparse_decode(q, kh, vh, idx=idx, cnt=cnt, host_kv=True)
+    torch.cuda.synchronize()
+    assert torch.equal(dev_out, host_out) and torch.equal(dev_lse, host_lse)
+    with pytest.raises(ValueError):
+        kernels.sparse_decode(q, k, v, idx=idx, cnt=cnt)  # pageable host memory is refused
