@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
   // ---- per-warp state: rows rA = 16*warp + lane/4 and rB = rA + 8 ----
   const int rA = warp * 16 + (lane >> 2), rB = rA + 8;
   const int rmodA = rA % p.rows_per_head, rmodB = rB % p.rows_per_head;
+  const bool rB_live = warp * 16 + 8 < M;  // warp-uniform: this warp's rB rows hold queries
   const float sl2 = p.scale * LOG2E;
   [[maybe_unused]] const int probs_G = M / p.rows_per_head;  // q-heads per unit (MODE_PROBS)
   const int causal_shift = p.pos_offset - p.causal_base;
@@ -518,8 +519,9 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
         const int key = nt * 8 + 2 * (lane & 3);
         *reinterpret_cast<float2*>(s_prob + rA * KPS + key) =
             make_float2(fast_exp2(s[nt][0] - lse2A), fast_exp2(s[nt][1] - lse2A));
-        *reinterpret_cast<float2*>(s_prob + rB * KPS + key) =
-            make_float2(fast_exp2(s[nt][2] - lse2B), fast_exp2(s[nt][3] - lse2B));
+        if (rB_live)
+          *reinterpret_cast<float2*>(s_prob + rB * KPS + key) =
+              make_float2(fast_exp2(s[nt][2] - lse2B), fast_exp2(s[nt][3] - lse2B));
       }
       __syncthreads();
       const int R = p.rows_per_head;
@@ -580,13 +582,17 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
         tB = fmaxf(tB, fmaxf(s[nt][2], s[nt][3]));
       }
       tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, 1));
-      tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 1));
       tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, 2));
-      tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 2));
-      const float nA = fmaxf(m_a, tA), nB = fmaxf(m_b, tB);
+      if (rB_live) {
+        tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 1));
+        tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 2));
+      } else {
+        tB = 0.f;  // padding rows: keep their state constant (m = 0, nothing accumulated)
+      }
+      const float nA = fmaxf(m_a, tA), nB = rB_live ? fmaxf(m_b, tB) : 0.f;
       // rows with no admissible key yet keep everything at zero
       const float bA = nA == -INFINITY ? 0.f : nA, bB = nB == -INFINITY ? 0.f : nB;
-      const float alA = fast_exp2(m_a - bA), alB = fast_exp2(m_b - bB);
+      const float alA = fast_exp2(m_a - bA), alB = rB_live ? fast_exp2(m_b - bB) : 1.f;
       m_a = nA;
       m_b = nB;
       float sumA = 0.f, sumB = 0.f;
@@ -594,7 +600,8 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
         const float p0 = fast_exp2(s[nt][0] - bA), p1 = fast_exp2(s[nt][1] - bA);
-        const float p2 = fast_exp2(s[nt][2] - bB), p3 = fast_exp2(s[nt][3] - bB);
+        // rows rB of the last warp are often all padding (M = 20: rows 24..31)
+        const float p2 = rB_live ? fast_exp2(s[nt][2] - bB) : 0.f, p3 = rB_live ? fast_exp2(s[nt][3] - bB) : 0.f;
         sumA += p0 + p1;
         sumB += p2 + p3;
         if constexpr (MODE == MODE_DECODE) {

@@ -1,5 +1,7 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 300 python -m pytest tests/test_gpu_attention.py -q -p no:cacheprovider --timeout 200 -k "offload or golden" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-tail -3 gpurun_out/pytest_gpu.log
-timeout 600 python tools/bench_offload.py 8 > gpurun_out/offload.log 2>&1
+timeout 600 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 200 > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+tail -2 gpurun_out/pytest_gpu.log
+B="python bench.py --steps 20 --warmup 5 --no-cpu-baseline"
+: > gpurun_out/ab.log
+for rep in 1 2; do echo "== run" >> gpurun_out/ab.log; timeout 300 $B >> gpurun_out/ab.log 2>&1; done
