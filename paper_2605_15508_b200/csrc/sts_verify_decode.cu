@@ -157,9 +157,10 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
   }
 
   // ---- tile space and this CTA's range (block-parallel scan) ----
+  // (the cluster schedule needs none of this: each cluster knows its unit)
   __shared__ long long s_scan[NW + 3];
   const int64_t cpt = (U + NTH - 1) / NTH;
-  const int64_t ub = (int64_t)tid * cpt, ue = ub + cpt < U ? ub + cpt : U;
+  const int64_t ub = (int64_t)tid * cpt, ue = CS > 1 ? ub : (ub + cpt < U ? ub + cpt : U);
   int64_t mine = 0;
   for (int64_t u0 = ub; u0 < ue; u0 += 4) {
     int t4[4];
@@ -183,7 +184,7 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
     before += ww < warp ? v : 0;
     T += v;
   }
-  if (T == 0) return;  // (a cluster's CTAs all see the same T)
+  if (CS == 1 && T == 0) return;
 
   // ---- schedule.  CS == 1: one contiguous tile range per CTA (stream-K); a
   // piece of a unit is (CTA range, unit), its partial slot is range + unit, and
