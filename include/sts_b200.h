@@ -208,6 +208,19 @@ STS_API int sts_row_union(const int32_t* idx_in_dev, int64_t in_ld, const int32_
                   int64_t out_ld, int32_t* cnt_out_dev, int32_t* status_dev, void* stream);
 
 /* ------------------------------------------------------------------------
+ * Algorithm 1 (offline head mapping): replaces the bitmask
+ * overlap of headmap.find_head_mapping (src/headmap.py:76-125).
+ * sts_topk_bitsets: row r's index list (idx_dev[r*idx_ld + j], j < cnt_dev[r])
+ *   -> bits_out[r][words] (bit i set iff i listed; zeroed first).
+ * sts_bitset_overlap: scores[ia][ib] += sum_w popc(a[ia][w] & b[ib][w]) over
+ *   W words per head (16-byte aligned, W % 4 == 0), uint64, deterministic.
+ * ---------------------------------------------------------------------- */
+STS_API int sts_topk_bitsets(const int32_t* idx_dev, int64_t idx_ld, const int32_t* cnt_dev, int64_t rows,
+                             int32_t words, uint32_t* bits_out_dev, void* stream);
+STS_API int sts_bitset_overlap(const uint32_t* a_dev, int32_t Ta, const uint32_t* b_dev, int32_t Tb, int64_t W,
+                               unsigned long long* scores_dev, void* stream);
+
+/* ------------------------------------------------------------------------
  * Sequence-sharded selection (context-parallel decode): the
  * global top-k of a row whose positions are split over P ranks, without
  * moving scores.  Replaces numkit.topk_indices / sparsity._select_row

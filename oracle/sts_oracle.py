@@ -460,3 +460,32 @@ def dist_select_protocol(values_local, lo: int, n_global: int, k: int, rank: int
         take[np.nonzero(tie)[0][:need]] = True
         out.append(lo + np.nonzero(above | take)[0].astype(np.int64))
     return out
+
+
+# ---------------------------------------------------------------------------
+# 6. Algorithm 1 (src/headmap.py:59-125): best-overlap draft head per target
+# ---------------------------------------------------------------------------
+
+
+def rowwise_topk_sets(matrix, k: int):
+    """src/headmap.py:59-62: top-k of each row's causal prefix."""
+    n = matrix.shape[0]
+    return [topk_indices(matrix[t, : t + 1], k) for t in range(n)]
+
+
+def find_head_mapping(samples, draft_heads, target_heads, k: int) -> dict:
+    """src/headmap.py:83-125 with python-set intersections (the reference
+    uses integer bitmasks; the counts are the same).  samples: list of
+    (draft dict, target dict).  Returns {target head: (draft head, score)}."""
+    totals = {th: np.zeros(len(draft_heads), dtype=np.int64) for th in target_heads}
+    for draft, target in samples:
+        dsets = {dh: [set(s.tolist()) for s in rowwise_topk_sets(draft[dh], k)] for dh in draft_heads}
+        for th in target_heads:
+            tsets = [set(s.tolist()) for s in rowwise_topk_sets(target[th], k)]
+            for j, dh in enumerate(draft_heads):
+                totals[th][j] += sum(len(a & b) for a, b in zip(tsets, dsets[dh]))
+    out = {}
+    for th in target_heads:
+        best = int(np.argmax(totals[th]))
+        out[th] = (draft_heads[best], int(totals[th][best]))
+    return out

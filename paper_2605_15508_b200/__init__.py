@@ -19,7 +19,7 @@ from .errors import (
     InputError,
     SpecSparseError,
 )
-from .headmap import HeadMapping, MappingSet, load_mapping
+from .headmap import HeadMapping, MappingSet, find_head_mapping, load_mapping
 from .sparsity import (
     SparsityConfig,
     draft_masks_decode,
@@ -46,6 +46,7 @@ __all__ = [
     "SpecSparseError",
     "draft_masks_decode",
     "draft_masks_prefill",
+    "find_head_mapping",
     "dump_masks",
     "load_mapping",
     "page_aggregate",

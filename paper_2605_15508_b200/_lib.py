@@ -49,6 +49,8 @@ SIGNATURES = {
                                   _p, _i32, _p, _i64, _p]),
     "sts_lse_merge": (C.c_int, [_p, _p, _i32, _i64, _i32, _i32, _p, _p, _p]),
     "sts_row_union": (C.c_int, [_p, _i64, _p, _p, _i64, _i32, _i32, _p, _p, _p, _i64, _p, _p, _p]),
+    "sts_topk_bitsets": (C.c_int, [_p, _i64, _p, _i64, _i32, _p, _p]),
+    "sts_bitset_overlap": (C.c_int, [_p, _i32, _p, _i32, _i64, _p, _p]),
     "sts_dist_select_rounds": (_i32, [_i32]),
     "sts_dist_select_workspace_bytes": (_sz, [_i64, _i32, _i32]),
     "sts_dist_select_begin": (C.c_int, [_p, _p, _p, _sz, _p]),

@@ -140,3 +140,80 @@ extern "C" int sts_row_union(const int32_t* idx_in_dev, int64_t in_ld, const int
   STS_LAUNCH_CHECK();
   return STS_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Algorithm 1 (headmap.find_head_mapping, src/headmap.py:83-125) on the GPU:
+// per-row top-k index lists -> bitsets, then for every (a-head, b-head) pair
+// the total popcount of the AND of their bitsets (integer: deterministic).
+// ---------------------------------------------------------------------------
+namespace sts {
+namespace {
+
+__global__ void bitset_scatter_kernel(const int32_t* __restrict__ idx, int64_t idx_ld, const int32_t* __restrict__ cnt,
+                                      int32_t words, uint32_t* bits) {
+  const int64_t r = blockIdx.x;
+  const int c = cnt[r];
+  uint32_t* row = bits + r * words;
+  for (int j = threadIdx.x; j < c; j += blockDim.x) {
+    const int i = idx[r * idx_ld + j];
+    if (i >= 0 && i < words * 32) atomicOr(row + (i >> 5), 1u << (i & 31));
+  }
+}
+
+constexpr int OVL_THREADS = 256;
+
+__global__ void __launch_bounds__(OVL_THREADS) bitset_overlap_kernel(const uint32_t* __restrict__ a,
+                                                                     const uint32_t* __restrict__ b,
+                                                                     int64_t W, int32_t Tb,
+                                                                     unsigned long long* scores) {
+  const int64_t ia = blockIdx.y, ib = blockIdx.x;
+  const uint4* pa = reinterpret_cast<const uint4*>(a + ia * W);
+  const uint4* pb = reinterpret_cast<const uint4*>(b + ib * W);
+  unsigned long long acc = 0;
+  const int64_t W4 = W / 4;
+  for (int64_t w = threadIdx.x; w < W4; w += OVL_THREADS) {
+    const uint4 x = __ldg(pa + w), y = __ldg(pb + w);
+    acc += __popc(x.x & y.x) + __popc(x.y & y.y) + __popc(x.z & y.z) + __popc(x.w & y.w);
+  }
+  for (int64_t w = 4 * W4 + threadIdx.x; w < W; w += OVL_THREADS) acc += __popc(a[ia * W + w] & b[ib * W + w]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ unsigned long long s_acc[OVL_THREADS / 32];
+  if ((threadIdx.x & 31) == 0) s_acc[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int i = 0; i < OVL_THREADS / 32; ++i) t += s_acc[i];
+    scores[ia * Tb + ib] += t;  // one block per pair: no race
+  }
+}
+
+}  // namespace
+}  // namespace sts
+
+extern "C" int sts_topk_bitsets(const int32_t* idx_dev, int64_t idx_ld, const int32_t* cnt_dev, int64_t rows,
+                                int32_t words, uint32_t* bits_out_dev, void* stream) {
+  STS_REQUIRE(rows >= 0 && words >= 1, STS_ERR_CONTRACT, "rows must be >= 0 and words >= 1");
+  if (rows == 0) return STS_OK;
+  STS_REQUIRE(idx_dev && cnt_dev && bits_out_dev, STS_ERR_CONTRACT, "null buffer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  STS_CUDA_CHECK(cudaMemsetAsync(bits_out_dev, 0, (size_t)rows * words * 4, st));
+  sts::bitset_scatter_kernel<<<(unsigned)rows, 128, 0, st>>>(idx_dev, idx_ld, cnt_dev, words, bits_out_dev);
+  STS_LAUNCH_CHECK();
+  return STS_OK;
+}
+
+extern "C" int sts_bitset_overlap(const uint32_t* a_dev, int32_t Ta, const uint32_t* b_dev, int32_t Tb, int64_t W,
+                                  unsigned long long* scores_dev, void* stream) {
+  STS_REQUIRE(Ta >= 0 && Tb >= 0 && W >= 0, STS_ERR_CONTRACT, "bad overlap shape");
+  STS_REQUIRE(Ta <= 65535, STS_ERR_CONTRACT, "Ta must be <= 65535");
+  if (Ta == 0 || Tb == 0 || W == 0) return STS_OK;
+  STS_REQUIRE(a_dev && b_dev && scores_dev, STS_ERR_CONTRACT, "null buffer");
+  STS_REQUIRE((reinterpret_cast<uintptr_t>(a_dev) | reinterpret_cast<uintptr_t>(b_dev)) % 16 == 0 && W % 4 == 0,
+              STS_ERR_CONTRACT, "bitsets must be 16-byte aligned with W % 4 == 0");
+  dim3 grid((unsigned)Tb, (unsigned)Ta);
+  sts::bitset_overlap_kernel<<<grid, sts::OVL_THREADS, 0, static_cast<cudaStream_t>(stream)>>>(a_dev, b_dev, W, Tb,
+                                                                                               scores_dev);
+  STS_LAUNCH_CHECK();
+  return STS_OK;
+}

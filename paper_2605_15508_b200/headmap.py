@@ -1,10 +1,11 @@
 """Head-mapping tables consumed by the hot path (src/headmap.py:30-56, :170-186).
 
-Only the runtime side is here: ``HeadMapping.entries`` (target head ->
-(draft head, score)) and ``MappingSet.nearest``.  The offline search
-(find_head_mapping, Algorithm 1) is out of scope ("next").
-``to_table`` lowers a mapping to the int32 indirection table the kernels use
-instead of copying masks per target head.
+The runtime side: ``HeadMapping.entries`` (target head -> (draft head,
+score)) and ``MappingSet.nearest``; ``to_table`` lowers a mapping to the int32
+indirection table the kernels use instead of copying masks per target head.
+The offline search ``find_head_mapping`` (Algorithm 1) runs
+on the GPU: per-row top-k sets from the radix select, bitsets, and a popcount
+overlap kernel (include/sts_b200.h sts_topk_bitsets / sts_bitset_overlap).
 """
 
 from __future__ import annotations
@@ -92,3 +93,61 @@ def load_mapping(path) -> HeadMapping:
         raise InputError(f"bad mapping file {path}: {exc}") from exc
     return HeadMapping(int(doc["k"]), entries, str(doc.get("trace_set_id", "")),
                        doc.get("draft_config"), doc.get("target_config"))
+
+
+def find_head_mapping(ts, k: int) -> HeadMapping:
+    """Best-overlap draft head for every target head (src/headmap.py:83-125),
+    on the GPU.
+
+    ``ts``: a trace set (the reference's ``TraceSet`` or any object with
+    ``samples`` — each with ``draft`` / ``target`` dicts of causal attention
+    matrices [n, n] keyed (layer, head) — and ``draft_config`` /
+    ``target_config`` with ``layers`` and ``heads``).  Per sample and head,
+    row t's set is the top-k of its prefix [0, t] (``rowwise_topk_sets``, the
+    tie rule of topk_indices); score(th, dh) = sum over samples and rows of
+    |set_th(t) & set_dh(t)|; ties go to the smallest (layer, head).
+    """
+    import torch
+
+    from . import _lib, kernels
+    from ._lib import call, ptr, stream_handle
+
+    if k < 1:
+        raise ContractViolation(f"k must be >= 1, got {k}")
+    if not ts.samples:
+        raise InputError("cannot build a mapping from an empty trace set")
+    draft_heads = [(l, h) for l in range(ts.draft_config.layers) for h in range(ts.draft_config.heads)]
+    target_heads = [(l, h) for l in range(ts.target_config.layers) for h in range(ts.target_config.heads)]
+    if not torch.cuda.is_available():
+        raise RuntimeError("find_head_mapping runs on the GPU (there is no CPU fallback)")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    scores = torch.zeros((len(target_heads), len(draft_heads)), dtype=torch.int64, device=dev)
+
+    def bitsets(mats, heads, n, words):
+        rows = torch.stack([torch.as_tensor(np.asarray(mats[hk], dtype=np.float32)) for hk in heads]).to(dev)
+        rows = rows.reshape(len(heads) * n, n)
+        if n % 4:
+            rows = torch.nn.functional.pad(rows, (0, 4 - n % 4))
+        row_len = torch.arange(1, n + 1, dtype=torch.int32, device=dev).repeat(len(heads))
+        idx, cnt = kernels.select_topk(rows.contiguous(), row_len=row_len, budget=int(k), include_current=False)
+        bits = torch.empty((len(heads) * n, words), dtype=torch.int32, device=dev)
+        call("sts_topk_bitsets", ptr(idx), idx.stride(0), ptr(cnt), len(heads) * n, words, ptr(bits),
+             stream_handle())
+        return bits.reshape(len(heads), n * words)
+
+    for sample in ts.samples:
+        n = int(sample.length)
+        words = -(-n // 32)
+        words = -(-words // 4) * 4  # 16-byte rows for the vector loads
+        tb = bitsets(sample.target, target_heads, n, words)
+        db = bitsets(sample.draft, draft_heads, n, words)
+        call("sts_bitset_overlap", ptr(tb), len(target_heads), ptr(db), len(draft_heads), n * words, ptr(scores),
+             stream_handle())
+    totals = scores.cpu().numpy()
+    entries = {}
+    for i, th in enumerate(target_heads):
+        best = int(np.argmax(totals[i]))  # first max = lexicographically smallest draft head
+        entries[th] = (draft_heads[best], int(totals[i, best]))
+    cid = ts.content_id() if hasattr(ts, "content_id") else ""
+    return HeadMapping(k=k, entries=entries, trace_set_id=cid, draft_config=ts.draft_config,
+                       target_config=ts.target_config)

@@ -216,7 +216,44 @@ def main() -> None:
         rows=np.stack(rows),  # (4 steps, H, 104) zero-padded
         base=np.asarray(100),
     )
+    make_headmap_golden()
     print("golden vectors written to", OUT)
+
+
+def make_headmap_golden():
+    """Algorithm 1 (headmap.find_head_mapping, src/headmap.py:83-125) on
+    synthetic paired traces: 2 samples, draft 2L x 3H, target 2L x 4H, for
+    k in (1, 3, 8); softmax rows plus tie-heavy rows."""
+    sys.path.insert(0, str(REF))
+    from specsparse import headmap, numkit
+    from specsparse.toymodel import ModelConfig
+    from specsparse.tracestore import TraceSample, TraceSet
+
+    rng = np.random.default_rng(77)
+    dcfg = ModelConfig(layers=2, heads=3, head_dim=8, vocab=32, max_seq=64)
+    tcfg = ModelConfig(layers=2, heads=4, head_dim=8, vocab=32, max_seq=64)
+    samples, mats = [], {}
+    for si, n in enumerate((23, 40)):
+        def mat(tie):
+            z = rng.standard_normal((n, n)) * 2.0
+            m = numkit.row_softmax(z, range(1, n + 1)).astype(np.float32)
+            if tie:
+                m = (np.round(m * 16) / 16).astype(np.float32)
+            return m
+        draft = {(l, h): mat(h == 2) for l in range(2) for h in range(3)}
+        target = {(l, h): mat(h == 3) for l in range(2) for h in range(4)}
+        samples.append(TraceSample(length=n, draft=draft, target=target))
+        for key, m in draft.items():
+            mats[f"s{si}_d{key[0]}_{key[1]}"] = m
+        for key, m in target.items():
+            mats[f"s{si}_t{key[0]}_{key[1]}"] = m
+    ts = TraceSet(draft_config=dcfg, target_config=tcfg, samples=samples)
+    res = {}
+    for k in (1, 3, 8):
+        mp = headmap.find_head_mapping(ts, k)
+        res[str(k)] = [[tl, th, mp.entries[(tl, th)][0][0], mp.entries[(tl, th)][0][1], int(mp.entries[(tl, th)][1])]
+                       for tl in range(2) for th in range(4)]
+    np.savez_compressed(OUT / "headmap.npz", result=json.dumps(res), lengths=np.asarray([23, 40]), **mats)
 
 
 if __name__ == "__main__":
