@@ -904,7 +904,6 @@ int launch_verify(DecodeParams& p, cudaStream_t st) {
     cfg.numAttrs = 1;
     STS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, merge_pieces_kernel<D, MODE>, p));
     count_launch();
-    STS_LAUNCH_CHECK();
   }
   return STS_OK;
 }
