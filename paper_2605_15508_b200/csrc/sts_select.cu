@@ -544,6 +544,249 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(SelectParams p) 
 }
 
 // ---------------------------------------------------------------------------
+// Select v2 (token mode, rows <= 48K): 16-bit key prefixes in shared memory.
+// Only the top 16 bits of each order key (sign, exponent, 7 mantissa bits)
+// are kept on chip (2 bytes per position: three rows fit on one SM, 256 rows
+// run in one wave on 148 SMs).  Two 8-bit radix passes find the 16-bit
+// threshold prefix (the first one fused into row formation); the low 16 bits
+// are resolved only for the positions in the threshold bin, recomputing their
+// full keys from the score rows (typically a few hundred per row).  Emit walks
+// positions in order: prefix above -> selected, prefix equal -> full-key
+// compare + tie rank (ties to the lowest index), extras always.
+// ---------------------------------------------------------------------------
+constexpr int SV2_THREADS = 512;
+constexpr int SV2_WARPS = SV2_THREADS / 32;
+constexpr int SV2_MAX = 49152;
+
+struct SV2Shared {
+  uint32_t hist[256];
+  int warp_tot[SV2_WARPS];
+  int bcast[4];
+};
+
+__device__ __forceinline__ int sv2_scan(int v, int* warp_tot, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int x = lane < SV2_WARPS ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    if (lane < SV2_WARPS) warp_tot[lane] = x;
+  }
+  __syncthreads();
+  const int before = warp > 0 ? warp_tot[warp - 1] : 0;
+  total = warp_tot[SV2_WARPS - 1];
+  __syncthreads();
+  return before + incl - v;
+}
+
+// warp-aggregated shared-memory histogram increment (hot bins: one atomic per
+// distinct bin per warp instead of one per lane)
+__device__ __forceinline__ void sv2_hist_add(uint32_t* hist, int bin, bool active) {
+  const unsigned mask = __ballot_sync(0xffffffffu, active);
+  if (!active) return;
+  const unsigned peers = __match_any_sync(mask, bin);
+  const int leader = __ffs(peers) - 1;
+  if ((int)(threadIdx.x & 31) == leader) atomicAdd(&hist[bin], (unsigned)__popc(peers));
+}
+
+// pick the digit whose descending cumulative count reaches krem (256 bins)
+__device__ __forceinline__ void sv2_pick(SV2Shared& sh, int krem, int& digit, int& above, int& inbin) {
+  const int tid = threadIdx.x;
+  const int v = tid < 256 ? (int)sh.hist[255 - tid] : 0;
+  int tot;
+  const int excl = sv2_scan(v, sh.warp_tot, tot);
+  if (tid < 256 && v > 0 && excl < krem && krem <= excl + v) {
+    sh.bcast[0] = 255 - tid;
+    sh.bcast[1] = excl;
+    sh.bcast[2] = v;
+  }
+  __syncthreads();
+  digit = sh.bcast[0];
+  above = sh.bcast[1];
+  inbin = sh.bcast[2];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(SV2_THREADS) select_v2_kernel(SelectParams p) {
+  __shared__ SV2Shared sh;
+  extern __shared__ __align__(16) uint16_t k16[];  // [n] key prefixes
+  const int tid = threadIdx.x;
+  const int64_t r = blockIdx.x;
+  const int n = p.row_len ? p.row_len[r] : p.n_common;
+  int32_t* out = p.idx_out + r * p.idx_ld;
+  int32_t srcs[8];
+  if (p.row_src) {
+    for (int q = 0; q < p.nsrc && q < 8; ++q) srcs[q] = p.row_src[r * p.nsrc + q];
+  } else {
+    srcs[0] = (int32_t)r;
+  }
+  int b;
+  if (p.budget_is_fraction) {
+    const double cc = ceil(p.budget * (double)n);
+    b = cc < 1.0 ? 1 : (int)cc;
+  } else {
+    b = (int)p.budget;
+  }
+  const bool cur = (p.flags & STS_SEL_CURRENT) != 0, sink = (p.flags & STS_SEL_SINK) != 0;
+  const int lo_extra = p.recent_window > 0 ? n - p.recent_window : n;
+  auto extra = [&](int j) { return j >= lo_extra || (sink && j == 0) || (cur && j == n - 1); };
+  auto full_key = [&](int j) { return f32_key(row_value(p, srcs, j)); };
+
+  int count = 0;
+  if (n <= 0) {
+  } else if (b >= n) {
+    for (int j = tid; j < n; j += SV2_THREADS) write_idx(p, out, j, j);
+    count = n;
+  } else {
+    // 1. formation: 16-bit prefixes + histogram of their top 8 bits
+    if (tid < 256) sh.hist[tid] = 0;
+    __syncthreads();
+    const bool vec = (p.ld % 4) == 0 && (reinterpret_cast<uintptr_t>(p.scores) % 16) == 0;
+    const int n4 = vec ? n / 4 : 0;
+    for (int v0 = 0; v0 < n4; v0 += SV2_THREADS) {
+      const int v = v0 + tid;
+      const bool ok = v < n4;
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (ok) {
+        a = *reinterpret_cast<const float4*>(p.scores + (int64_t)srcs[0] * p.ld + 4 * v);
+        for (int q = 1; q < p.nsrc; ++q) {
+          const float4 x = *reinterpret_cast<const float4*>(p.scores + (int64_t)srcs[q] * p.ld + 4 * v);
+          a.x = __fadd_rn(a.x, x.x); a.y = __fadd_rn(a.y, x.y); a.z = __fadd_rn(a.z, x.z); a.w = __fadd_rn(a.w, x.w);
+        }
+      }
+      const uint32_t k0 = f32_key(a.x) >> 16, k1 = f32_key(a.y) >> 16, k2 = f32_key(a.z) >> 16, k3 = f32_key(a.w) >> 16;
+      if (ok) {
+        uint2 packed;
+        packed.x = k0 | (k1 << 16);
+        packed.y = k2 | (k3 << 16);
+        *reinterpret_cast<uint2*>(k16 + 4 * v) = packed;
+      }
+      sv2_hist_add(sh.hist, (int)(k0 >> 8), ok);
+      sv2_hist_add(sh.hist, (int)(k1 >> 8), ok);
+      sv2_hist_add(sh.hist, (int)(k2 >> 8), ok);
+      sv2_hist_add(sh.hist, (int)(k3 >> 8), ok);
+    }
+    for (int j0 = 4 * n4; j0 < n; j0 += SV2_THREADS) {
+      const int j = j0 + tid;
+      const bool ok = j < n;
+      const uint32_t k = ok ? full_key(j) >> 16 : 0u;
+      if (ok) k16[j] = (uint16_t)k;
+      sv2_hist_add(sh.hist, (int)(k >> 8), ok);
+    }
+    __syncthreads();
+    int d1, above, inbin;
+    sv2_pick(sh, b, d1, above, inbin);
+    int krem = b - above;
+    // 2. second 8 bits of the prefix
+    uint32_t t16 = (uint32_t)d1 << 8;
+    uint32_t pm16 = 0xff00u;
+    if (krem != inbin) {
+      if (tid < 256) sh.hist[tid] = 0;
+      __syncthreads();
+      for (int j0 = 0; j0 < n; j0 += SV2_THREADS) {
+        const int j = j0 + tid;
+        const uint32_t k = j < n ? k16[j] : 0u;
+        const bool m = j < n && (k >> 8) == (uint32_t)d1;
+        sv2_hist_add(sh.hist, (int)(k & 0xffu), m);
+      }
+      __syncthreads();
+      int d2;
+      sv2_pick(sh, krem, d2, above, inbin);
+      krem -= above;
+      t16 |= (uint32_t)d2;
+      pm16 = 0xffffu;
+    }
+    // 3. low 16 bits among the positions whose prefix equals t16 (full keys
+    //    recomputed from the score rows)
+    uint32_t T = t16 << 16, pmask = pm16 << 16;
+    bool all_bin = krem == inbin;
+    for (int shift = 8; shift >= 0 && !all_bin && pm16 == 0xffffu; shift -= 8) {
+      if (tid < 256) sh.hist[tid] = 0;
+      __syncthreads();
+      for (int j0 = 0; j0 < n; j0 += SV2_THREADS) {
+        const int j = j0 + tid;
+        const bool cand = j < n && k16[j] == t16;
+        uint32_t key = 0;
+        if (cand) key = full_key(j);
+        const bool m = cand && (key & pmask) == T;
+        sv2_hist_add(sh.hist, (int)((key >> shift) & 0xffu), m);
+      }
+      __syncthreads();
+      int d;
+      sv2_pick(sh, krem, d, above, inbin);
+      krem -= above;
+      T |= (uint32_t)d << shift;
+      pmask |= 0xffu << shift;
+      all_bin = krem == inbin;
+    }
+    // here: keys with (key & pmask) > T (prefix-wise) are above; == T are the
+    // threshold ties of which the first krem (index order) are taken
+    // (all of them when all_bin)
+    // 4. emit in index order
+    int run_sel = 0, run_tie = 0;
+    for (int base = 0; base < n; base += 4 * SV2_THREADS) {
+      const int j0 = base + 4 * tid;
+      uint32_t sel = 0, eq = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = j0 + q;
+        if (j >= n) break;
+        const uint32_t k = k16[j];
+        if ((k & pm16) > (t16 & pm16)) {
+          sel |= 1u << q;
+        } else if ((k & pm16) == (t16 & pm16)) {
+          if (pm16 != 0xffffu || pmask == 0xffff0000u) {
+            eq |= 1u << q;  // resolved at the prefix level
+          } else {
+            const uint32_t mk = full_key(j) & pmask;
+            if (mk > T) sel |= 1u << q;
+            else if (mk == T) eq |= 1u << q;
+          }
+        }
+      }
+      int tie_tot = 0;
+      if (all_bin) {
+        sel |= eq;
+      } else {
+        int rank = run_tie + sv2_scan(__popc(eq), sh.warp_tot, tie_tot);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if ((eq >> q) & 1u) {
+            if (rank < krem) sel |= 1u << q;
+            ++rank;
+          }
+        run_tie += tie_tot;
+      }
+      if (j0 + 3 >= lo_extra || (sink && j0 == 0) || (cur && j0 + 3 >= n - 1)) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (j0 + q < n && extra(j0 + q)) sel |= 1u << q;
+      }
+      int sel_tot;
+      int pos = run_sel + sv2_scan(__popc(sel), sh.warp_tot, sel_tot);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if ((sel >> q) & 1u) write_idx(p, out, pos++, j0 + q);
+      run_sel += sel_tot;
+    }
+    count = run_sel;
+  }
+  for (int t = tid; t < p.tail_len; t += SV2_THREADS) write_idx(p, out, count + t, max(n, 0) + t);
+  if (tid == 0) p.cnt_out[r] = count + p.tail_len;
+}
+
+// ---------------------------------------------------------------------------
 // Cluster select (token mode): a thread-block cluster of C CTAs per row, CTA c
 // holding the keys of positions [c*n/C, (c+1)*n/C) in its shared memory.  The
 // radix passes exchange 256-bin histograms through distributed shared memory
@@ -891,6 +1134,22 @@ extern "C" int sts_select_topk(const float* scores_dev, int64_t ld, const int32_
   p.status = status_dev;
   p.buf_bytes = key_buf_bytes(max_len, page_size);
 
+  // experimental (STS_SELECT_V2=1): token-mode rows <= 48K through the 16-bit
+  // prefix select.  Parity-tested, but measured slower at c2 (158 vs 63 us:
+  // the threshold-bin candidates' full keys are recomputed with scattered,
+  // latency-bound loads in three passes), so off by default.
+  {
+    static const int env = getenv("STS_SELECT_V2") ? atoi(getenv("STS_SELECT_V2")) : 0;
+    if (env == 1 && page_size == 1 && max_len > 0 && max_len <= SV2_MAX && rows <= ((int64_t)1 << 31) - 1) {
+      const size_t smem2 = (((size_t)max_len * 2 + 15) & ~size_t(15));
+      static const cudaError_t a2 =
+          cudaFuncSetAttribute(select_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SV2_MAX * 2);
+      STS_CUDA_CHECK(a2);
+      select_v2_kernel<<<(unsigned)rows, SV2_THREADS, smem2, static_cast<cudaStream_t>(stream)>>>(p);
+      STS_LAUNCH_CHECK();
+      return STS_OK;
+    }
+  }
   // experimental (STS_SELECT_CLUSTER=1): token-mode rows that fit C x 16K keys
   // through one thread-block cluster per row.  Measured slower than the
   // single-CTA kernel at c2 (150 vs 63 us: 8-bit digits without candidate

@@ -199,6 +199,24 @@ def test_cluster_select_variant(cuda_ok):
     root = Path(__file__).resolve().parent.parent
     env = dict(os.environ, STS_SELECT_CLUSTER="1")
     r = subprocess.run([sys.executable, "-m", "pytest", str(root / "tests" / "test_gpu_select.py"), "-q", "-x",
-                        "-p", "no:cacheprovider", "-k", "not cluster_select_variant"],
+                        "-p", "no:cacheprovider", "-k", "not variant"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_prefix16_select_variant(cuda_ok):
+    """The selection parity suite again through the experimental 16-bit prefix
+    select (STS_SELECT_V2=1: token-mode rows <= 48K keep 2-byte key prefixes on
+    chip, full keys recomputed for the threshold bin), in a subprocess because
+    the library reads the knob once."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    env = dict(os.environ, STS_SELECT_V2="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", str(root / "tests" / "test_gpu_select.py"), "-q", "-x",
+                        "-p", "no:cacheprovider", "-k", "not variant"],
                        env=env, cwd=root, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
