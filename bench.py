@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="collective backend for N > 1 (gloo + --one-gpu: functional check on a single GPU)")
     ap.add_argument("--one-gpu", action="store_true", help="map every rank to cuda:0 (functional checks only)")
+    ap.add_argument("--merge", default="gather", choices=["gather", "p2p"],
+                    help="sharded path: NCCL all-gather + merge, or one peer-memory merge kernel over symmetric memory")
     ap.add_argument("--context", type=int, default=None, help="override the config's context length")
     ap.add_argument("--batch", type=int, default=None, help="override the config's batch")
     return ap.parse_args()
@@ -487,6 +489,8 @@ def run_sharded(args, world, rank, local):
     cfg = SparsityConfig(budget=budget, page_size=args.page_size)
     table = random_mapping_table(shape, seed=5)
     step = sharded.ShardedVerifyStep(shape, cfg, table, rank, world, device=dev, align=max(64, args.page_size))
+    if args.merge == "p2p" and world > 1:
+        step.enable_p2p()
     dq, dk, tq, tk, tv = sharded.local_synthetic_inputs(shape, step.bounds, rank, dev, seed=0)
     dqv, dkv, q, k, v = step.local_views(dq, dk, tq, tk, tv, full=False)
     flush = L2Flush(dev, args.flush)
@@ -576,7 +580,8 @@ def run_sharded(args, world, rank, local):
                    "context": shape.context, "batch": shape.batch, "gamma": shape.gamma, "mode": "S",
                    "page_size": args.page_size, "shard_positions": step.n_loc,
                    "keys_per_kv_head": round(keys_per_unit, 1), "l2": flush.describe(),
-                   "parallelism": f"sequence-sharded x{world} ({args.dist_backend} histogram allreduce + LSE merge)"},
+                   "parallelism": f"sequence-sharded x{world} ({args.dist_backend} histogram allreduce + "
+                                  f"{'peer-memory' if args.merge == 'p2p' and world > 1 else 'all-gather'} LSE merge)"},
         "dense_us": round(den, 2), "speedup_vs_dense": round(den / att, 3),
         "mask_build_us": {"draft_capture": round(cap, 2), "select": round(sel, 2)},
         "sts_step_us": round(cap + sel + att, 2), "step_speedup_vs_dense": round(den / (cap + sel + att), 3),

@@ -193,6 +193,15 @@ STS_API int sts_lse_merge(const float* o_part_dev, const float* lse_part_dev, in
                   int64_t rows, int32_t d, int32_t out_dtype, void* out_dev,
                   float* lse_out_dev, void* stream);
 
+/* sts_lse_merge_ptrs — the same merge with part q read at part_ptrs_dev[q]
+ * (a device array of nparts float pointers, e.g. every rank's symmetric-memory
+ * buffer mapped over NVLink): O_q at ptr + o_offset ([rows][d] floats), LSE_q
+ * at ptr + l_offset ([rows]).  One kernel = all-gather + merge over peer
+ * memory; results identical to sts_lse_merge on the same parts. */
+STS_API int sts_lse_merge_ptrs(const void* part_ptrs_dev, int32_t nparts, int64_t rows, int32_t d,
+                               int64_t o_offset, int64_t l_offset, int32_t out_dtype, void* out_dev,
+                               float* lse_out_dev, void* stream);
+
 /* ------------------------------------------------------------------------
  * sts_row_union — mode R (reference-exact per-row masks) under GQA: build,
  * for each unit, the sorted union of the M per-row index lists together with

@@ -92,6 +92,39 @@ __global__ void __launch_bounds__(UNION_THREADS) union_compact_kernel(
   if (threadIdx.x == 0) cnt_out[u] = run < out_ld ? run : (int)out_ld;
 }
 
+// Same merge, parts addressed through a device array of pointers — one per
+// rank's symmetric-memory buffer (peer addresses over NVLink): a one-shot
+// all-gather + merge with no staging copy.  Arithmetic order = lse_merge_kernel.
+__global__ void __launch_bounds__(MERGE_WARPS * 32) lse_merge_ptrs_kernel(
+    const float* const* __restrict__ parts, int nparts, int64_t rows, int d, int64_t o_off, int64_t l_off,
+    int out_dtype, void* out, float* lse_out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * MERGE_WARPS + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  float m = -INFINITY;
+  for (int q = 0; q < nparts; ++q) m = fmaxf(m, __ldcg(parts[q] + l_off + row));
+  float tot = 0.f;
+  if (m != -INFINITY)
+    for (int q = 0; q < nparts; ++q) tot += expf(__ldcg(parts[q] + l_off + row) - m);
+  if (lane == 0 && lse_out) lse_out[row] = tot > 0.f ? m + logf(tot) : -INFINITY;
+  if (!out) return;
+  for (int e = lane; e < d; e += 32) {
+    float acc = 0.f;
+    if (tot > 0.f) {
+      for (int q = 0; q < nparts; ++q) {
+        const float l = __ldcg(parts[q] + l_off + row);
+        if (l == -INFINITY) continue;
+        acc += expf(l - m) * __ldcg(parts[q] + o_off + row * d + e);
+      }
+      acc /= tot;
+    }
+    if (out_dtype == STS_DTYPE_BF16)
+      static_cast<__nv_bfloat16*>(out)[row * d + e] = __float2bfloat16_rn(acc);
+    else
+      static_cast<float*>(out)[row * d + e] = acc;
+  }
+}
+
 }  // namespace
 
 int lse_merge_launch(const float* o_part, const float* lse_part, int nparts, int64_t rows, int d,
@@ -214,6 +247,21 @@ extern "C" int sts_bitset_overlap(const uint32_t* a_dev, int32_t Ta, const uint3
   dim3 grid((unsigned)Tb, (unsigned)Ta);
   sts::bitset_overlap_kernel<<<grid, sts::OVL_THREADS, 0, static_cast<cudaStream_t>(stream)>>>(a_dev, b_dev, W, Tb,
                                                                                                scores_dev);
+  STS_LAUNCH_CHECK();
+  return STS_OK;
+}
+
+extern "C" int sts_lse_merge_ptrs(const void* part_ptrs_dev, int32_t nparts, int64_t rows, int32_t d,
+                                  int64_t o_offset, int64_t l_offset, int32_t out_dtype, void* out_dev,
+                                  float* lse_out_dev, void* stream) {
+  STS_REQUIRE(nparts >= 1 && rows >= 0 && d >= 1, STS_ERR_CONTRACT, "bad merge shape");
+  STS_REQUIRE(out_dtype == STS_DTYPE_F32 || out_dtype == STS_DTYPE_BF16, STS_ERR_CONTRACT, "bad out dtype");
+  if (rows == 0) return STS_OK;
+  STS_REQUIRE(part_ptrs_dev, STS_ERR_CONTRACT, "null part pointer array");
+  const int64_t blocks = (rows + MERGE_WARPS - 1) / MERGE_WARPS;
+  lse_merge_ptrs_kernel<<<(unsigned)blocks, MERGE_WARPS * 32, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const float* const*>(part_ptrs_dev), nparts, rows, d, o_offset, l_offset, out_dtype, out_dev,
+      lse_out_dev);
   STS_LAUNCH_CHECK();
   return STS_OK;
 }

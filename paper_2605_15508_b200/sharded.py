@@ -43,6 +43,7 @@ from .verify import VerifyShape
 
 ALL_REDUCE_SUM = "all_reduce_sum"
 ALL_GATHER = "all_gather"
+BARRIER = "barrier"  # device-side barrier over the ranks' symmetric-memory handle (p2p merge)
 
 
 def shard_bounds(n: int, nranks: int, align: int = 1):
@@ -69,6 +70,8 @@ def run(protocol, group=None):
             kind = req[0]
             if kind == ALL_REDUCE_SUM:
                 dist.all_reduce(req[1], op=dist.ReduceOp.SUM, group=group)
+            elif kind == BARRIER:
+                req[1].barrier(channel=0)
             elif kind == ALL_GATHER:
                 src, dst = req[1], req[2]
                 if dist.get_backend(group) == "nccl":
@@ -92,7 +95,7 @@ def run_single(protocol):
         while True:
             if req[0] == ALL_GATHER:
                 req[2].view(-1).copy_(req[1].view(-1))
-            req = protocol.send(None)
+            req = protocol.send(None)  # (all-reduce over one rank and barriers are no-ops)
     except StopIteration as stop:
         result = stop.value
     return result
@@ -120,6 +123,8 @@ def run_lockstep(protocols):
             stacked = torch.stack([r[1] for r in reqs]).view(-1)
             for r in reqs:
                 r[2].view(-1).copy_(stacked)
+        elif kind == BARRIER:
+            pass  # virtual ranks share one stream: already ordered
         else:  # pragma: no cover
             raise RuntimeError(f"unknown collective {kind!r}")
         done = 0
@@ -272,7 +277,43 @@ class ShardedVerifyStep:
             recent_window=cfg.recent_window, tail_len=s.rows, n_kv_local=self.n_loc, idx=self.idx, cnt=self.cnt,
             status=self.status, stream=stream)
 
+    # -- p2p merge: partials in symmetric memory, merged over peer pointers ----
+    def enable_p2p(self, group=None):
+        """Put this rank's partial (O, LSE) in torch symmetric memory and merge
+        by reading every rank's buffer over NVLink in one kernel
+        (sts_lse_merge_ptrs) after a device-side barrier, instead of an NCCL
+        all-gather + local merge.  Needs torch.distributed initialised."""
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+
+        grp = group or dist.group.WORLD
+        try:
+            symm.enable_symm_mem_for_group(grp.group_name)
+        except Exception:  # pragma: no cover - already enabled / not needed
+            pass
+        U, M, d = self.out.shape
+        buf = symm.empty(U * M * d + U * M, dtype=torch.float32, device=self.device)
+        hdl = symm.rendezvous(buf, grp)
+        self._use_part_buffer(buf, hdl.buffer_ptrs_dev, hdl)
+
+    def _use_part_buffer(self, buf, ptrs_dev, hdl=None):
+        U, M, d = self.out.shape
+        self.part_buf = buf
+        self.o_part = buf[: U * M * d].view(U, M, d)
+        self.l_part = buf[U * M * d:].view(U, M)
+        self.part_ptrs_dev = ptrs_dev  # int (device address) or a device int64 tensor of the P pointers
+        self.p2p_handle = hdl
+        self.merge_mode = "p2p"
+
     def _merge(self, stream=None):
+        if getattr(self, "merge_mode", "gather") == "p2p":
+            U, M, d = self.out.shape
+            ptrs = self.part_ptrs_dev if isinstance(self.part_ptrs_dev, int) else self.part_ptrs_dev.data_ptr()
+            yield (BARRIER, self.p2p_handle)  # every rank's partial is written and visible
+            call("sts_lse_merge_ptrs", ptrs, self.nranks, U * M, d, 0, U * M * d, _lib.STS_DTYPE_BF16,
+                 ptr(self.out), ptr(self.lse), stream_handle(stream))
+            yield (BARRIER, self.p2p_handle)  # nobody rewrites its partial while peers still read it
+            return
         yield (ALL_GATHER, self.o_part, self.o_all)
         yield (ALL_GATHER, self.l_part, self.l_all)
         U, M, d = self.out.shape
@@ -341,3 +382,16 @@ def local_synthetic_inputs(shape: VerifyShape, bounds, rank: int, device, dtype=
     dq = randn((s.batch, s.draft_layers, s.draft_q_heads, s.rows, s.draft_head_dim), seed + 3)
     dk = randn((s.batch, s.draft_layers, s.draft_kv_heads, n, s.draft_head_dim), seed + 4 + 1000 * rank)
     return dq, dk, tq, tk, tv
+
+
+def link_p2p_lockstep(steps):
+    """Single-process stand-in for ``enable_p2p`` (virtual ranks on one GPU):
+    each rank's partials go to its own buffer and the merge reads all of them
+    through a device pointer array — the same kernel and addressing as the
+    symmetric-memory path, without NVLink."""
+    U, M, d = steps[0].out.shape
+    bufs = [torch.empty(U * M * d + U * M, dtype=torch.float32, device=st.device) for st in steps]
+    ptrs = torch.tensor([b.data_ptr() for b in bufs], dtype=torch.int64, device=steps[0].device)
+    for st, b in zip(steps, bufs):
+        st._use_part_buffer(b, ptrs)
+    return bufs, ptrs

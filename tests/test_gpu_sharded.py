@@ -155,3 +155,31 @@ def test_sharded_verify_step_matches_oracle(cuda_ok):
     q1, k1, v1 = tq.reshape(s.target_units, -1, s.head_dim), tk.flatten(0, 2), tv.flatten(0, 2)
     ref, _ = kernels.sparse_decode(q1, k1, v1, n_dense=s.n_kv, causal_base=s.context, rows_per_head=s.rows)
     np.testing.assert_allclose(dense[0][0].float().cpu().numpy(), ref.float().cpu().numpy(), rtol=2e-2, atol=2e-2)
+
+
+def test_p2p_merge_matches_gather_merge(cuda_ok):
+    """The peer-pointer merge (sts_lse_merge_ptrs: every rank's partial read
+    through a device array of pointers, as over NVLink symmetric memory) gives
+    the all-gather + merge result bit for bit (virtual ranks on one GPU)."""
+    import torch
+
+    from paper_2605_15508_b200 import SparsityConfig, sharded
+    from paper_2605_15508_b200.verify import VerifyShape, random_mapping_table, synthetic_inputs
+
+    s = VerifyShape(batch=1, context=2500, gamma=4, target_layers=2, target_q_heads=8, target_kv_heads=2,
+                    head_dim=128, draft_layers=2, draft_q_heads=8, draft_kv_heads=2, draft_head_dim=64)
+    cfg = SparsityConfig(budget=0.1)
+    table = random_mapping_table(s, seed=4)
+    dq, dk, tq, tk, tv = synthetic_inputs(s, "cuda", seed=9)
+    P = 3
+    outs = {}
+    for mode in ("gather", "p2p"):
+        steps = [sharded.ShardedVerifyStep(s, cfg, table, r, P, device="cuda") for r in range(P)]
+        if mode == "p2p":
+            keep = sharded.link_p2p_lockstep(steps)  # noqa: F841 (buffers stay alive)
+        views = [st.local_views(dq, dk, tq, tk, tv) for st in steps]
+        res = sharded.run_lockstep([st.step(*v) for st, v in zip(steps, views)])
+        torch.cuda.synchronize()
+        outs[mode] = [o.clone() for o, _ in res]
+    for a, b in zip(outs["gather"], outs["p2p"]):
+        assert torch.equal(a, b)
