@@ -33,6 +33,13 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "target attn us/verify step at 90% sparsity; speedup vs dense; HBM GB/s"
+MODEL_NAMES = {
+    "c1": "tiny draft 2L/4H -> target 4L/8H",
+    "c2": "Llama-3.2-1B draft -> Llama-3.1-8B target",
+    "c3": "Qwen2.5-0.5B draft -> Qwen2.5-7B target",
+    "c4": "Llama-3.2-1B draft -> Llama-3.1-8B target",
+    "c5": "Llama-3.2-1B draft -> Llama-3.1-70B target",
+}
 
 
 def parse():
@@ -54,6 +61,8 @@ def parse():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="collective backend for N > 1 (gloo + --one-gpu: functional check on a single GPU)")
     ap.add_argument("--one-gpu", action="store_true", help="map every rank to cuda:0 (functional checks only)")
+    ap.add_argument("--head-groups", type=int, default=0,
+                    help="heads x sequence sharding: ranks per head group = gpus / head_groups (0: 2 for c5, else 1)")
     ap.add_argument("--merge", default="gather", choices=["gather", "p2p"],
                     help="sharded path: NCCL all-gather + merge, or one peer-memory merge kernel over symmetric memory")
     ap.add_argument("--context", type=int, default=None, help="override the config's context length")
@@ -261,7 +270,7 @@ def main():
         args.config = "c2" if world == 1 else "c4"
     if args.impl == "reference":
         return run_reference(args)
-    if args.config == "c4" or world > 1:
+    if args.config in ("c4", "c5") or world > 1:
         return run_sharded(args, world, rank, local)
 
     import numpy as np
@@ -488,10 +497,29 @@ def run_sharded(args, world, rank, local):
     budget = round(1.0 - args.sparsity, 10)
     cfg = SparsityConfig(budget=budget, page_size=args.page_size)
     table = random_mapping_table(shape, seed=5)
-    step = sharded.ShardedVerifyStep(shape, cfg, table, rank, world, device=dev, align=max(64, args.page_size))
+    # heads x sequence: head group g = rank // sp holds kv-heads [g*Hkv/hp, ...),
+    # the sp ranks of a group split the sequence and exchange among themselves
+    hp = args.head_groups or (2 if args.config == "c5" and world % 2 == 0 and world > 1 else 1)
+    if world % hp or shape.target_kv_heads % hp:
+        raise SystemExit(f"--head-groups {hp} must divide the GPU count {world} and the kv-heads")
+    sp = world // hp
+    g, srank = rank // sp, rank % sp
+    kv_bytes = (shape.batch * shape.target_layers * shape.target_kv_heads * shape.n_kv * shape.head_dim * 4
+                + shape.batch * shape.draft_layers * shape.draft_kv_heads * shape.n_kv * shape.draft_head_dim * 2)
+    if kv_bytes / world > 170e9:
+        raise SystemExit(f"{args.config} needs {kv_bytes / 1e9:.0f} GB of KV cache: run it on >= "
+                         f"{math.ceil(kv_bytes / 170e9)} GPUs (torchrun --nproc-per-node N bench.py --gpus N)")
+    group = None
+    if world > 1 and hp > 1:
+        groups = [dist.new_group(list(range(h * sp, (h + 1) * sp))) for h in range(hp)]
+        group = groups[g]
+        drive = lambda proto: sharded.run(proto, group=group)  # noqa: E731
+    step = sharded.ShardedVerifyStep(shape, cfg, table, srank, sp, device=dev, align=max(64, args.page_size),
+                                     head_groups=hp, head_group=g)
     if args.merge == "p2p" and world > 1:
-        step.enable_p2p()
-    dq, dk, tq, tk, tv = sharded.local_synthetic_inputs(shape, step.bounds, rank, dev, seed=0)
+        step.enable_p2p(group)
+    dq, dk, tq, tk, tv = sharded.local_synthetic_inputs(shape, step.bounds, srank, dev, seed=0, head_groups=hp,
+                                                       head_group=g)
     dqv, dkv, q, k, v = step.local_views(dq, dk, tq, tk, tv, full=False)
     flush = L2Flush(dev, args.flush)
     st = torch.cuda.current_stream()
@@ -574,13 +602,14 @@ def run_sharded(args, world, rank, local):
         "warmup": args.warmup, "ms_per_step": round(att / 1e3, 5), "higher_is_better": False,
         "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded N(0,1) bf16 Q/K/V per shard, random head mapping)",
-        "config": {"workload": f"{args.config}: Llama-3.1-8B target / Llama-3.2-1B draft shapes, {shape.context} "
-                               f"context, KV sharded by sequence over {world} GPU(s), batch {shape.batch}, gamma "
+        "config": {"workload": f"{args.config}: {MODEL_NAMES.get(args.config, 'synthetic')} shapes, {shape.context} "
+                               f"context, KV sharded over {world} GPU(s) ({hp} head groups x {sp} sequence shards), "
+                               f"batch {shape.batch}, gamma "
                                f"{shape.gamma}, sparsity {args.sparsity}, mode S, page_size {args.page_size}",
                    "context": shape.context, "batch": shape.batch, "gamma": shape.gamma, "mode": "S",
                    "page_size": args.page_size, "shard_positions": step.n_loc,
                    "keys_per_kv_head": round(keys_per_unit, 1), "l2": flush.describe(),
-                   "parallelism": f"sequence-sharded x{world} ({args.dist_backend} histogram allreduce + "
+                   "parallelism": f"{hp} head group(s) x sequence-sharded x{sp} ({args.dist_backend} histogram allreduce + "
                                   f"{'peer-memory' if args.merge == 'p2p' and world > 1 else 'all-gather'} LSE merge)"},
         "dense_us": round(den, 2), "speedup_vs_dense": round(den / att, 3),
         "mask_build_us": {"draft_capture": round(cap, 2), "select": round(sel, 2)},

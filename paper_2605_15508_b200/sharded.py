@@ -208,10 +208,21 @@ class ShardedVerifyStep:
     """
 
     def __init__(self, shape: VerifyShape, sparsity: SparsityConfig, mapping_table, rank: int, nranks: int,
-                 device=None, align: int | None = None):
+                 device=None, align: int | None = None, head_groups: int = 1, head_group: int = 0):
+        """``rank`` / ``nranks``: position in the SEQUENCE group (the ranks
+        whose collectives this step exchanges).  ``head_groups`` > 1 adds
+        heads parallelism (BASELINE config 5): this rank holds only target
+        kv-heads [head_group * Hkv / head_groups, ...) of every layer and batch
+        (their K/V and queries), while the draft capture is computed for all
+        draft heads (any of them can map onto this group's target heads)."""
         s = self.shape = shape
         self.cfg = sparsity
         self.rank, self.nranks = int(rank), int(nranks)
+        if s.target_kv_heads % head_groups:
+            raise ValueError("target kv-heads must divide evenly into head groups")
+        self.head_groups, self.head_group = int(head_groups), int(head_group)
+        self.hkv = s.target_kv_heads // head_groups
+        self.kv_lo = head_group * self.hkv
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.device = dev
         R, base = s.rows, s.context
@@ -232,7 +243,9 @@ class ShardedVerifyStep:
         self.n_cols = max(4, -(-self.n_loc // 4) * 4)
         src = (np.arange(s.batch)[:, None, None, None] * nd
                + table.reshape(1, s.target_layers, s.target_kv_heads, Gt))
-        self.row_src = torch.from_numpy(src.reshape(-1, Gt).astype(np.int32)).to(dev)
+        src = src[:, :, self.kv_lo : self.kv_lo + self.hkv]  # this head group's kv-heads
+        self.row_src = torch.from_numpy(np.ascontiguousarray(src).reshape(-1, Gt).astype(np.int32)).to(dev)
+        self.U = U = s.batch * s.target_layers * self.hkv  # target units held here
         # draft side
         self.ws_draft = Workspace(dev)
         GRd = s.draft_group * R
@@ -241,15 +254,14 @@ class ShardedVerifyStep:
         self.lse_global = torch.empty((s.draft_units * GRd,), dtype=torch.float32, device=dev)
         self.draft_rows = torch.zeros((s.batch * nd, self.n_cols), dtype=torch.float32, device=dev)
         # selection
-        self.selector = DistSelector(s.target_units, self.n_loc, ps, nranks, dev)
+        self.selector = DistSelector(U, self.n_loc, ps, nranks, dev)
         cap = min(self.n_loc, self.k_top * ps + int(sparsity.include_sink) + sparsity.recent_window + R)
         self.idx_ld = max(1, cap)
-        self.idx = torch.empty((s.target_units, self.idx_ld), dtype=torch.int32, device=dev)
-        self.cnt = torch.empty((s.target_units,), dtype=torch.int32, device=dev)
+        self.idx = torch.empty((U, self.idx_ld), dtype=torch.int32, device=dev)
+        self.cnt = torch.empty((U,), dtype=torch.int32, device=dev)
         # attention
         self.M = Gt * R
         self.ws_dec = Workspace(dev)
-        U = s.target_units
         self.o_part = torch.empty((U, self.M, s.head_dim), dtype=torch.float32, device=dev)
         self.l_part = torch.empty((U, self.M), dtype=torch.float32, device=dev)
         self.o_all = torch.empty((nranks, U, self.M, s.head_dim), dtype=torch.float32, device=dev)
@@ -349,7 +361,13 @@ class ShardedVerifyStep:
         already are the local shard."""
         s = self.shape
         sl = slice(self.lo, self.hi) if full else slice(0, self.n_loc)
-        q = tq.reshape(s.target_units, self.M, s.head_dim)
+        Gt = s.target_group
+        if tq.shape[2] == s.target_q_heads and self.head_groups > 1:  # full-head tensors: take this group
+            tq = tq[:, :, self.kv_lo * Gt : (self.kv_lo + self.hkv) * Gt]
+        if tk.shape[2] == s.target_kv_heads and self.head_groups > 1:
+            tk = tk[:, :, self.kv_lo : self.kv_lo + self.hkv]
+            tv = tv[:, :, self.kv_lo : self.kv_lo + self.hkv]
+        q = tq.reshape(self.U, self.M, s.head_dim)
         k = tk.flatten(0, 2)[:, sl]
         v = tv.flatten(0, 2)[:, sl]
         dqv = dq.reshape(s.draft_units, s.draft_group * s.rows, s.draft_head_dim)
@@ -357,7 +375,8 @@ class ShardedVerifyStep:
         return dqv, dkv, q, k, v
 
 
-def local_synthetic_inputs(shape: VerifyShape, bounds, rank: int, device, dtype=torch.bfloat16, seed: int = 0):
+def local_synthetic_inputs(shape: VerifyShape, bounds, rank: int, device, dtype=torch.bfloat16, seed: int = 0,
+                           head_groups: int = 1, head_group: int = 0):
     """This rank's shard of synthetic_inputs (verify.py): the same seeded
     values a single GPU would hold at positions [lo, hi), generated shard by
     shard so no rank ever materialises the full cache (1M-token contexts)."""
@@ -376,9 +395,12 @@ def local_synthetic_inputs(shape: VerifyShape, bounds, rank: int, device, dtype=
             flat[i : i + m] = torch.randn(m, generator=g, device=device, dtype=torch.float32).to(dtype)
         return t
 
-    tq = randn((s.batch, s.target_layers, s.target_q_heads, s.rows, s.head_dim), seed + 0)
-    tk = randn((s.batch, s.target_layers, s.target_kv_heads, n, s.head_dim), seed + 1 + 1000 * rank)
-    tv = randn((s.batch, s.target_layers, s.target_kv_heads, n, s.head_dim), seed + 2 + 1000 * rank)
+    hkv = s.target_kv_heads // head_groups
+    hq = hkv * s.target_group
+    hs = 100000 * head_group  # head groups draw independent values
+    tq = randn((s.batch, s.target_layers, hq, s.rows, s.head_dim), seed + 0 + hs)
+    tk = randn((s.batch, s.target_layers, hkv, n, s.head_dim), seed + 1 + 1000 * rank + hs)
+    tv = randn((s.batch, s.target_layers, hkv, n, s.head_dim), seed + 2 + 1000 * rank + hs)
     dq = randn((s.batch, s.draft_layers, s.draft_q_heads, s.rows, s.draft_head_dim), seed + 3)
     dk = randn((s.batch, s.draft_layers, s.draft_kv_heads, n, s.draft_head_dim), seed + 4 + 1000 * rank)
     return dq, dk, tq, tk, tv

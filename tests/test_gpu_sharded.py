@@ -183,3 +183,44 @@ def test_p2p_merge_matches_gather_merge(cuda_ok):
         outs[mode] = [o.clone() for o, _ in res]
     for a, b in zip(outs["gather"], outs["p2p"]):
         assert torch.equal(a, b)
+
+
+def test_heads_times_sequence_sharding(cuda_ok):
+    """BASELINE config 5's layout: 2 head groups x 2 sequence shards (4 virtual
+    ranks). Each head group runs its own sequence-sharded protocol over its
+    kv-heads; together they reproduce the single-GPU masks and attention."""
+    import torch
+
+    from paper_2605_15508_b200 import SparsityConfig, sharded
+    from paper_2605_15508_b200.verify import VerifyShape, random_mapping_table, synthetic_inputs
+
+    s = VerifyShape(batch=2, context=1800, gamma=4, target_layers=2, target_q_heads=8, target_kv_heads=4,
+                    head_dim=128, draft_layers=2, draft_q_heads=8, draft_kv_heads=2, draft_head_dim=64)
+    cfg = SparsityConfig(budget=0.1)
+    table = random_mapping_table(s, seed=6)
+    dq, dk, tq, tk, tv = synthetic_inputs(s, "cuda", seed=12)
+    hp, sp = 2, 2
+    qf = tq.reshape(s.batch, s.target_layers, s.target_kv_heads, -1, s.head_dim).float().cpu().numpy()
+    kf = tk.float().cpu().numpy()
+    vf = tv.float().cpu().numpy()
+    ocfg = O.OracleSparsityConfig(0.1, 1, False, False, 0)
+    for g in range(hp):
+        steps = [sharded.ShardedVerifyStep(s, cfg, table, r, sp, device="cuda", head_groups=hp, head_group=g)
+                 for r in range(sp)]
+        views = [st.local_views(dq, dk, tq, tk, tv) for st in steps]
+        outs = sharded.run_lockstep([st.step(*v) for st, v in zip(steps, views)])
+        torch.cuda.synchronize()
+        D = np.concatenate([st.draft_rows[:, : st.n_loc].cpu().numpy() for st in steps], axis=1)
+        src = steps[0].row_src.cpu().numpy()
+        out = outs[0][0].float().cpu().numpy()
+        hkv = s.target_kv_heads // hp
+        for u in range(steps[0].U):
+            b, rest = divmod(u, s.target_layers * hkv)
+            l, h = divmod(rest, hkv)
+            kvh = g * hkv + h
+            want_idx = O.mode_s_index_list(O.reduce_rows_fp32([D[j] for j in src[u]]), s.context, s.rows, ocfg)
+            got_idx = np.concatenate([st.lo + st.idx[u, : int(st.cnt[u])].cpu().numpy() for st in steps])
+            assert np.array_equal(got_idx, want_idx), (g, u)
+            want, _ = O.block_attention(qf[b, l, kvh], kf[b, l, kvh], vf[b, l, kvh], want_idx,
+                                        causal_base=s.context, rows_per_head=s.rows)
+            np.testing.assert_allclose(out[u], want, rtol=2e-2, atol=2e-2)
