@@ -32,8 +32,6 @@ constexpr int DD_BITS = 8;
 constexpr int DD_BINS = 1 << DD_BITS;
 constexpr int DIST_THREADS = 512;
 constexpr int DIST_CHUNK = 8192;      // keys per CTA in the key / histogram passes
-constexpr int EMIT_THREADS = 1024;
-constexpr int EMIT_WARPS = EMIT_THREADS / 32;
 
 struct DistState {
   uint64_t prefix;  // chosen digits so far (in key space)
@@ -60,6 +58,7 @@ struct DistParams {
   DistState* state;
   uint8_t* keys;  // [rows][nkeys_pad] of K
   int64_t keys_ld;
+  int vec4;       // score rows 16-byte aligned with ld % 4 == 0 (token keys load float4)
 };
 
 __device__ __forceinline__ int local_committed(const DistParams& p) {
@@ -146,6 +145,38 @@ __global__ void __launch_bounds__(DIST_THREADS) dist_keys_kernel(DistParams p, i
   load_srcs(p, r, srcs);
   K* keys = reinterpret_cast<K*>(p.keys + r * p.keys_ld * sizeof(K));
   const int j_end = min(nk, (int)(blockIdx.x + 1) * DIST_CHUNK);
+  if constexpr (sizeof(K) == 4) {
+    if (p.vec4) {
+      // 4 consecutive positions per thread: one 16-byte load per source row
+      // (rows are padded to a multiple of 4), sources summed in order
+      for (int j = blockIdx.x * DIST_CHUNK + 4 * threadIdx.x; j < j_end; j += 4 * DIST_THREADS) {
+        float4 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < p.nsrc) v[q] = *reinterpret_cast<const float4*>(p.scores + (int64_t)srcs[q] * p.ld + j);
+        float4 a = v[0];
+#pragma unroll
+        for (int q = 1; q < 8; ++q)
+          if (q < p.nsrc) {
+            a.x = __fadd_rn(a.x, v[q].x);
+            a.y = __fadd_rn(a.y, v[q].y);
+            a.z = __fadd_rn(a.z, v[q].z);
+            a.w = __fadd_rn(a.w, v[q].w);
+          }
+        const uint4 k4 = make_uint4(f32_key(a.x), f32_key(a.y), f32_key(a.z), f32_key(a.w));
+        *reinterpret_cast<uint4*>(keys + j) = k4;
+        atomicAdd(&sh[digit_of<K>(k4.x, 0)], 1u);
+        if (j + 1 < j_end) atomicAdd(&sh[digit_of<K>(k4.y, 0)], 1u);
+        if (j + 2 < j_end) atomicAdd(&sh[digit_of<K>(k4.z, 0)], 1u);
+        if (j + 3 < j_end) atomicAdd(&sh[digit_of<K>(k4.w, 0)], 1u);
+      }
+      __syncthreads();
+      int32_t* h = hist + r * DD_BINS;
+      for (int i = threadIdx.x; i < DD_BINS; i += DIST_THREADS)
+        if (sh[i]) atomicAdd(h + i, (int)sh[i]);
+      return;
+    }
+  }
   for (int j = blockIdx.x * DIST_CHUNK + threadIdx.x; j < j_end; j += DIST_THREADS) {
     K key;
     if constexpr (sizeof(K) == 4) {
@@ -178,9 +209,20 @@ __global__ void __launch_bounds__(DIST_THREADS) dist_hist_kernel(DistParams p, i
   const K* keys = reinterpret_cast<const K*>(p.keys + r * p.keys_ld * sizeof(K));
   const K pm = (K)st.pmask, pf = (K)st.prefix;
   const int j_end = min(nk, (int)(blockIdx.x + 1) * DIST_CHUNK);
-  for (int j = blockIdx.x * DIST_CHUNK + threadIdx.x; j < j_end; j += DIST_THREADS) {
-    const K key = keys[j];
-    if ((key & pm) == pf) atomicAdd(&sh[digit_of<K>(key, round)], 1u);
+  if constexpr (sizeof(K) == 4) {
+    // keys rows are padded to a multiple of 4 and 16-byte aligned
+    for (int j = blockIdx.x * DIST_CHUNK + 4 * threadIdx.x; j < j_end; j += 4 * DIST_THREADS) {
+      const uint4 k4 = *reinterpret_cast<const uint4*>(keys + j);
+      const K kk[4] = {k4.x, k4.y, k4.z, k4.w};
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (j + q < j_end && (kk[q] & pm) == pf) atomicAdd(&sh[digit_of<K>(kk[q], round)], 1u);
+    }
+  } else {
+    for (int j = blockIdx.x * DIST_CHUNK + threadIdx.x; j < j_end; j += DIST_THREADS) {
+      const K key = keys[j];
+      if ((key & pm) == pf) atomicAdd(&sh[digit_of<K>(key, round)], 1u);
+    }
   }
   __syncthreads();
   int32_t* h = hist + r * DD_BINS;
@@ -240,32 +282,6 @@ __global__ void dist_advance_kernel(DistParams p, int round, const int32_t* hist
   p.state[r] = st;
 }
 
-__device__ __forceinline__ int emit_block_scan(int v, int* warp_tot, int& total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int incl = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += t;
-  }
-  if (lane == 31) warp_tot[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    int x = warp_tot[lane];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += t;
-    }
-    warp_tot[lane] = x;
-  }
-  __syncthreads();
-  const int before = warp > 0 ? warp_tot[warp - 1] : 0;
-  total = warp_tot[EMIT_WARPS - 1];
-  __syncthreads();
-  return before + incl - v;
-}
-
 struct EmitParams {
   int rank;
   int nranks;
@@ -278,130 +294,337 @@ struct EmitParams {
   int64_t idx_ld;
   int32_t* cnt_out;
   int32_t* status;
-  uint32_t* page_bits;      // [rows][page_bits_ld] scratch (page mode)
-  int64_t page_bits_ld;
+  uint32_t* bits;           // [rows][bits_ld] selected-key bitmap (tokens, or pages)
+  int64_t bits_ld;
+  int32_t* key_cnt;         // [rows][key_chunks] threshold ties per key chunk
+  int32_t* tok_cnt;         // [rows][tok_chunks] selected tokens per token chunk
+  int key_chunks;
+  int tok_chunks;
 };
 
-// one CTA per row: ascending local offsets of the selected positions.
-// Phase 1 decides the local keys (tokens, or pages) in index order: above the
-// threshold, or a threshold tie whose global tie rank (ties on lower ranks +
-// local rank) is below the remaining k.  Token mode writes indices directly;
-// page mode records a page bitmap and phase 2 expands it to tokens.  Extras
-// (sink, recent window, current — global positions) and the in-block tail
-// are added in the token pass.
-template <typename K>
-__global__ void __launch_bounds__(EMIT_THREADS) dist_emit_kernel(DistParams p, EmitParams e) {
-  __shared__ int warp_tot[EMIT_WARPS];
-  const int64_t r = blockIdx.x;
-  const DistState st = p.state[r];
-  const int nc = local_committed(p);
-  const int nk = local_keys(p);
-  const int ps = p.page_size;
-  const K* keys = reinterpret_cast<const K*>(p.keys + r * p.keys_ld * sizeof(K));
-  int32_t* out = e.idx_out + r * e.idx_ld;
-  uint32_t* pbits = e.page_bits ? e.page_bits + r * e.page_bits_ld : nullptr;
+// The emit is split over (chunk, row) CTAs of EMIT_CHUNK keys / tokens:
+//   ties   count the threshold ties of each key chunk
+//   bits   selected-key bitmap: keys above the threshold, plus the ties whose
+//          global rank (ties on lower ranks + earlier chunks + in-chunk rank)
+//          is below the remaining k
+//   count  selected tokens per token chunk (bitmap of the token's key, or an
+//          extra: sink / recent window / current)
+//   emit   ascending local offsets at the chunk's prefix; chunk 0 adds the
+//          in-block tail and the row count
+// Each warp owns 1024 consecutive keys as 32 ballot words (lane w keeps word w).
+constexpr int EMIT_THREADS = 512;
+constexpr int EMIT_WARPS = EMIT_THREADS / 32;
+constexpr int EMIT_CHUNK = EMIT_WARPS * 1024;
+
+struct EmitRow {
+  int need;      // ties this rank takes
+  bool all_ties; // every local tie is taken
+};
+
+__device__ __forceinline__ EmitRow emit_row(const DistState& st, const EmitParams& e, int64_t r, int64_t rows) {
   int before = 0;
-  for (int q = 0; q < e.rank; ++q) before += e.ties_all[(int64_t)q * p.rows + r];
-  int need = st.krem - before;
-  need = need < 0 ? 0 : need;
-  const bool all_ties = need >= st.ties_local;
-  const int lo_extra = e.recent_window > 0 ? p.n_global - e.recent_window : p.n_global;
-  const bool cur = (e.flags & STS_SEL_CURRENT) != 0, sink = (e.flags & STS_SEL_SINK) != 0;
-  const K pm = (K)st.pmask, pf = (K)st.prefix;
-  const int lane = threadIdx.x & 31;
+  for (int q = 0; q < e.rank; ++q) before += e.ties_all[(int64_t)q * rows + r];
+  EmitRow er;
+  er.need = max(st.krem - before, 0);
+  er.all_ties = er.need >= st.ties_local;
+  return er;
+}
 
-  auto is_extra = [&](int j) {
-    const int g = p.lo + j;
-    return g >= lo_extra || (sink && g == 0) || (cur && g == p.n_global - 1);
-  };
-
-  int run_sel = 0, run_tie = 0;
-  for (int base = 0; base < nk; base += 4 * EMIT_THREADS) {
-    const int j0 = base + 4 * threadIdx.x;
-    uint32_t sel = 0, eq = 0;
+// exclusive prefix of counts[0 .. c) (one row's chunk counts), block-wide
+__device__ __forceinline__ int chunk_prefix(const int32_t* counts, int c, int* red) {
+  int s = 0;
+  for (int i = threadIdx.x; i < c; i += EMIT_THREADS) s += counts[i];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int j = j0 + q;
-      if (j >= nk) break;
-      if (st.dense) {
-        sel |= 1u << q;
-        continue;
-      }
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  int t = 0;
+#pragma unroll
+  for (int w = 0; w < EMIT_WARPS; ++w) t += red[w];
+  __syncthreads();
+  return t;
+}
+
+// exclusive scan of one value per warp (lane 0's), block-wide
+__device__ __forceinline__ int warp_offsets(int v, int* red, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  int before = 0;
+  total = 0;
+#pragma unroll
+  for (int w = 0; w < EMIT_WARPS; ++w) {
+    const int x = red[w];
+    before += w < warp ? x : 0;
+    total += x;
+  }
+  __syncthreads();
+  return before;
+}
+
+__device__ __forceinline__ int lane_excl_scan(int v, int& warp_total) {
+  const int lane = threadIdx.x & 31;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  warp_total = __shfl_sync(0xffffffffu, incl, 31);
+  return incl - v;
+}
+
+// gt / eq ballot words of this warp's 1024 keys; lane w returns word w
+template <typename K>
+__device__ __forceinline__ void key_words(const K* keys, int nk, int64_t j0, K pm, K pf, uint32_t& gt, uint32_t& eq) {
+  const int lane = threadIdx.x & 31;
+  gt = eq = 0;
+#pragma unroll 8
+  for (int w = 0; w < 32; ++w) {
+    const int64_t j = j0 + 32 * w + lane;
+    bool g = false, q = false;
+    if (j < nk) {
       const K mk = keys[j] & pm;
-      sel |= mk > pf ? (1u << q) : 0u;
-      eq |= mk == pf ? (1u << q) : 0u;
+      g = mk > pf;
+      q = mk == pf;
     }
-    if (all_ties) {
+    const uint32_t bg = __ballot_sync(0xffffffffu, g), bq = __ballot_sync(0xffffffffu, q);
+    if (lane == w) {
+      gt = bg;
+      eq = bq;
+    }
+  }
+}
+
+// 32-bit keys: 16-byte loads, 4 keys per lane per 128-key block; the 8 lanes
+// of a block quarter OR their nibbles into one word, then lane w takes word w
+__device__ __forceinline__ void key_words(const uint32_t* keys, int nk, int64_t j0, uint32_t pm, uint32_t pf,
+                                          uint32_t& gt, uint32_t& eq) {
+  const int lane = threadIdx.x & 31;
+  gt = eq = 0;
+  uint4 k4[8];
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int64_t j = j0 + 128 * it + 4 * lane;
+    k4[it] = j < nk ? *reinterpret_cast<const uint4*>(keys + j) : make_uint4(0, 0, 0, 0);
+  }
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int64_t j = j0 + 128 * it + 4 * lane;
+    const uint32_t kk[4] = {k4[it].x, k4[it].y, k4[it].z, k4[it].w};
+    uint32_t g = 0, q = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const uint32_t mk = kk[t] & pm;
+      const bool in = j + t < nk;
+      g |= (in && mk > pf) ? (1u << t) : 0u;
+      q |= (in && mk == pf) ? (1u << t) : 0u;
+    }
+    g <<= 4 * (lane & 7);
+    q <<= 4 * (lane & 7);
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      g |= __shfl_xor_sync(0xffffffffu, g, o);
+      q |= __shfl_xor_sync(0xffffffffu, q, o);
+    }
+    // words 4*it .. 4*it+3 now sit in lanes 0, 8, 16, 24
+    const uint32_t gw = __shfl_sync(0xffffffffu, g, 8 * (lane & 3));
+    const uint32_t qw = __shfl_sync(0xffffffffu, q, 8 * (lane & 3));
+    if ((lane >> 2) == it) {
+      gt = gw;
+      eq = qw;
+    }
+  }
+}
+
+template <typename K>
+__global__ void __launch_bounds__(EMIT_THREADS) dist_emit_ties_kernel(DistParams p, EmitParams e) {
+  __shared__ int red[EMIT_WARPS];
+  const int64_t r = blockIdx.y;
+  const DistState st = p.state[r];
+  const EmitRow er = emit_row(st, e, r, p.rows);
+  int cnt = 0;
+  if (!st.dense && !er.all_ties) {
+    const K* keys = reinterpret_cast<const K*>(p.keys + r * p.keys_ld * sizeof(K));
+    uint32_t gt, eq;
+    key_words(keys, local_keys(p), (int64_t)blockIdx.x * EMIT_CHUNK + (threadIdx.x >> 5) * 1024, (K)st.pmask,
+                 (K)st.prefix, gt, eq);
+    int c = __popc(eq);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    int total;
+    warp_offsets(c, red, total);
+    cnt = total;
+  }
+  if (threadIdx.x == 0) e.key_cnt[r * e.key_chunks + blockIdx.x] = cnt;
+}
+
+template <typename K>
+__global__ void __launch_bounds__(EMIT_THREADS) dist_emit_bits_kernel(DistParams p, EmitParams e) {
+  __shared__ int red[EMIT_WARPS];
+  const int64_t r = blockIdx.y;
+  const DistState st = p.state[r];
+  const EmitRow er = emit_row(st, e, r, p.rows);
+  const int nk = local_keys(p);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t j0 = (int64_t)blockIdx.x * EMIT_CHUNK + warp * 1024;
+  uint32_t* bits = e.bits + r * e.bits_ld;
+  const int64_t word = j0 / 32 + lane;
+  const bool valid = 32 * word < nk;
+  uint32_t sel;
+  if (st.dense) {
+    const int64_t left = nk - 32 * word;
+    sel = left >= 32 ? 0xffffffffu : (left > 0 ? (1u << left) - 1u : 0u);
+  } else {
+    const K* keys = reinterpret_cast<const K*>(p.keys + r * p.keys_ld * sizeof(K));
+    uint32_t gt, eq;
+    key_words(keys, nk, j0, (K)st.pmask, (K)st.prefix, gt, eq);
+    sel = gt;
+    if (er.all_ties) {
       sel |= eq;
     } else {
-      int tie_tot;
-      int rank = run_tie + emit_block_scan(__popc(eq), warp_tot, tie_tot);
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if ((eq >> q) & 1u) {
-          if (rank < need) sel |= 1u << q;
-          ++rank;
-        }
-      run_tie += tie_tot;
-    }
-    if (ps == 1) {
-      if (j0 + 3 >= lo_extra - p.lo || (sink && p.lo == 0 && j0 == 0) || (cur && j0 + 3 >= p.n_global - 1 - p.lo)) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (j0 + q < nk && is_extra(j0 + q)) sel |= 1u << q;
+      const int base = chunk_prefix(e.key_cnt + r * e.key_chunks, blockIdx.x, red);
+      int wt;
+      const int lx = lane_excl_scan(__popc(eq), wt);
+      int total;
+      const int rank0 = base + warp_offsets(wt, red, total) + lx;
+      int take = min(max(er.need - rank0, 0), __popc(eq));
+      uint32_t x = eq;
+      while (take-- > 0) {
+        const uint32_t low = x & (0u - x);
+        sel |= low;
+        x ^= low;
       }
-      int sel_tot;
-      int pos = run_sel + emit_block_scan(__popc(sel), warp_tot, sel_tot);
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if ((sel >> q) & 1u) {
-          if (pos < e.idx_ld) out[pos] = j0 + q;
-          else set_status(e.status, STS_DEV_IDX_CAPACITY);
-          ++pos;
-        }
-      run_sel += sel_tot;
-    } else {
-      // 8 lanes x 4 pages = one 32-bit word of the page bitmap
-      uint32_t w = (sel & 0xfu) << ((lane & 7) * 4);
-      w |= __shfl_xor_sync(0xffffffffu, w, 1);
-      w |= __shfl_xor_sync(0xffffffffu, w, 2);
-      w |= __shfl_xor_sync(0xffffffffu, w, 4);
-      if ((lane & 7) == 0 && j0 < nk) pbits[j0 >> 5] = w;
     }
   }
-  if (ps > 1) {
-    __syncthreads();  // page bitmap (global, this CTA's own writes) visible block-wide
-    for (int base = 0; base < nc; base += 4 * EMIT_THREADS) {
-      const int j0 = base + 4 * threadIdx.x;
-      uint32_t sel = 0;
+  if (valid) bits[word] = sel;
+}
+
+// selected bit of local token j (its key's bitmap bit, or an extra)
+struct TokenSel {
+  const uint32_t* bits;
+  int ps, nc, lo, n_global, lo_extra;
+  bool sink, cur;
+  __device__ __forceinline__ bool operator()(int64_t j) const {
+    if (j >= nc) return false;
+    const int64_t k = ps == 1 ? j : j / ps;
+    const int g = lo + (int)j;
+    return ((bits[k >> 5] >> (k & 31)) & 1u) || g >= lo_extra || (sink && g == 0) || (cur && g == n_global - 1);
+  }
+};
+
+// bits of [a, b) inside the 32-token word starting at w0
+__device__ __forceinline__ uint32_t range_bits(int64_t a, int64_t b, int64_t w0) {
+  const int64_t l = max(a - w0, (int64_t)0), h = min(b - w0, (int64_t)32);
+  if (h <= l) return 0u;
+  return (h - l == 32 ? 0xffffffffu : ((1u << (h - l)) - 1u)) << l;
+}
+
+// token mode: the selected tokens of word w (bitmap word | extras), committed only
+__device__ __forceinline__ uint32_t token_word(const TokenSel& t, int64_t w) {
+  const int64_t w0 = 32 * w;
+  if (w0 >= t.nc) return 0u;
+  uint32_t m = t.bits[w] | range_bits((int64_t)t.lo_extra - t.lo, t.nc, w0);
+  if (t.sink && t.lo == 0 && w == 0) m |= 1u;
+  if (t.cur) m |= range_bits((int64_t)t.n_global - 1 - t.lo, (int64_t)t.n_global - t.lo, w0);
+  return m & range_bits(0, t.nc, w0);
+}
+
+__device__ __forceinline__ TokenSel token_sel(const DistParams& p, const EmitParams& e, int64_t r) {
+  TokenSel t;
+  t.bits = e.bits + r * e.bits_ld;
+  t.ps = p.page_size;
+  t.nc = local_committed(p);
+  t.lo = p.lo;
+  t.n_global = p.n_global;
+  t.lo_extra = e.recent_window > 0 ? p.n_global - e.recent_window : p.n_global;
+  t.sink = (e.flags & STS_SEL_SINK) != 0;
+  t.cur = (e.flags & STS_SEL_CURRENT) != 0;
+  return t;
+}
+
+__global__ void __launch_bounds__(EMIT_THREADS) dist_emit_count_kernel(DistParams p, EmitParams e) {
+  __shared__ int red[EMIT_WARPS];
+  const int64_t r = blockIdx.y;
+  const TokenSel sel = token_sel(p, e, r);
+  const int lane = threadIdx.x & 31;
+  const int64_t j0 = (int64_t)blockIdx.x * EMIT_CHUNK + (threadIdx.x >> 5) * 1024;
+  int c = 0;
+  if (sel.ps == 1) {
+    c = __popc(token_word(sel, (int64_t)blockIdx.x * (EMIT_CHUNK / 32) + threadIdx.x));
+  } else if (j0 < sel.nc) {
+#pragma unroll 4
+    for (int w = 0; w < 32; ++w) c += sel(j0 + 32 * w + lane) ? 1 : 0;
+  }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int j = j0 + q;
-        if (j >= nc) break;
-        const int pg = j / ps;
-        if (((pbits[pg >> 5] >> (pg & 31)) & 1u) || is_extra(j)) sel |= 1u << q;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  int total;
+  warp_offsets(c, red, total);
+  if (threadIdx.x == 0) e.tok_cnt[r * e.tok_chunks + blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(EMIT_THREADS) dist_emit_write_kernel(DistParams p, EmitParams e) {
+  __shared__ int red[EMIT_WARPS];
+  const int64_t r = blockIdx.y;
+  const TokenSel sel = token_sel(p, e, r);
+  const int lane = threadIdx.x & 31;
+  const int64_t j0 = (int64_t)blockIdx.x * EMIT_CHUNK + (threadIdx.x >> 5) * 1024;
+  int32_t* out = e.idx_out + r * e.idx_ld;
+  const int32_t* tc = e.tok_cnt + r * e.tok_chunks;
+  const int64_t w = (int64_t)blockIdx.x * (EMIT_CHUNK / 32) + threadIdx.x;
+  uint32_t m = sel.ps == 1 ? token_word(sel, w) : 0u;  // issued before the prefix sum
+  const int base = chunk_prefix(tc, blockIdx.x, red);
+  if (sel.ps == 1) {
+    // one token word per thread
+    int wt;
+    const int lx = lane_excl_scan(__popc(m), wt);
+    int total;
+    int at = base + warp_offsets(wt, red, total) + lx;
+    while (m) {
+      const int b = __ffs(m) - 1;
+      m &= m - 1u;
+      if (at < e.idx_ld) out[at] = (int32_t)(32 * w + b);
+      else set_status(e.status, STS_DEV_IDX_CAPACITY);
+      ++at;
+    }
+  } else {
+    uint32_t mine = 0;
+    if (j0 < sel.nc) {
+#pragma unroll 4
+      for (int ww = 0; ww < 32; ++ww) {
+        const uint32_t b = __ballot_sync(0xffffffffu, sel(j0 + 32 * ww + lane));
+        if (lane == ww) mine = b;
       }
-      int sel_tot;
-      int pos = run_sel + emit_block_scan(__popc(sel), warp_tot, sel_tot);
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if ((sel >> q) & 1u) {
-          if (pos < e.idx_ld) out[pos] = j0 + q;
+    }
+    int wt;
+    lane_excl_scan(__popc(mine), wt);
+    int total;
+    int pos = base + warp_offsets(wt, red, total);
+    if (j0 < sel.nc) {
+      const uint32_t lt = (1u << lane) - 1u;
+      for (int ww = 0; ww < 32; ++ww) {
+        const uint32_t b = __shfl_sync(0xffffffffu, mine, ww);
+        if ((b >> lane) & 1u) {
+          const int at = pos + __popc(b & lt);
+          if (at < e.idx_ld) out[at] = (int32_t)(j0 + 32 * ww + lane);
           else set_status(e.status, STS_DEV_IDX_CAPACITY);
-          ++pos;
         }
-      run_sel += sel_tot;
+        pos += __popc(b);
+      }
     }
   }
-  // in-block tail: global [n_global, n_global + tail_len) held here
-  const int t_lo = max(p.n_global - p.lo, 0);
-  const int t_hi = min(p.n_global + e.tail_len - p.lo, e.n_kv_local);
-  for (int j = t_lo + threadIdx.x; j < t_hi; j += EMIT_THREADS) {
-    const int pos = run_sel + (j - t_lo);
-    if (pos < e.idx_ld) out[pos] = j;
-    else set_status(e.status, STS_DEV_IDX_CAPACITY);
+  if (blockIdx.x == 0) {
+    // in-block tail: global [n_global, n_global + tail_len) held here
+    const int all = chunk_prefix(tc, e.tok_chunks, red);
+    const int t_lo = max(p.n_global - p.lo, 0);
+    const int t_hi = min(p.n_global + e.tail_len - p.lo, e.n_kv_local);
+    for (int j = t_lo + threadIdx.x; j < t_hi; j += EMIT_THREADS) {
+      const int at = all + (j - t_lo);
+      if (at < e.idx_ld) out[at] = j;
+      else set_status(e.status, STS_DEV_IDX_CAPACITY);
+    }
+    if (threadIdx.x == 0) e.cnt_out[r] = all + max(t_hi - t_lo, 0);
   }
-  if (threadIdx.x == 0) e.cnt_out[r] = run_sel + max(t_hi - t_lo, 0);
 }
 
 }  // namespace
@@ -416,19 +639,40 @@ int64_t dist_keys_ld(int32_t n_local, int32_t page_size) {
 }
 
 int64_t dist_bits_ld(int32_t n_local, int32_t page_size) {
-  if (page_size == 1) return 0;
   return (dist_keys_ld(n_local, page_size) + 31) / 32 + 1;
 }
 
-size_t dist_ws_bytes(int64_t rows, int32_t n_local, int32_t page_size) {
-  const size_t state = ((size_t)rows * sizeof(DistState) + 255) & ~size_t(255);
-  const size_t ksz = page_size == 1 ? 4 : 8;
-  const size_t keys = ((size_t)rows * dist_keys_ld(n_local, page_size) * ksz + 255) & ~size_t(255);
-  const size_t bits = (size_t)rows * dist_bits_ld(n_local, page_size) * 4;
-  return state + keys + bits + 256;
+int64_t dist_key_chunks(int32_t n_local, int32_t page_size) {
+  const int64_t nk = page_size == 1 ? n_local : ((int64_t)n_local + page_size - 1) / page_size;
+  return nk > 0 ? (nk + EMIT_CHUNK - 1) / EMIT_CHUNK : 1;
 }
 
-int dist_params(const sts_dist_rows* g, void* ws, size_t ws_bytes, DistParams& p, uint32_t** bits) {
+int64_t dist_tok_chunks(int32_t n_local) { return n_local > 0 ? ((int64_t)n_local + EMIT_CHUNK - 1) / EMIT_CHUNK : 1; }
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+// workspace: [state][keys][selected-key bitmap][tie counts per key chunk][token counts per token chunk]
+struct DistWs {
+  size_t state, keys, bits, key_cnt, tok_cnt;
+};
+
+DistWs dist_ws_layout(int64_t rows, int32_t n_local, int32_t page_size) {
+  DistWs w;
+  const size_t ksz = page_size == 1 ? 4 : 8;
+  w.state = align256((size_t)rows * sizeof(DistState));
+  w.keys = align256((size_t)rows * dist_keys_ld(n_local, page_size) * ksz);
+  w.bits = align256((size_t)rows * dist_bits_ld(n_local, page_size) * 4);
+  w.key_cnt = align256((size_t)rows * dist_key_chunks(n_local, page_size) * 4);
+  w.tok_cnt = align256((size_t)rows * dist_tok_chunks(n_local) * 4);
+  return w;
+}
+
+size_t dist_ws_bytes(int64_t rows, int32_t n_local, int32_t page_size) {
+  const DistWs w = dist_ws_layout(rows, n_local, page_size);
+  return w.state + w.keys + w.bits + w.key_cnt + w.tok_cnt + 256;
+}
+
+int dist_params(const sts_dist_rows* g, void* ws, size_t ws_bytes, DistParams& p, EmitParams* e = nullptr) {
   STS_REQUIRE(g != nullptr, STS_ERR_CONTRACT, "null geometry");
   STS_REQUIRE(g->rows >= 0 && g->rows <= 65535, STS_ERR_CONTRACT, "rows must be in [0, 65535]");
   STS_REQUIRE(g->nsrc >= 1 && g->nsrc <= 8, STS_ERR_CONTRACT, "nsrc must be in [1, 8], got %d", g->nsrc);
@@ -452,14 +696,20 @@ int dist_params(const sts_dist_rows* g, void* ws, size_t ws_bytes, DistParams& p
   p.n_local = g->n_local;
   p.k_top = g->k_top;
   p.page_size = g->page_size;
+  p.vec4 = (g->ld % 4 == 0 && (reinterpret_cast<uintptr_t>(g->scores_dev) & 15) == 0) ? 1 : 0;
+  const DistWs w = dist_ws_layout(g->rows, g->n_local, g->page_size);
   uint8_t* base = static_cast<uint8_t*>(ws);
-  const size_t state = ((size_t)g->rows * sizeof(DistState) + 255) & ~size_t(255);
-  const size_t ksz = g->page_size == 1 ? 4 : 8;
-  const size_t keys = ((size_t)g->rows * dist_keys_ld(g->n_local, g->page_size) * ksz + 255) & ~size_t(255);
   p.state = reinterpret_cast<DistState*>(base);
-  p.keys = base + state;
+  p.keys = base + w.state;
   p.keys_ld = dist_keys_ld(g->n_local, g->page_size);
-  *bits = reinterpret_cast<uint32_t*>(base + state + keys);
+  if (e) {
+    e->bits = reinterpret_cast<uint32_t*>(base + w.state + w.keys);
+    e->bits_ld = dist_bits_ld(g->n_local, g->page_size);
+    e->key_cnt = reinterpret_cast<int32_t*>(base + w.state + w.keys + w.bits);
+    e->tok_cnt = reinterpret_cast<int32_t*>(base + w.state + w.keys + w.bits + w.key_cnt);
+    e->key_chunks = (int)dist_key_chunks(g->n_local, g->page_size);
+    e->tok_chunks = (int)dist_tok_chunks(g->n_local);
+  }
   return STS_OK;
 }
 
@@ -488,8 +738,7 @@ extern "C" size_t sts_dist_select_workspace_bytes(int64_t rows, int32_t n_local,
 extern "C" int sts_dist_select_begin(const sts_dist_rows* g, int32_t* hist_local_dev, void* workspace_dev,
                                      size_t workspace_bytes, void* stream) {
   DistParams p;
-  uint32_t* bits;
-  int rc = dist_params(g, workspace_dev, workspace_bytes, p, &bits);
+  int rc = dist_params(g, workspace_dev, workspace_bytes, p);
   if (rc != STS_OK) return rc;
   if (p.rows == 0) return STS_OK;
   STS_REQUIRE(hist_local_dev, STS_ERR_CONTRACT, "null histogram");
@@ -505,8 +754,7 @@ extern "C" int sts_dist_select_round(const sts_dist_rows* g, int32_t round, cons
                                      int32_t* hist_local_dev, int32_t* ties_local_dev, void* workspace_dev,
                                      size_t workspace_bytes, void* stream) {
   DistParams p;
-  uint32_t* bits;
-  int rc = dist_params(g, workspace_dev, workspace_bytes, p, &bits);
+  int rc = dist_params(g, workspace_dev, workspace_bytes, p);
   if (rc != STS_OK) return rc;
   const int rounds = sts_dist_select_rounds(p.page_size);
   STS_REQUIRE(round >= 0 && round < rounds, STS_ERR_CONTRACT, "round %d out of [0, %d)", round, rounds);
@@ -537,15 +785,14 @@ extern "C" int sts_dist_select_finish(const sts_dist_rows* g, int32_t rank, int3
                                       int32_t* cnt_out_dev, int32_t* status_dev, void* workspace_dev,
                                       size_t workspace_bytes, void* stream) {
   DistParams p;
-  uint32_t* bits;
-  int rc = dist_params(g, workspace_dev, workspace_bytes, p, &bits);
+  EmitParams e;
+  int rc = dist_params(g, workspace_dev, workspace_bytes, p, &e);
   if (rc != STS_OK) return rc;
   STS_REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, STS_ERR_CONTRACT, "bad rank %d of %d", rank, nranks);
   STS_REQUIRE(recent_window >= 0 && tail_len >= 0, STS_ERR_INPUT, "recent_window / tail_len must be >= 0");
   STS_REQUIRE(n_kv_local >= 0, STS_ERR_CONTRACT, "n_kv_local must be >= 0");
   if (p.rows == 0) return STS_OK;
   STS_REQUIRE(ties_all_dev && idx_out_dev && cnt_out_dev, STS_ERR_CONTRACT, "null buffer");
-  EmitParams e;
   e.rank = rank;
   e.nranks = nranks;
   e.ties_all = ties_all_dev;
@@ -557,11 +804,21 @@ extern "C" int sts_dist_select_finish(const sts_dist_rows* g, int32_t rank, int3
   e.idx_ld = idx_ld;
   e.cnt_out = cnt_out_dev;
   e.status = status_dev;
-  e.page_bits = p.page_size == 1 ? nullptr : bits;
-  e.page_bits_ld = dist_bits_ld(p.n_local, p.page_size);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  if (p.page_size == 1) dist_emit_kernel<uint32_t><<<(unsigned)p.rows, EMIT_THREADS, 0, st>>>(p, e);
-  else dist_emit_kernel<uint64_t><<<(unsigned)p.rows, EMIT_THREADS, 0, st>>>(p, e);
+  const dim3 kgrid((unsigned)e.key_chunks, (unsigned)p.rows), tgrid((unsigned)e.tok_chunks, (unsigned)p.rows);
+  if (p.page_size == 1) {
+    dist_emit_ties_kernel<uint32_t><<<kgrid, EMIT_THREADS, 0, st>>>(p, e);
+    STS_LAUNCH_CHECK();
+    dist_emit_bits_kernel<uint32_t><<<kgrid, EMIT_THREADS, 0, st>>>(p, e);
+  } else {
+    dist_emit_ties_kernel<uint64_t><<<kgrid, EMIT_THREADS, 0, st>>>(p, e);
+    STS_LAUNCH_CHECK();
+    dist_emit_bits_kernel<uint64_t><<<kgrid, EMIT_THREADS, 0, st>>>(p, e);
+  }
+  STS_LAUNCH_CHECK();
+  dist_emit_count_kernel<<<tgrid, EMIT_THREADS, 0, st>>>(p, e);
+  STS_LAUNCH_CHECK();
+  dist_emit_write_kernel<<<tgrid, EMIT_THREADS, 0, st>>>(p, e);
   STS_LAUNCH_CHECK();
   return STS_OK;
 }
