@@ -79,6 +79,11 @@ __device__ __forceinline__ int unit_tiles(const DecodeParams& p, int64_t u, int 
 }
 
 
+// resident warps per SM the draft (K-only) kernels' register budget targets
+#ifndef STS_DRAFT_WARPS
+#define STS_DRAFT_WARPS 16
+#endif
+
 template <int D, int NW, int KT, int STAGES, int MODE>
 struct VL {
   static constexpr bool K_ONLY = MODE != MODE_DECODE;
@@ -98,7 +103,7 @@ struct VL {
   // resident CTAs per SM the register allocation must allow: the shared-memory
   // limit, capped so a warp keeps ~168 registers (O, Q fragments, S, P)
   static constexpr int SMEM_CTAS = (227 * 1024) / (SMEM + 1024);
-  static constexpr int REG_CTAS = K_ONLY ? 16 / NW : (NW == 1 ? 12 : (NW == 2 ? 6 : 3));
+  static constexpr int REG_CTAS = K_ONLY ? STS_DRAFT_WARPS / NW : (NW == 1 ? 12 : (NW == 2 ? 6 : 3));
   static constexpr int MINB = SMEM_CTAS < REG_CTAS ? (SMEM_CTAS < 1 ? 1 : SMEM_CTAS) : REG_CTAS;
   static constexpr int GROWS = THREADS / CH;      // rows per gather pass
   static constexpr int GJ = (KT + GROWS - 1) / GROWS;
