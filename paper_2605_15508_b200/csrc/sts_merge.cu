@@ -193,32 +193,113 @@ __global__ void bitset_scatter_kernel(const int32_t* __restrict__ idx, int64_t i
   }
 }
 
-constexpr int OVL_THREADS = 256;
+// |A ∩ B| of two bitsets is the dot product of their 0/1 bit vectors, so the
+// all-pairs overlap is an integer GEMM: scores[Ta][Tb] += A[Ta][K] · B[Tb][K]ᵀ
+// with K = 32·W bits.  It runs on the int8 tensor cores (mma.sync m16n8k32
+// u8·u8 → s32, exact): each 4-bit nibble of a bitset word expands to four
+// 0/1 bytes with one multiply — (x·0x204081) & 0x01010101 puts bit i at byte
+// i — straight into the MMA fragment registers, so the bitsets stay 1 bit per
+// element in memory.  CTA tile 128 a-rows × 64 b-rows, four warps of 64 × 32
+// (4 × 4 MMAs per 32-bit word), words staged through shared memory in chunks
+// of OVL_KC with padded rows (the 8 row groups of a warp hit distinct banks).
+constexpr int OVL_THREADS = 128;
+constexpr int OVL_TA = 128, OVL_TB = 64;
+constexpr int OVL_KC = 32;  // words per chunk
+constexpr int OVL_PITCH = OVL_KC + 1;
 
-__global__ void __launch_bounds__(OVL_THREADS) bitset_overlap_kernel(const uint32_t* __restrict__ a,
-                                                                     const uint32_t* __restrict__ b,
-                                                                     int64_t W, int32_t Tb,
+__device__ __forceinline__ uint32_t nibble_bytes(uint32_t x, int shift) {
+  return (((x >> shift) & 15u) * 0x204081u) & 0x01010101u;
+}
+
+__device__ __forceinline__ void mma_u8_16832(int (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+__global__ void __launch_bounds__(OVL_THREADS) bitset_overlap_kernel(const uint32_t* __restrict__ a, int32_t Ta,
+                                                                     const uint32_t* __restrict__ b, int32_t Tb,
+                                                                     int64_t ld, int64_t W, int64_t kspan,
                                                                      unsigned long long* scores) {
-  const int64_t ia = blockIdx.y, ib = blockIdx.x;
-  const uint4* pa = reinterpret_cast<const uint4*>(a + ia * W);
-  const uint4* pb = reinterpret_cast<const uint4*>(b + ib * W);
-  unsigned long long acc = 0;
-  const int64_t W4 = W / 4;
-  for (int64_t w = threadIdx.x; w < W4; w += OVL_THREADS) {
-    const uint4 x = __ldg(pa + w), y = __ldg(pb + w);
-    acc += __popc(x.x & y.x) + __popc(x.y & y.y) + __popc(x.z & y.z) + __popc(x.w & y.w);
-  }
-  for (int64_t w = 4 * W4 + threadIdx.x; w < W; w += OVL_THREADS) acc += __popc(a[ia * W + w] & b[ib * W + w]);
+  __shared__ uint32_t As[OVL_TA * OVL_PITCH];
+  __shared__ uint32_t Bs[OVL_TB * OVL_PITCH];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int wa = (warp >> 1) * 64, wb = (warp & 1) * 32;  // warp tile origin inside the CTA tile
+  const int64_t a0 = (int64_t)blockIdx.y * OVL_TA, b0 = (int64_t)blockIdx.x * OVL_TB;
+  // loader: 8 threads per row, one uint4 each (a: 16 rows per pass x 8 passes, b: x 4)
+  const int lr = tid >> 3, lc = tid & 7;
+  int acc[4][4][4];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  __shared__ unsigned long long s_acc[OVL_THREADS / 32];
-  if ((threadIdx.x & 31) == 0) s_acc[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long t = 0;
-    for (int i = 0; i < OVL_THREADS / 32; ++i) t += s_acc[i];
-    scores[ia * Tb + ib] += t;  // one block per pair: no race
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[i][j][e] = 0;
+  const int64_t W4 = W / 4;  // W % 4 == 0 (checked on the host)
+  // split-K: this CTA takes words [kspan * z, kspan * (z + 1)) (kspan % OVL_KC == 0)
+  const int64_t k_lo = kspan * blockIdx.z, k_hi = k_lo + kspan < W ? k_lo + kspan : W;
+  for (int64_t c0 = k_lo; c0 < k_hi; c0 += OVL_KC) {
+    const int64_t v = c0 / 4 + lc;
+    uint4 xa[OVL_TA / 16], xb[OVL_TB / 16];
+#pragma unroll
+    for (int i = 0; i < OVL_TA / 16; ++i) {
+      const int64_t r = a0 + lr + 16 * i;
+      xa[i] = r < Ta && v < W4 ? __ldg(reinterpret_cast<const uint4*>(a + r * ld) + v) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int i = 0; i < OVL_TB / 16; ++i) {
+      const int64_t r = b0 + lr + 16 * i;
+      xb[i] = r < Tb && v < W4 ? __ldg(reinterpret_cast<const uint4*>(b + r * ld) + v) : make_uint4(0, 0, 0, 0);
+    }
+    __syncthreads();  // previous chunk consumed
+#pragma unroll
+    for (int i = 0; i < OVL_TA / 16; ++i) {
+      uint32_t* d = As + (lr + 16 * i) * OVL_PITCH + 4 * lc;
+      d[0] = xa[i].x; d[1] = xa[i].y; d[2] = xa[i].z; d[3] = xa[i].w;
+    }
+#pragma unroll
+    for (int i = 0; i < OVL_TB / 16; ++i) {
+      uint32_t* d = Bs + (lr + 16 * i) * OVL_PITCH + 4 * lc;
+      d[0] = xb[i].x; d[1] = xb[i].y; d[2] = xb[i].z; d[3] = xb[i].w;
+    }
+    __syncthreads();
+#pragma unroll 2
+    for (int w = 0; w < OVL_KC; ++w) {
+      uint32_t bf[4][2];
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const uint32_t y = Bs[(wb + nt * 8 + g) * OVL_PITCH + w];
+        bf[nt][0] = nibble_bytes(y, 4 * q);
+        bf[nt][1] = nibble_bytes(y, 16 + 4 * q);
+      }
+#pragma unroll
+      for (int mt = 0; mt < 4; ++mt) {
+        const uint32_t x0 = As[(wa + mt * 16 + g) * OVL_PITCH + w];
+        const uint32_t x1 = As[(wa + mt * 16 + 8 + g) * OVL_PITCH + w];
+        const uint32_t af[4] = {nibble_bytes(x0, 4 * q), nibble_bytes(x1, 4 * q), nibble_bytes(x0, 16 + 4 * q),
+                                nibble_bytes(x1, 16 + 4 * q)};
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) mma_u8_16832(acc[mt][nt], af, bf[nt]);
+      }
+    }
   }
+#pragma unroll
+  for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t ia = a0 + wa + mt * 16 + g + 8 * h;
+      if (ia >= Ta) continue;
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int64_t ib = b0 + wb + nt * 8 + 2 * q + e;
+          // integer adds commute: the split-K partials land in any order, same result
+          if (ib < Tb) atomicAdd(scores + ia * Tb + ib, (unsigned long long)acc[mt][nt][2 * h + e]);
+        }
+    }
 }
 
 }  // namespace
@@ -244,9 +325,19 @@ extern "C" int sts_bitset_overlap(const uint32_t* a_dev, int32_t Ta, const uint3
   STS_REQUIRE(a_dev && b_dev && scores_dev, STS_ERR_CONTRACT, "null buffer");
   STS_REQUIRE((reinterpret_cast<uintptr_t>(a_dev) | reinterpret_cast<uintptr_t>(b_dev)) % 16 == 0 && W % 4 == 0,
               STS_ERR_CONTRACT, "bitsets must be 16-byte aligned with W % 4 == 0");
-  dim3 grid((unsigned)Tb, (unsigned)Ta);
-  sts::bitset_overlap_kernel<<<grid, sts::OVL_THREADS, 0, static_cast<cudaStream_t>(stream)>>>(a_dev, b_dev, W, Tb,
-                                                                                               scores_dev);
+  // per-CTA counts are signed 32-bit: at most 2^25 words (2^30 bits) per split
+  const int64_t gx = (Tb + sts::OVL_TB - 1) / sts::OVL_TB, gy = (Ta + sts::OVL_TA - 1) / sts::OVL_TA;
+  const int64_t chunks = (W + sts::OVL_KC - 1) / sts::OVL_KC;
+  int64_t ksplit = (3 * (int64_t)sts::num_sms() + gx * gy - 1) / (gx * gy);  // ~3 CTAs per SM
+  const int64_t min_split = (W + (int64_t(1) << 25) - 1) >> 25;
+  ksplit = ksplit < min_split ? min_split : ksplit;
+  ksplit = ksplit > chunks ? chunks : ksplit;
+  STS_REQUIRE(ksplit <= 65535, STS_ERR_CONTRACT, "bitsets too long (W = %lld words)", (long long)W);
+  const int64_t kspan = (chunks + ksplit - 1) / ksplit * sts::OVL_KC;
+  ksplit = (W + kspan - 1) / kspan;
+  const dim3 grid((unsigned)gx, (unsigned)gy, (unsigned)ksplit);
+  sts::bitset_overlap_kernel<<<grid, sts::OVL_THREADS, 0, static_cast<cudaStream_t>(stream)>>>(
+      a_dev, Ta, b_dev, Tb, W, W, kspan, scores_dev);
   STS_LAUNCH_CHECK();
   return STS_OK;
 }

@@ -46,3 +46,28 @@ def test_gpu_algorithm1_matches_reference(cuda_ok):
         mp = find_head_mapping(ts, int(k))
         for tl, th, dl, dh, score in rows:
             assert mp.entries[(tl, th)] == ((dl, dh), score), (k, tl, th)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("Ta,Tb,W", [(1, 1, 4), (70, 33, 100), (64, 130, 4096), (5, 200, 36), (3, 2, 100000), (300, 129, 1028)])
+def test_gpu_bitset_overlap_matches_popcount(cuda_ok, Ta, Tb, W):
+    """sts_bitset_overlap (tiled AND + popcount) = numpy's popcount of the ANDs,
+    accumulated into the existing scores (ragged tiles and chunks)."""
+    import torch
+
+    from paper_2605_15508_b200 import _lib
+    from paper_2605_15508_b200._lib import call, ptr, stream_handle
+
+    _lib.load()
+    rng = np.random.default_rng(Ta * 1000 + Tb + W)
+    a = rng.integers(0, 2**32, size=(Ta, W), dtype=np.uint64).astype(np.uint32)
+    b = rng.integers(0, 2**32, size=(Tb, W), dtype=np.uint64).astype(np.uint32)
+    a[0, :] = 0xFFFFFFFF  # saturated row
+    init = rng.integers(0, 1000, size=(Ta, Tb)).astype(np.int64)
+    da = torch.from_numpy(a.view(np.int32)).cuda()
+    db = torch.from_numpy(b.view(np.int32)).cuda()
+    scores = torch.from_numpy(init.copy()).cuda()
+    call("sts_bitset_overlap", ptr(da), Ta, ptr(db), Tb, W, ptr(scores), stream_handle())
+    torch.cuda.synchronize()
+    pc = np.unpackbits((a[:, None, :] & b[None, :, :]).view(np.uint8), axis=-1).sum(axis=-1)
+    np.testing.assert_array_equal(scores.cpu().numpy(), init + pc)
