@@ -27,6 +27,7 @@ All buffers are allocated once in ``__init__``; ``step`` allocates nothing.
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -148,6 +149,9 @@ class STSVerifyStep:
         keys = self.idx_ld
         self.splits = splits if splits is not None else kernels._lib.load().sts_auto_splits(s.target_units, keys)
         self.dense_splits = kernels._lib.load().sts_auto_splits(s.target_units, s.n_kv)
+        # unit groups of the host-buffer attention pipeline (see attend_host)
+        # (2 measured best at c2: 157 vs 200 µs for 1, 200 for 3 — tools/gpu_e2e_chunks.sh)
+        self.host_chunks = int(os.environ.get("STS_HOST_CHUNKS", "2"))
 
     # -- the four stages ----------------------------------------------------------
     def capture(self, draft_q, draft_k, stream=None):
@@ -222,18 +226,59 @@ class STSVerifyStep:
             self._d_dq = torch.empty(h_dq.shape, dtype=h_dq.dtype, device=self.device)
         return getattr(self, "_d_dq", None), self._d_tq
 
-    def attend_host(self, h_tq, target_k, target_v, h_out):
+    def attend_host(self, h_tq, target_k, target_v, h_out, chunks=None):
         """Target attention with host queries: H2D copy of Q [B, L, Hq, R, d]
-        (pinned), the attention graph, D2H copy of the output into ``h_out``.
-        The masks are the ones the last ``build_masks`` produced."""
+        (pinned), the attention, D2H copy of the output into ``h_out`` (pinned,
+        shaped like ``self.out``).  The masks are the ones the last
+        ``build_masks`` produced.
+
+        ``chunks`` > 1 pipelines the copies with the kernel: the units are cut
+        into ``chunks`` contiguous groups and, inside one CUDA graph, the H2D of
+        group c+1 and the D2H of group c-1 run on side streams while group c
+        attends, so the link time hides behind the HBM-bound kernel.
+        """
+        chunks = self.host_chunks if chunks is None else int(chunks)
         _, d_tq = self._host_buffers(None, h_tq)
-        d_tq.copy_(h_tq, non_blocking=True)
         q, k, v = self.target_views(d_tq, target_k, target_v)
-        key = ("attend", target_k.data_ptr(), target_v.data_ptr(),
-               self.idx.data_ptr() if self.idx is not None else 0)
-        self._graph(key, lambda: self.attend(q, k, v)).replay()
-        h_out.copy_(self.out, non_blocking=True)
+        idx_ptr = self.idx.data_ptr() if self.idx is not None else 0
+        if chunks <= 1:
+            d_tq.copy_(h_tq, non_blocking=True)
+            key = ("attend", target_k.data_ptr(), target_v.data_ptr(), idx_ptr)
+            self._graph(key, lambda: self.attend(q, k, v)).replay()
+            h_out.copy_(self.out, non_blocking=True)
+            return h_out
+        key = ("attend_host", chunks, h_tq.data_ptr(), h_out.data_ptr(), target_k.data_ptr(), target_v.data_ptr(),
+               idx_ptr)
+        self._graph(key, lambda: self._attend_pipelined(h_tq, d_tq, q, k, v, h_out, chunks)).replay()
         return h_out
+
+    def _attend_pipelined(self, h_tq, d_tq, q, k, v, h_out, chunks):
+        s = self.shape
+        U = s.target_units
+        C = max(1, min(chunks, U))
+        main = torch.cuda.current_stream(self.device)
+        if getattr(self, "_copy_streams", None) is None:
+            self._copy_streams = (torch.cuda.Stream(device=self.device), torch.cuda.Stream(device=self.device))
+        s_in, s_out = self._copy_streams
+        hq, dq_ = h_tq.view(U, -1), d_tq.view(U, -1)
+        ho = h_out.view(U, -1)
+        s_in.wait_stream(main)
+        s_out.wait_stream(main)
+        causal = s.context if self.mode == "S" else -1
+        for c in range(C):
+            u0, u1 = U * c // C, U * (c + 1) // C
+            with torch.cuda.stream(s_in):
+                dq_[u0:u1].copy_(hq[u0:u1], non_blocking=True)
+            main.wait_stream(s_in)
+            member = self.member[u0:u1] if self.member is not None else None
+            kernels.sparse_decode(q[u0:u1], k[u0:u1], v[u0:u1], idx=self.idx[u0:u1], cnt=self.cnt[u0:u1],
+                                  member=member, causal_base=causal, rows_per_head=s.rows,
+                                  out=self.out[u0:u1], lse=self.lse[u0:u1], status=self.status,
+                                  workspace=self.ws_dec, stream=main)
+            s_out.wait_stream(main)
+            with torch.cuda.stream(s_out):
+                ho[u0:u1].copy_(self.out[u0:u1].view(u1 - u0, -1), non_blocking=True)
+        main.wait_stream(s_out)
 
     def step_host(self, h_dq, draft_k, h_tq, target_k, target_v, h_out):
         """The whole verify step with host queries (draft Q [B, Ld, Hqd, R, dd]
