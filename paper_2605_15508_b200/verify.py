@@ -257,19 +257,19 @@ class STSVerifyStep:
         U = s.target_units
         C = max(1, min(chunks, U))
         main = torch.cuda.current_stream(self.device)
-        if getattr(self, "_copy_streams", None) is None:
-            self._copy_streams = (torch.cuda.Stream(device=self.device), torch.cuda.Stream(device=self.device))
-        s_in, s_out = self._copy_streams
-        hq, dq_ = h_tq.view(U, -1), d_tq.view(U, -1)
+        s_in, s_out = self._streams()
+        dq_ = d_tq.view(U, -1)
+        hq = h_tq.view(U, -1) if h_tq is not None else None  # None: the queries are on the device already
         ho = h_out.view(U, -1)
         s_in.wait_stream(main)
         s_out.wait_stream(main)
         causal = s.context if self.mode == "S" else -1
         for c in range(C):
             u0, u1 = U * c // C, U * (c + 1) // C
-            with torch.cuda.stream(s_in):
-                dq_[u0:u1].copy_(hq[u0:u1], non_blocking=True)
-            main.wait_stream(s_in)
+            if hq is not None:
+                with torch.cuda.stream(s_in):
+                    dq_[u0:u1].copy_(hq[u0:u1], non_blocking=True)
+                main.wait_stream(s_in)
             member = self.member[u0:u1] if self.member is not None else None
             kernels.sparse_decode(q[u0:u1], k[u0:u1], v[u0:u1], idx=self.idx[u0:u1], cnt=self.cnt[u0:u1],
                                   member=member, causal_base=causal, rows_per_head=s.rows,
@@ -280,18 +280,49 @@ class STSVerifyStep:
                 ho[u0:u1].copy_(self.out[u0:u1].view(u1 - u0, -1), non_blocking=True)
         main.wait_stream(s_out)
 
-    def step_host(self, h_dq, draft_k, h_tq, target_k, target_v, h_out):
+    def step_host(self, h_dq, draft_k, h_tq, target_k, target_v, h_out, chunks=None):
         """The whole verify step with host queries (draft Q [B, Ld, Hqd, R, dd]
-        and target Q), replayed as one CUDA graph; output copied to ``h_out``."""
+        and target Q), replayed as one CUDA graph; output copied to ``h_out``.
+
+        With ``chunks`` > 1 (default ``host_chunks``) the copies ride inside the
+        graph: the target-Q H2D runs on a side stream under the capture and
+        select stages, and the output D2H of each unit group overlaps the
+        attention of the next."""
+        chunks = self.host_chunks if chunks is None else int(chunks)
         d_dq, d_tq = self._host_buffers(h_dq, h_tq)
-        d_dq.copy_(h_dq, non_blocking=True)
-        d_tq.copy_(h_tq, non_blocking=True)
         dq, dk = self.draft_views(d_dq, draft_k)
         q, k, v = self.target_views(d_tq, target_k, target_v)
-        key = ("step", draft_k.data_ptr(), target_k.data_ptr(), target_v.data_ptr())
-        self._graph(key, lambda: self.step(dq, dk, q, k, v)).replay()
-        h_out.copy_(self.out, non_blocking=True)
+        if chunks <= 1:
+            d_dq.copy_(h_dq, non_blocking=True)
+            d_tq.copy_(h_tq, non_blocking=True)
+            key = ("step", draft_k.data_ptr(), target_k.data_ptr(), target_v.data_ptr())
+            self._graph(key, lambda: self.step(dq, dk, q, k, v)).replay()
+            h_out.copy_(self.out, non_blocking=True)
+            return h_out
+
+        def body():
+            main = torch.cuda.current_stream(self.device)
+            s_in, _ = self._streams()
+            s_in.wait_stream(main)
+            with torch.cuda.stream(s_in):
+                d_dq.copy_(h_dq, non_blocking=True)
+            main.wait_stream(s_in)
+            with torch.cuda.stream(s_in):  # under capture + select
+                d_tq.copy_(h_tq, non_blocking=True)
+            self.capture(dq, dk)
+            self.build_masks()
+            main.wait_stream(s_in)
+            self._attend_pipelined(None, d_tq, q, k, v, h_out, chunks)
+
+        key = ("step_host", chunks, h_dq.data_ptr(), h_tq.data_ptr(), h_out.data_ptr(), draft_k.data_ptr(),
+               target_k.data_ptr(), target_v.data_ptr())
+        self._graph(key, body).replay()
         return h_out
+
+    def _streams(self):
+        if getattr(self, "_copy_streams", None) is None:
+            self._copy_streams = (torch.cuda.Stream(device=self.device), torch.cuda.Stream(device=self.device))
+        return self._copy_streams
 
     # -- layouts ------------------------------------------------------------------
     def target_views(self, q, k, v):

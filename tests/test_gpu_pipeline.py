@@ -141,7 +141,7 @@ def test_host_buffer_api_matches_device_path(cuda_ok):
     h_out = torch.empty(want.shape, dtype=want.dtype).pin_memory()
     for _ in range(2):  # first call captures the graph, second replays it
         h_out.zero_()
-        step.step_host(dq.cpu().pin_memory(), dk, tq.cpu().pin_memory(), tk, tv, h_out)
+        step.step_host(dq.cpu().pin_memory(), dk, tq.cpu().pin_memory(), tk, tv, h_out, chunks=1)
         torch.cuda.synchronize()
         assert torch.equal(h_out, want.cpu())
     h_out.zero_()
@@ -160,3 +160,14 @@ def test_host_buffer_api_matches_device_path(cuda_ok):
             got.append(h_out.clone())
         assert torch.equal(got[0], got[1])
         torch.testing.assert_close(got[0].float(), want.cpu().float(), rtol=2e-2, atol=2e-2)
+    # the whole step with in-graph copies (target-Q H2D under capture + select,
+    # D2H per unit group): same masks, attention within tolerance, deterministic
+    h_dq = dq.cpu().pin_memory()
+    got = []
+    for _ in range(2):
+        h_out.zero_()
+        step.step_host(h_dq, dk, h_tq, tk, tv, h_out, chunks=2)
+        torch.cuda.synchronize()
+        got.append(h_out.clone())
+    assert torch.equal(got[0], got[1])
+    torch.testing.assert_close(got[0].float(), want.cpu().float(), rtol=2e-2, atol=2e-2)
