@@ -538,6 +538,8 @@ def run_sharded(args, world, rank, local):
     assert step.status.item() == 0, f"device status {step.status.item()}"
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     t_cap, t_sel, t_att, t_den = [], [], [], []
+    lib = _lib.load()
+    launches0 = lib.sts_launch_count()  # our kernels launched inside the timed loop (library counter)
     with ClockSampler(local) as clocks:
         for _ in range(args.steps):
             flush()
@@ -565,6 +567,7 @@ def run_sharded(args, world, rank, local):
             t_sel.append(e[1].elapsed_time(e[2]) * 1e3)
             t_att.append(e3.elapsed_time(e4) * 1e3)
             t_den.append(e5.elapsed_time(e6) * 1e3)
+    launches = int(lib.sts_launch_count() - launches0)
     # end to end through the public API: host Q in, host O out (every rank)
     h_tq, h_dq = tq.cpu().pin_memory(), dq.cpu().pin_memory()
     h_out = torch.empty(step.out.shape, dtype=step.out.dtype).pin_memory()
@@ -625,7 +628,7 @@ def run_sharded(args, world, rank, local):
         "cpu_baseline": None,
         "e2e": {"value": round(e2e, 2), "unit": "us", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "what": "ShardedVerifyStep.step per rank: H2D target+draft Q, capture, select, attention, merge, D2H"},
-        "gpu_launches": None,
+        "gpu_launches": launches,
         "clocks": clocks.summary(),
     }
     if rank == 0:
