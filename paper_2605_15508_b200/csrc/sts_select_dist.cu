@@ -119,13 +119,18 @@ __device__ __forceinline__ int digit_of(K key, int round) {
   return (int)((key >> (KB - DD_BITS * (round + 1))) & (K)(DD_BINS - 1));
 }
 
-// keys of the local positions + round-0 histogram; grid (chunks, rows)
+// keys of the local positions + round-0 histogram; a linear grid of
+// rows x chunks, ROW-fastest: the CTAs resident together cover the same
+// position chunk of every row, so a draft row mapped into several target rows
+// (mode S sums each target row's mapped draft rows) is read from HBM once and
+// from L2 for its other targets
 template <typename K>
 __global__ void __launch_bounds__(DIST_THREADS) dist_keys_kernel(DistParams p, int32_t* hist) {
   __shared__ uint32_t sh[DD_BINS];
-  const int64_t r = blockIdx.y;
+  const int64_t r = (int64_t)blockIdx.x % p.rows;
+  const int chunk = (int)((int64_t)blockIdx.x / p.rows);
   for (int i = threadIdx.x; i < DD_BINS; i += DIST_THREADS) sh[i] = 0;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (chunk == 0 && threadIdx.x == 0) {
     DistState s;
     s.prefix = 0;
     s.pmask = 0;
@@ -144,12 +149,12 @@ __global__ void __launch_bounds__(DIST_THREADS) dist_keys_kernel(DistParams p, i
   int32_t srcs[8];
   load_srcs(p, r, srcs);
   K* keys = reinterpret_cast<K*>(p.keys + r * p.keys_ld * sizeof(K));
-  const int j_end = min(nk, (int)(blockIdx.x + 1) * DIST_CHUNK);
+  const int j_end = min(nk, (chunk + 1) * DIST_CHUNK);
   if constexpr (sizeof(K) == 4) {
     if (p.vec4) {
       // 4 consecutive positions per thread: one 16-byte load per source row
       // (rows are padded to a multiple of 4), sources summed in order
-      for (int j = blockIdx.x * DIST_CHUNK + 4 * threadIdx.x; j < j_end; j += 4 * DIST_THREADS) {
+      for (int j = chunk * DIST_CHUNK + 4 * threadIdx.x; j < j_end; j += 4 * DIST_THREADS) {
         float4 v[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q)
@@ -177,7 +182,7 @@ __global__ void __launch_bounds__(DIST_THREADS) dist_keys_kernel(DistParams p, i
       return;
     }
   }
-  for (int j = blockIdx.x * DIST_CHUNK + threadIdx.x; j < j_end; j += DIST_THREADS) {
+  for (int j = chunk * DIST_CHUNK + threadIdx.x; j < j_end; j += DIST_THREADS) {
     K key;
     if constexpr (sizeof(K) == 4) {
       key = f32_key(dist_value(p, srcs, j));
@@ -744,8 +749,11 @@ extern "C" int sts_dist_select_begin(const sts_dist_rows* g, int32_t* hist_local
   STS_REQUIRE(hist_local_dev, STS_ERR_CONTRACT, "null histogram");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   STS_CUDA_CHECK(cudaMemsetAsync(hist_local_dev, 0, (size_t)p.rows * DD_BINS * 4, st));
-  if (p.page_size == 1) dist_keys_kernel<uint32_t><<<dist_grid(p), DIST_THREADS, 0, st>>>(p, hist_local_dev);
-  else dist_keys_kernel<uint64_t><<<dist_grid(p), DIST_THREADS, 0, st>>>(p, hist_local_dev);
+  const dim3 g2 = dist_grid(p);
+  STS_REQUIRE((int64_t)g2.x * g2.y < (int64_t(1) << 31), STS_ERR_CONTRACT, "rows x position chunks too large");
+  const unsigned lin = (unsigned)((int64_t)g2.x * g2.y);  // rows x chunks, row-fastest
+  if (p.page_size == 1) dist_keys_kernel<uint32_t><<<lin, DIST_THREADS, 0, st>>>(p, hist_local_dev);
+  else dist_keys_kernel<uint64_t><<<lin, DIST_THREADS, 0, st>>>(p, hist_local_dev);
   STS_LAUNCH_CHECK();
   return STS_OK;
 }
