@@ -90,7 +90,7 @@ class STSVerifyStep:
     """Preallocated GPU pipeline for one verify step (see module docstring)."""
 
     def __init__(self, shape: VerifyShape, sparsity: SparsityConfig, mapping_table, mode: str = "S",
-                 device=None, splits=None):
+                 device=None, splits=None, long_row_min=None):
         if mode not in ("S", "R"):
             raise ValueError("mode must be 'S' or 'R'")
         if shape.target_q_heads % shape.target_kv_heads or shape.draft_q_heads % shape.draft_kv_heads:
@@ -124,6 +124,16 @@ class STSVerifyStep:
             self.idx = torch.empty((s.target_units, self.idx_ld), dtype=torch.int32, device=dev)
             self.cnt = torch.empty((s.target_units,), dtype=torch.int32, device=dev)
             self.member = None
+            # long rows (>= long_row_min committed positions, default 64K): the
+            # chunk-parallel radix select of the sharded path at P = 1 (every
+            # pass spread over (row, chunk) CTAs) instead of one CTA per row
+            lr_min = int(os.environ.get("STS_LONG_ROW", "65536")) if long_row_min is None else int(long_row_min)
+            self._dist = None
+            if base >= lr_min and s.target_units <= 65535:
+                from .sharded import DistSelector
+
+                self._dist = DistSelector(s.target_units, s.n_kv, sparsity.page_size, 1, dev)
+                self._dist_k = self.budget if sparsity.page_size == 1 else -(-self.budget // sparsity.page_size)
         else:
             rows_total = s.batch * nd * R
             self.draft_rows = torch.zeros((rows_total, self.n_draft_cols), dtype=torch.float32, device=dev)
@@ -165,7 +175,14 @@ class STSVerifyStep:
     def build_masks(self, stream=None):
         """Stage 3: radix top-k selection (+ union for mode R)."""
         s, cfg = self.shape, self.cfg
-        if self.mode == "S":
+        if self.mode == "S" and self._dist is not None:
+            from .sharded import run_single
+
+            run_single(self._dist.protocol(
+                self.draft_rows, row_src=self.row_src, n_global=s.context, lo=0, k_top=self._dist_k, rank=0,
+                include_current=False, include_sink=cfg.include_sink, recent_window=cfg.recent_window,
+                tail_len=s.rows, n_kv_local=s.n_kv, idx=self.idx, cnt=self.cnt, status=self.status, stream=stream))
+        elif self.mode == "S":
             kernels.select_topk(self.draft_rows, row_src=self.row_src, n_common=s.context,
                                 budget=int(self.budget), page_size=cfg.page_size, include_current=False,
                                 include_sink=cfg.include_sink, recent_window=cfg.recent_window,

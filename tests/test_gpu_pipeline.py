@@ -51,8 +51,9 @@ def test_draft_capture_rows_match_reference_math(cuda_ok):
             np.testing.assert_array_equal(rows_s[u * G + hh, :base], mine)
 
 
-@pytest.mark.parametrize("ps,sink,win", [(1, False, 0), (16, True, 64)])
-def test_verify_step_mode_s(cuda_ok, ps, sink, win):
+@pytest.mark.parametrize("ps,sink,win,long_rows", [(1, False, 0, False), (16, True, 64, False), (1, False, 0, True),
+                                                   (16, True, 64, True), (1, True, 32, True)])
+def test_verify_step_mode_s(cuda_ok, ps, sink, win, long_rows):
     import torch
 
     from paper_2605_15508_b200 import SparsityConfig
@@ -61,7 +62,9 @@ def test_verify_step_mode_s(cuda_ok, ps, sink, win):
     s = _small_shape()
     cfg = SparsityConfig(budget=0.1, page_size=ps, include_sink=sink, recent_window=win)
     table = random_mapping_table(s, seed=1)
-    step = STSVerifyStep(s, cfg, table, mode="S")
+    # long_rows: the chunk-parallel (sharded-path, P = 1) select instead of one CTA per row
+    step = STSVerifyStep(s, cfg, table, mode="S", long_row_min=1 if long_rows else None)
+    assert (step._dist is not None) == long_rows
     dq, dk, tq, tk, tv = synthetic_inputs(s, "cuda", seed=3)
     q, k, v = step.target_views(tq, tk, tv)
     dqv, dkv = step.draft_views(dq, dk)
