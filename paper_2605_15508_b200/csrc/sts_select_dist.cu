@@ -119,6 +119,52 @@ __device__ __forceinline__ int digit_of(K key, int round) {
   return (int)((key >> (KB - DD_BITS * (round + 1))) & (K)(DD_BINS - 1));
 }
 
+// fp64 key of a FULL page of PS tokens held in registers: 16-byte loads of
+// every source (summed in fp32, source order), then the numpy reduceat
+// segment order x0 + pairwise(x[1:PS]) of dist_pairwise, unrolled
+template <int PS>
+__device__ __forceinline__ double page_sum_regs(const DistParams& p, const int32_t* srcs, int start) {
+  float x[PS];
+#pragma unroll
+  for (int t = 0; t < PS / 4; ++t) {
+    float4 a = *reinterpret_cast<const float4*>(p.scores + (int64_t)srcs[0] * p.ld + start + 4 * t);
+#pragma unroll
+    for (int q = 1; q < 8; ++q)
+      if (q < p.nsrc) {
+        const float4 v = *reinterpret_cast<const float4*>(p.scores + (int64_t)srcs[q] * p.ld + start + 4 * t);
+        a.x = __fadd_rn(a.x, v.x);
+        a.y = __fadd_rn(a.y, v.y);
+        a.z = __fadd_rn(a.z, v.z);
+        a.w = __fadd_rn(a.w, v.w);
+      }
+    x[4 * t] = a.x;
+    x[4 * t + 1] = a.y;
+    x[4 * t + 2] = a.z;
+    x[4 * t + 3] = a.w;
+  }
+  constexpr int n = PS - 1;  // pairwise over x[1 .. PS)
+  double res;
+  if constexpr (n < 8) {
+    res = 0.0;
+#pragma unroll
+    for (int i = 0; i < n; ++i) res = __dadd_rn(res, (double)x[1 + i]);
+  } else {
+    double r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = (double)x[1 + j];
+    constexpr int body = n - n % 8;
+#pragma unroll
+    for (int i = 8; i < body; i += 8)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = __dadd_rn(r[j], (double)x[1 + i + j]);
+    res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                    __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+#pragma unroll
+    for (int i = body; i < n; ++i) res = __dadd_rn(res, (double)x[1 + i]);
+  }
+  return __dadd_rn((double)x[0], res);
+}
+
 // keys of the local positions + round-0 histogram; a linear grid of
 // rows x chunks, ROW-fastest: the CTAs resident together cover the same
 // position chunk of every row, so a draft row mapped into several target rows
@@ -189,8 +235,14 @@ __global__ void __launch_bounds__(DIST_THREADS) dist_keys_kernel(DistParams p, i
     } else {
       const int start = j * p.page_size;
       const int len = min(p.page_size, nc - start);
-      const double x0 = (double)dist_value(p, srcs, start);
-      key = f64_key(len == 1 ? x0 : __dadd_rn(x0, dist_pairwise(p, srcs, start + 1, len - 1)));
+      if (p.vec4 && len == p.page_size && (p.page_size == 8 || p.page_size == 16 || p.page_size == 32)) {
+        key = f64_key(p.page_size == 16   ? page_sum_regs<16>(p, srcs, start)
+                      : p.page_size == 8  ? page_sum_regs<8>(p, srcs, start)
+                                          : page_sum_regs<32>(p, srcs, start));
+      } else {
+        const double x0 = (double)dist_value(p, srcs, start);
+        key = f64_key(len == 1 ? x0 : __dadd_rn(x0, dist_pairwise(p, srcs, start + 1, len - 1)));
+      }
     }
     keys[j] = key;
     atomicAdd(&sh[digit_of<K>(key, 0)], 1u);
