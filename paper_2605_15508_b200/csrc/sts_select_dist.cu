@@ -494,6 +494,53 @@ __device__ __forceinline__ void key_words(const uint32_t* keys, int nk, int64_t 
   }
 }
 
+// selected bit of local token j (its key's bitmap bit, or an extra)
+struct TokenSel {
+  const uint32_t* bits;
+  int ps, nc, lo, n_global, lo_extra;
+  bool sink, cur;
+  __device__ __forceinline__ bool operator()(int64_t j) const {
+    if (j >= nc) return false;
+    const int64_t k = ps == 1 ? j : j / ps;
+    const int g = lo + (int)j;
+    return ((bits[k >> 5] >> (k & 31)) & 1u) || g >= lo_extra || (sink && g == 0) || (cur && g == n_global - 1);
+  }
+};
+
+// bits of [a, b) inside the 32-token word starting at w0
+__device__ __forceinline__ uint32_t range_bits(int64_t a, int64_t b, int64_t w0) {
+  const int64_t l = max(a - w0, (int64_t)0), h = min(b - w0, (int64_t)32);
+  if (h <= l) return 0u;
+  return (h - l == 32 ? 0xffffffffu : ((1u << (h - l)) - 1u)) << l;
+}
+
+// token mode: the selected tokens of word w (bitmap word | extras), committed only
+__device__ __forceinline__ uint32_t token_word_from(const TokenSel& t, int64_t w, uint32_t key_word) {
+  const int64_t w0 = 32 * w;
+  if (w0 >= t.nc) return 0u;
+  uint32_t m = key_word | range_bits((int64_t)t.lo_extra - t.lo, t.nc, w0);
+  if (t.sink && t.lo == 0 && w == 0) m |= 1u;
+  if (t.cur) m |= range_bits((int64_t)t.n_global - 1 - t.lo, (int64_t)t.n_global - t.lo, w0);
+  return m & range_bits(0, t.nc, w0);
+}
+
+__device__ __forceinline__ uint32_t token_word(const TokenSel& t, int64_t w) {
+  return 32 * w >= t.nc ? 0u : token_word_from(t, w, t.bits[w]);
+}
+
+__device__ __forceinline__ TokenSel token_sel(const DistParams& p, const EmitParams& e, int64_t r) {
+  TokenSel t;
+  t.bits = e.bits + r * e.bits_ld;
+  t.ps = p.page_size;
+  t.nc = local_committed(p);
+  t.lo = p.lo;
+  t.n_global = p.n_global;
+  t.lo_extra = e.recent_window > 0 ? p.n_global - e.recent_window : p.n_global;
+  t.sink = (e.flags & STS_SEL_SINK) != 0;
+  t.cur = (e.flags & STS_SEL_CURRENT) != 0;
+  return t;
+}
+
 template <typename K>
 __global__ void __launch_bounds__(EMIT_THREADS) dist_emit_ties_kernel(DistParams p, EmitParams e) {
   __shared__ int red[EMIT_WARPS];
@@ -555,49 +602,17 @@ __global__ void __launch_bounds__(EMIT_THREADS) dist_emit_bits_kernel(DistParams
     }
   }
   if (valid) bits[word] = sel;
-}
-
-// selected bit of local token j (its key's bitmap bit, or an extra)
-struct TokenSel {
-  const uint32_t* bits;
-  int ps, nc, lo, n_global, lo_extra;
-  bool sink, cur;
-  __device__ __forceinline__ bool operator()(int64_t j) const {
-    if (j >= nc) return false;
-    const int64_t k = ps == 1 ? j : j / ps;
-    const int g = lo + (int)j;
-    return ((bits[k >> 5] >> (k & 31)) & 1u) || g >= lo_extra || (sink && g == 0) || (cur && g == n_global - 1);
+  if (p.page_size == 1) {
+    // token mode: key chunk == token chunk, so the selected-token count of the
+    // chunk (keys | extras) is known here and the count pass is skipped
+    const TokenSel ts = token_sel(p, e, r);
+    int c = __popc(token_word_from(ts, word, valid ? sel : 0u));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    int total;
+    warp_offsets(c, red, total);
+    if (threadIdx.x == 0) e.tok_cnt[r * e.tok_chunks + blockIdx.x] = total;
   }
-};
-
-// bits of [a, b) inside the 32-token word starting at w0
-__device__ __forceinline__ uint32_t range_bits(int64_t a, int64_t b, int64_t w0) {
-  const int64_t l = max(a - w0, (int64_t)0), h = min(b - w0, (int64_t)32);
-  if (h <= l) return 0u;
-  return (h - l == 32 ? 0xffffffffu : ((1u << (h - l)) - 1u)) << l;
-}
-
-// token mode: the selected tokens of word w (bitmap word | extras), committed only
-__device__ __forceinline__ uint32_t token_word(const TokenSel& t, int64_t w) {
-  const int64_t w0 = 32 * w;
-  if (w0 >= t.nc) return 0u;
-  uint32_t m = t.bits[w] | range_bits((int64_t)t.lo_extra - t.lo, t.nc, w0);
-  if (t.sink && t.lo == 0 && w == 0) m |= 1u;
-  if (t.cur) m |= range_bits((int64_t)t.n_global - 1 - t.lo, (int64_t)t.n_global - t.lo, w0);
-  return m & range_bits(0, t.nc, w0);
-}
-
-__device__ __forceinline__ TokenSel token_sel(const DistParams& p, const EmitParams& e, int64_t r) {
-  TokenSel t;
-  t.bits = e.bits + r * e.bits_ld;
-  t.ps = p.page_size;
-  t.nc = local_committed(p);
-  t.lo = p.lo;
-  t.n_global = p.n_global;
-  t.lo_extra = e.recent_window > 0 ? p.n_global - e.recent_window : p.n_global;
-  t.sink = (e.flags & STS_SEL_SINK) != 0;
-  t.cur = (e.flags & STS_SEL_CURRENT) != 0;
-  return t;
 }
 
 __global__ void __launch_bounds__(EMIT_THREADS) dist_emit_count_kernel(DistParams p, EmitParams e) {
@@ -876,8 +891,10 @@ extern "C" int sts_dist_select_finish(const sts_dist_rows* g, int32_t rank, int3
     dist_emit_bits_kernel<uint64_t><<<kgrid, EMIT_THREADS, 0, st>>>(p, e);
   }
   STS_LAUNCH_CHECK();
-  dist_emit_count_kernel<<<tgrid, EMIT_THREADS, 0, st>>>(p, e);
-  STS_LAUNCH_CHECK();
+  if (p.page_size > 1) {  // token mode: counted by the bits pass
+    dist_emit_count_kernel<<<tgrid, EMIT_THREADS, 0, st>>>(p, e);
+    STS_LAUNCH_CHECK();
+  }
   dist_emit_write_kernel<<<tgrid, EMIT_THREADS, 0, st>>>(p, e);
   STS_LAUNCH_CHECK();
   return STS_OK;
