@@ -182,6 +182,14 @@ STS_API int sts_draft_probs(int32_t dtype, const void* q_dev, const void* k_cach
                     int32_t n_keys, int32_t pos_offset, int32_t base, float scale,
                     const float* lse_dev, int32_t mode, float* out_dev, int64_t out_ld,
                     void* stream);
+/* Raw pre-softmax scores (ForwardRecord.scores / record_scores,
+ * src/toymodel.py:225-240, :351-352): out[(u*G+hh)*R + i][j] = scale * q.k_j
+ * (fp32, natural units) for local j with global position <= base+i; other
+ * entries are left untouched.  Same geometry as sts_draft_probs mode 1. */
+STS_API int sts_draft_scores(int32_t dtype, const void* q_dev, const void* k_cache_dev,
+                     int64_t kv_unit_stride, int64_t units, int32_t G, int32_t R, int32_t d,
+                     int32_t n_keys, int32_t pos_offset, int32_t base, float scale,
+                     float* out_dev, int64_t out_ld, void* stream);
 
 /* ------------------------------------------------------------------------
  * sts_lse_merge — merge P partial attention results (split-K or

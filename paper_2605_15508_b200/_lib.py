@@ -47,6 +47,8 @@ SIGNATURES = {
                                 _p, _p, _sz, _p]),
     "sts_draft_probs": (C.c_int, [_i32, _p, _p, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _i32, _f32,
                                   _p, _i32, _p, _i64, _p]),
+    "sts_draft_scores": (C.c_int, [_i32, _p, _p, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _i32, _f32,
+                                   _p, _i64, _p]),
     "sts_lse_merge": (C.c_int, [_p, _p, _i32, _i64, _i32, _i32, _p, _p, _p]),
     "sts_lse_merge_ptrs": (C.c_int, [_p, _i32, _i64, _i32, _i64, _i64, _i32, _p, _p, _p]),
     "sts_row_union": (C.c_int, [_p, _i64, _p, _p, _i64, _i32, _i32, _p, _p, _p, _i64, _p, _p, _p]),

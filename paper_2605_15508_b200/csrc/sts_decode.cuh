@@ -40,7 +40,7 @@ struct DecodeParams {
   const float* lse_in;  // [units][M] natural-log LSE
   float* probs_out;
   int64_t out_ld;
-  int probs_mode;       // 0: reduced over rows (mode S), 1: per row (mode R)
+  int probs_mode;       // 0: reduced over rows (mode S), 1: per row (mode R), 2: per-row raw logits
   int idx_cap;
   // stream-K bookkeeping (sts_stream.cu)
   int* counters;        // [units], zeroed before each launch

@@ -339,3 +339,24 @@ extern "C" int sts_draft_probs(int32_t dtype, const void* q_dev, const void* k_c
   p.probs_mode = mode;
   return stream_launch(MODE_PROBS, p, nullptr, 0, st);
 }
+
+extern "C" int sts_draft_scores(int32_t dtype, const void* q_dev, const void* k_cache_dev,
+                                int64_t kv_unit_stride, int64_t units, int32_t G, int32_t R,
+                                int32_t d, int32_t n_keys, int32_t pos_offset, int32_t base,
+                                float scale, float* out_dev, int64_t out_ld, void* stream) {
+  STS_REQUIRE(dtype == STS_DTYPE_BF16, STS_ERR_CONTRACT, "draft scores run in bf16");
+  STS_REQUIRE(units >= 0 && G >= 1 && R >= 1 && n_keys >= 0, STS_ERR_CONTRACT, "bad draft shape");
+  STS_REQUIRE(units <= 65535, STS_ERR_CONTRACT, "units must be <= 65535");
+  STS_REQUIRE(q_dev && k_cache_dev && out_dev, STS_ERR_CONTRACT, "null buffer");
+  STS_REQUIRE(out_ld >= n_keys, STS_ERR_CONTRACT, "out_ld must be >= n_keys");
+  if (units == 0) return STS_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  DecodeParams p;
+  draft_params(p, q_dev, k_cache_dev, kv_unit_stride, units, G, R, d, n_keys, pos_offset, base, scale);
+  p.splits = 1;
+  p.lse_in = nullptr;
+  p.probs_out = out_dev;
+  p.out_ld = out_ld;
+  p.probs_mode = 2;
+  return stream_launch(MODE_PROBS, p, nullptr, 0, st);
+}

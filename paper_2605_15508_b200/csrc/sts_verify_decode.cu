@@ -361,8 +361,8 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
       qa[kk][3] = okB ? __ldg(qB + kk * 8 + 4) : 0u;
     }
     if constexpr (MODE == MODE_PROBS) {
-      lse2A = okA ? p.lse_in[u * M + rA] * LOG2E : 0.f;
-      lse2B = okB ? p.lse_in[u * M + rB] * LOG2E : 0.f;
+      lse2A = okA && p.lse_in ? p.lse_in[u * M + rA] * LOG2E : 0.f;  // (raw-logit mode: no LSE)
+      lse2B = okB && p.lse_in ? p.lse_in[u * M + rB] * LOG2E : 0.f;
     }
   };
 
@@ -520,14 +520,24 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
       // (mode R) or summed over each head's speculative rows in row order
       // (mode S, committed positions only); one thread per key, no divides
       constexpr int KPS = L::KPS;
+      if (p.probs_mode == 2) {  // raw logits q.k * scale (ForwardRecord.scores), natural units
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const int key = nt * 8 + 2 * (lane & 3);
-        *reinterpret_cast<float2*>(s_prob + rA * KPS + key) =
-            make_float2(fast_exp2(s[nt][0] - lse2A), fast_exp2(s[nt][1] - lse2A));
-        if (rB_live)
-          *reinterpret_cast<float2*>(s_prob + rB * KPS + key) =
-              make_float2(fast_exp2(s[nt][2] - lse2B), fast_exp2(s[nt][3] - lse2B));
+        for (int nt = 0; nt < NT; ++nt) {
+          const int key = nt * 8 + 2 * (lane & 3);
+          *reinterpret_cast<float2*>(s_prob + rA * KPS + key) = make_float2(s[nt][0] * LN2, s[nt][1] * LN2);
+          if (rB_live)
+            *reinterpret_cast<float2*>(s_prob + rB * KPS + key) = make_float2(s[nt][2] * LN2, s[nt][3] * LN2);
+        }
+      } else {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int key = nt * 8 + 2 * (lane & 3);
+          *reinterpret_cast<float2*>(s_prob + rA * KPS + key) =
+              make_float2(fast_exp2(s[nt][0] - lse2A), fast_exp2(s[nt][1] - lse2A));
+          if (rB_live)
+            *reinterpret_cast<float2*>(s_prob + rB * KPS + key) =
+                make_float2(fast_exp2(s[nt][2] - lse2B), fast_exp2(s[nt][3] - lse2B));
+        }
       }
       __syncthreads();
       const int R = p.rows_per_head;

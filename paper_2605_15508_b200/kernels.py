@@ -255,6 +255,22 @@ def draft_probs(q: torch.Tensor, k_cache: torch.Tensor, lse: torch.Tensor, *, G:
     return out
 
 
+def draft_scores(q: torch.Tensor, k_cache: torch.Tensor, *, G: int, R: int, base: int, n_keys=None,
+                 pos_offset: int = 0, scale=None, out=None, stream=None):
+    """Raw draft scores (the reference's ForwardRecord.scores, src/toymodel.py:
+    225-240, :351-352): [U*G*R, ld] fp32 rows of scale * q.k, row i valid up to
+    global position base+i (the rest stays as allocated: zeros by default)."""
+    _require_cuda(q, k_cache)
+    U, GR, d = q.shape
+    n_keys = k_cache.shape[1] if n_keys is None else int(n_keys)
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    if out is None:
+        out = torch.zeros((U * GR, n_keys), dtype=torch.float32, device=q.device)
+    call("sts_draft_scores", STS_DTYPE[q.dtype], ptr(q.contiguous()), ptr(k_cache), k_cache.stride(0), U, G, R, d,
+         n_keys, pos_offset, base, scale, ptr(out), out.stride(0), stream_handle(stream))
+    return out
+
+
 def lse_merge(o_parts: torch.Tensor | None, lse_parts: torch.Tensor, *, out_dtype=torch.float32,
               out=None, lse_out=None, stream=None):
     """Merge P partial attention results: o_parts [P, rows, d] fp32 (or None),

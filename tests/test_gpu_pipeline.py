@@ -51,6 +51,35 @@ def test_draft_capture_rows_match_reference_math(cuda_ok):
             np.testing.assert_array_equal(rows_s[u * G + hh, :base], mine)
 
 
+def test_draft_raw_scores_match_reference_math(cuda_ok):
+    """sts_draft_scores = the reference's ForwardRecord.scores (raw q.k/sqrt(d)
+    per speculative row over its causal prefix; src/toymodel.py:225-240,
+    :351-352) on the same bf16-rounded q/K, and softmax of it = the captured
+    probabilities."""
+    import torch
+
+    from paper_2605_15508_b200 import kernels
+
+    rng = np.random.default_rng(7)
+    U, G, R, d, base = 2, 4, 5, 64, 700
+    N = base + R
+    q = torch.from_numpy(rng.standard_normal((U, G * R, d)).astype(np.float32)).bfloat16().cuda()
+    k = torch.from_numpy(rng.standard_normal((U, N, d)).astype(np.float32)).bfloat16().cuda()
+    raw = kernels.draft_scores(q, k, G=G, R=R, base=base).cpu().numpy()
+    lse = kernels.draft_lse(q, k, G=G, R=R, base=base)
+    probs = kernels.draft_probs(q, k, lse, G=G, R=R, base=base, mode="R").cpu().numpy()
+    qf, kf = q.double().cpu().numpy(), k.double().cpu().numpy()
+    for u in range(U):
+        for m in range(G * R):
+            i = m % R
+            row = (u * G * R) + m
+            want = kf[u, : base + i + 1] @ qf[u, m] / np.sqrt(d)
+            np.testing.assert_allclose(raw[row, : base + i + 1], want, rtol=1e-4, atol=1e-4)
+            assert not raw[row, base + i + 1 :].any()  # beyond the row's prefix: untouched
+            sm = np.exp(want - want.max())
+            np.testing.assert_allclose(probs[row, : base + i + 1], sm / sm.sum(), rtol=1e-3, atol=1e-7)
+
+
 @pytest.mark.parametrize("ps,sink,win,long_rows", [(1, False, 0, False), (16, True, 64, False), (1, False, 0, True),
                                                    (16, True, 64, True), (1, True, 32, True)])
 def test_verify_step_mode_s(cuda_ok, ps, sink, win, long_rows):
