@@ -252,10 +252,12 @@ STS_API int sts_bitset_overlap(const uint32_t* a_dev, int32_t Ta, const uint32_t
  *
  *   begin(g, hist)                                   local keys + digit-0 hist
  *   for r in 0 .. sts_dist_select_rounds(ps)-1:
- *       hist_g = allreduce_sum(hist)                 (NCCL, int32 [rows][256])
+ *       hist_g = allreduce_sum(hist)                 (NCCL, int32 [rows][2048])
  *       round(g, r, hist_g, hist, r == last ? ties : NULL)
  *   ties_all = allgather(ties)                       (int32 [P][rows])
  *   finish(g, rank, P, ties_all, ...)                local index lists
+ * Digits are 11 bits from the top (the last one takes the rest): 3 rounds
+ * for fp32 token keys, 6 for fp64 page keys.
  *
  * Output: ascending LOCAL offsets (global = lo + offset) of the selected
  * committed positions, the extras (sink = global 0, recent window, current =
@@ -275,7 +277,7 @@ typedef struct sts_dist_rows {
   int32_t page_size;
 } sts_dist_rows;
 
-#define STS_DIST_BINS 256
+#define STS_DIST_BINS 2048
 
 STS_API int32_t sts_dist_select_rounds(int32_t page_size);
 STS_API size_t sts_dist_select_workspace_bytes(int64_t rows, int32_t n_local, int32_t page_size);

@@ -392,17 +392,28 @@ def fp32_order_keys(x) -> np.ndarray:
 # 5. sequence-sharded radix-select protocol (restates csrc/sts_select_dist.cu)
 # ---------------------------------------------------------------------------
 
-DIST_BITS = 8
+DIST_BITS = 11  # digit width (the last digit takes the remaining bits)
+
+
+def dist_digits(kbits: int = 32):
+    """(shift, width) of each radix round, from the top (csrc/sts_select_dist.cu dd_*)."""
+    out, top = [], kbits
+    while top > 0:
+        w = min(DIST_BITS, top)
+        out.append((top - w, w))
+        top -= w
+    return out
 
 
 def dist_select_protocol(values_local, lo: int, n_global: int, k: int, rank: int, nranks: int, torch_mod=None):
     """One rank of the sharded top-k protocol, in numpy, yielding the same
     collective requests as paper_2605_15508_b200.sharded.DistSelector
-    (("all_reduce_sum", int32 tensor [rows][256]), ("all_gather", ties [rows],
+    (("all_reduce_sum", int32 tensor [rows][2048]), ("all_gather", ties [rows],
     ties_all [P][rows])).  Returns the selected GLOBAL indices per row
     (ascending).  ``values_local``: fp32 [rows, n_local] at global positions
-    lo.. ; positions >= n_global are ignored.  Token mode, fp32 keys, 8-bit
-    digits from the top; the threshold/tie rule of topk_indices (src/numkit.py:74-86)."""
+    lo.. ; positions >= n_global are ignored.  Token mode, fp32 keys, 11-bit
+    digits from the top (11 + 11 + 10); the threshold/tie rule of topk_indices
+    (src/numkit.py:74-86)."""
     import torch
 
     vals = np.asarray(values_local, dtype=np.float32)
@@ -415,15 +426,15 @@ def dist_select_protocol(values_local, lo: int, n_global: int, k: int, rank: int
     dense = k >= n_global
     done = np.full(rows, dense, bool)
     ties_local = np.zeros(rows, np.int64)
-    for rnd in range(32 // DIST_BITS):
-        shift = 32 - DIST_BITS * (rnd + 1)
+    for shift, width in dist_digits(32):
+        nb = 1 << width
         hist = np.zeros((rows, 1 << DIST_BITS), np.int64)
         for r in range(rows):
             if done[r]:
                 continue
             m = (keys[r] & pmask[r]) == prefix[r]
-            d = ((keys[r][m] >> np.uint64(shift)) & np.uint64(0xFF)).astype(np.int64)
-            hist[r] = np.bincount(d, minlength=256)
+            d = ((keys[r][m] >> np.uint64(shift)) & np.uint64(nb - 1)).astype(np.int64)
+            hist[r, :nb] = np.bincount(d, minlength=nb)
         h_local = hist.copy()
         t = torch.from_numpy(hist.astype(np.int32))
         yield ("all_reduce_sum", t)
@@ -432,13 +443,13 @@ def dist_select_protocol(values_local, lo: int, n_global: int, k: int, rank: int
             if done[r]:
                 continue
             acc = 0
-            for digit in range(255, -1, -1):
+            for digit in range(nb - 1, -1, -1):
                 c = int(hg[r, digit])
                 if acc < krem[r] <= acc + c:
                     break
                 acc += c
             prefix[r] |= np.uint64(digit) << np.uint64(shift)
-            pmask[r] |= np.uint64(0xFF) << np.uint64(shift)
+            pmask[r] |= np.uint64(nb - 1) << np.uint64(shift)
             krem[r] -= acc
             if shift == 0 or krem[r] == c:
                 done[r] = True

@@ -62,7 +62,7 @@ SIGNATURES = {
                                          _p]),
 }
 
-STS_DIST_BINS = 256
+STS_DIST_BINS = 2048
 
 
 class DistRows(C.Structure):

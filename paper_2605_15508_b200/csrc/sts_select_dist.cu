@@ -19,7 +19,7 @@
 //            of them in index order — plus the extras and the in-block tail,
 //            as ascending LOCAL offsets.
 //
-// Digits are 8 bits from the top (4 rounds for token keys, 8 for page keys);
+// Digits are 11 bits from the top (3 rounds for token keys, 6 for page keys);
 // a row whose chosen bin is taken whole (remaining k == bin count) is resolved
 // early and skips the remaining rounds' work.  Collectives stay O(rounds + 1)
 // for all rows of all layers at once (one histogram buffer per round).
@@ -28,8 +28,18 @@
 namespace sts {
 namespace {
 
-constexpr int DD_BITS = 8;
-constexpr int DD_BINS = 1 << DD_BITS;
+// digits of DD_BITS from the top; the last digit takes the remaining bits
+// (32-bit keys: 11 + 11 + 10, 64-bit page keys: 5 x 11 + 9)
+constexpr int DD_BITS = 11;
+constexpr int DD_BINS = 1 << DD_BITS;  // histogram row stride (bins of the widest digit)
+
+__host__ __device__ constexpr int dd_rounds(int kbits) { return (kbits + DD_BITS - 1) / DD_BITS; }
+__host__ __device__ constexpr int dd_shift(int kbits, int round) {
+  return kbits - DD_BITS * (round + 1) > 0 ? kbits - DD_BITS * (round + 1) : 0;
+}
+__host__ __device__ constexpr int dd_width(int kbits, int round) {
+  return kbits - DD_BITS * round < DD_BITS ? kbits - DD_BITS * round : DD_BITS;
+}
 constexpr int DIST_THREADS = 512;
 constexpr int DIST_CHUNK = 8192;      // keys per CTA in the key / histogram passes
 
@@ -116,7 +126,7 @@ __device__ __forceinline__ int local_keys(const DistParams& p) {
 template <typename K>
 __device__ __forceinline__ int digit_of(K key, int round) {
   constexpr int KB = sizeof(K) * 8;
-  return (int)((key >> (KB - DD_BITS * (round + 1))) & (K)(DD_BINS - 1));
+  return (int)((key >> dd_shift(KB, round)) & (K)((1 << dd_width(KB, round)) - 1));
 }
 
 // fp64 key of a FULL page of PS tokens held in registers: 16-byte loads of
@@ -298,14 +308,11 @@ __global__ void dist_advance_kernel(DistParams p, int round, const int32_t* hist
   DistState st = p.state[r];
   if (st.done) return;
   const int32_t* hg = hist_global + r * DD_BINS;
-  // lane owns bins 255-8*lane .. 248-8*lane (descending)
-  int cnt[8];
+  // lane owns PER consecutive bins, descending: nb-1-PER*lane .. nb-PER-PER*lane
+  const int nb = 1 << dd_width(KB, round);
+  const int per = nb / 32;  // widths >= 9 bits: >= 16 bins per lane
   int lsum = 0;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    cnt[q] = hg[DD_BINS - 1 - 8 * lane - q];
-    lsum += cnt[q];
-  }
+  for (int q = 0; q < per; ++q) lsum += hg[nb - 1 - per * lane - q];
   int incl = lsum;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -318,18 +325,18 @@ __global__ void dist_advance_kernel(DistParams p, int round, const int32_t* hist
   if (who == 0) return;  // inconsistent histogram (cannot happen): leave the row unresolved
   if (lane != __ffs(who) - 1) return;
   int acc = excl, digit = 0, inbin = 0;
-#pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    if (acc < st.krem && st.krem <= acc + cnt[q]) {
-      digit = DD_BINS - 1 - 8 * lane - q;
-      inbin = cnt[q];
+  for (int q = 0; q < per; ++q) {
+    const int c = hg[nb - 1 - per * lane - q];
+    if (acc < st.krem && st.krem <= acc + c) {
+      digit = nb - 1 - per * lane - q;
+      inbin = c;
       break;
     }
-    acc += cnt[q];
+    acc += c;
   }
-  const int shift = KB - DD_BITS * (round + 1);
+  const int shift = dd_shift(KB, round);
   st.prefix |= (uint64_t)digit << shift;
-  st.pmask |= (uint64_t)(DD_BINS - 1) << shift;
+  st.pmask |= (uint64_t)(nb - 1) << shift;
   st.krem -= acc;
   if (shift == 0 || st.krem == inbin) {
     st.done = 1;
@@ -801,7 +808,7 @@ __global__ void dist_ties_kernel(const DistState* state, int64_t rows, int32_t* 
 
 using namespace sts;
 
-extern "C" int32_t sts_dist_select_rounds(int32_t page_size) { return page_size == 1 ? 4 : 8; }
+extern "C" int32_t sts_dist_select_rounds(int32_t page_size) { return page_size == 1 ? dd_rounds(32) : dd_rounds(64); }
 
 extern "C" size_t sts_dist_select_workspace_bytes(int64_t rows, int32_t n_local, int32_t page_size) {
   return dist_ws_bytes(rows, n_local, page_size < 1 ? 1 : page_size);

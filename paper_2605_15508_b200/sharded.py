@@ -8,7 +8,7 @@ step then runs, on every rank, with only three kinds of exchange:
   capture   local draft LSE per row -> all-gather (P x rows floats) ->
             global LSE (sts_lse_merge, LSE only) -> local probability rows
   select    global top-k threshold by radix rounds over an all-reduced
-            histogram (int32 [rows][256] per round, every (layer, head) row at
+            histogram (int32 [rows][2048] per round, every (layer, head) row at
             once) + one all-gather of per-rank tie counts, so the union of the
             ranks' selections is bit-exactly the single-GPU selection of the
             concatenated row (ties to the lowest GLOBAL index,

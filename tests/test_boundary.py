@@ -79,7 +79,7 @@ def test_host_validation_without_gpu():
     with pytest.raises(ConfigError, match="k must be"):
         _lib.call("sts_dist_select_begin", ctypes.addressof(g), 8, 8, 1 << 30, None)
     lib = _lib.load()
-    assert lib.sts_dist_select_rounds(1) == 4 and lib.sts_dist_select_rounds(16) == 8
+    assert lib.sts_dist_select_rounds(1) == 3 and lib.sts_dist_select_rounds(16) == 6
     assert lib.sts_dist_select_workspace_bytes(256, 131072, 1) >= 256 * 131072 * 4
 
 
