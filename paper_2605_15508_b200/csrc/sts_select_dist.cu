@@ -41,7 +41,10 @@ __host__ __device__ constexpr int dd_width(int kbits, int round) {
   return kbits - DD_BITS * round < DD_BITS ? kbits - DD_BITS * round : DD_BITS;
 }
 constexpr int DIST_THREADS = 512;
-constexpr int DIST_CHUNK = 8192;      // keys per CTA in the key / histogram passes
+#ifndef STS_DIST_CHUNK
+#define STS_DIST_CHUNK 32768
+#endif
+constexpr int DIST_CHUNK = STS_DIST_CHUNK;  // keys per CTA in the key / histogram passes
 
 struct DistState {
   uint64_t prefix;  // chosen digits so far (in key space)
