@@ -124,15 +124,15 @@ class STSVerifyStep:
             self.idx = torch.empty((s.target_units, self.idx_ld), dtype=torch.int32, device=dev)
             self.cnt = torch.empty((s.target_units,), dtype=torch.int32, device=dev)
             self.member = None
-            # long token rows (>= long_row_min committed positions, default
-            # 64K): the chunk-parallel radix select of the sharded path at P = 1
-            # (every pass spread over (row, chunk) CTAs) instead of one CTA per
-            # row.  Measured: c3 980 -> 840 us; c2 (32K) 63 -> 105 us and page
-            # keys (8 rounds of 64-bit digits) 1380 -> 2780 us at c3, so those
-            # stay on select_kernel
+            # long rows (>= long_row_min committed positions, default 64K): the
+            # chunk-parallel radix select of the sharded path at P = 1 (every
+            # pass spread over (row, chunk) CTAs) instead of one CTA per row.
+            # Measured (tools/select_route_ab.py): c3 token 973 -> 796 us, c3
+            # page 16 1376 -> 1218 us; at c2 (32K) select_kernel stays faster
+            # (token 63 vs 105 us, page 16 112 vs 177 us)
             lr_min = int(os.environ.get("STS_LONG_ROW", "65536")) if long_row_min is None else int(long_row_min)
             self._dist = None
-            if base >= lr_min and s.target_units <= 65535 and (sparsity.page_size == 1 or long_row_min is not None):
+            if base >= lr_min and s.target_units <= 65535:
                 from .sharded import DistSelector
 
                 self._dist = DistSelector(s.target_units, s.n_kv, sparsity.page_size, 1, dev)
