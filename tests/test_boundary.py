@@ -81,6 +81,16 @@ def test_host_validation_without_gpu():
     lib = _lib.load()
     assert lib.sts_dist_select_rounds(1) == 3 and lib.sts_dist_select_rounds(16) == 6
     assert lib.sts_dist_select_workspace_bytes(256, 131072, 1) >= 256 * 131072 * 4
+    # the oracle's restatement of the protocol uses the same digits (top-down,
+    # widths <= STS_DIST_BINS bins, covering every key bit once)
+    from oracle.sts_oracle import dist_digits
+
+    for kbits, ps in ((32, 1), (64, 16)):
+        dg = dist_digits(kbits)
+        assert len(dg) == lib.sts_dist_select_rounds(ps)
+        assert sum(w for _, w in dg) == kbits and dg[-1][0] == 0
+        assert all(1 << w <= _lib.STS_DIST_BINS for _, w in dg)
+        assert [sh for sh, _ in dg] == sorted((sh for sh, _ in dg), reverse=True)
 
 
 def test_sparsity_config_mirrors_reference():
