@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define STS_ABI_VERSION 2
+#define STS_ABI_VERSION 3
 
 #define STS_OK 0
 #define STS_ERR_INPUT 1
@@ -56,6 +56,8 @@ extern "C" {
 #define STS_DEV_IDX_CAPACITY 0x1 /* an index list exceeded idx_ld           */
 #define STS_DEV_EMPTY_ROW 0x2    /* a query row had no admissible key       */
 #define STS_DEV_BAD_INDEX 0x4    /* an index was outside the cached context */
+#define STS_DEV_SELECT_INCONSISTENT 0x8 /* sharded select: the global histogram did not
+                                           resolve a row (ranks disagree on k / shards) */
 
 STS_API const char* sts_last_error(void);
 STS_API int sts_abi_version(void);
@@ -122,11 +124,20 @@ STS_API int sts_page_aggregate(const float* scores_dev, int64_t ld, int64_t rows
  *   = softmax_S(q.k*scale) V ; lse_dev[u][M] = natural
  *   log-sum-exp of the scaled scores (nullable).  dtype F32 computes in fp32
  *   on CUDA cores (parity path); BF16 uses tensor cores with fp32 accumulate.
+ *   splits: F32 -> split-K factor (>= 1, partials merged by sts_lse_merge);
+ *   BF16 -> work schedule: 0 auto (one thread-block cluster per unit when
+ *   the key streams are short, else persistent stream-K), 1 stream-K,
+ *   2/3/4/6/8 clusters of exactly that many CTAs per unit (DSMEM merge).
  * ---------------------------------------------------------------------- */
 STS_API size_t sts_sparse_decode_workspace_bytes(int64_t units, int32_t M, int32_t d, int32_t splits);
 /* split-K factor that fills 148 SMs x 2 CTAs in whole waves (>= 8 key tiles
  * of 16 per CTA); what the host uses when it has no better knowledge. */
 STS_API int32_t sts_auto_splits(int64_t units, int64_t keys_per_unit);
+/* the BF16 work schedule sts_sparse_decode resolves for `schedule` (0 = auto)
+ * with these sizes: 1 = stream-K, C >= 2 = clusters of C CTAs; 0 if the shape
+ * is unsupported.  Launches nothing. */
+STS_API int32_t sts_sparse_decode_schedule(int64_t units, int32_t M, int32_t d, int64_t keys_per_unit,
+                                           int32_t schedule);
 STS_API int sts_sparse_decode(int32_t dtype, int32_t out_dtype, const void* q_dev, const void* k_cache_dev,
                       const void* v_cache_dev, int64_t kv_unit_stride, int64_t kv_row_stride, int64_t units,
                       int32_t M, int32_t d, const int32_t* idx_dev, int64_t idx_ld,
@@ -257,7 +268,10 @@ STS_API int sts_bitset_overlap(const uint32_t* a_dev, int32_t Ta, const uint32_t
  *   ties_all = allgather(ties)                       (int32 [P][rows])
  *   finish(g, rank, P, ties_all, ...)                local index lists
  * Digits are 11 bits from the top (the last one takes the rest): 3 rounds
- * for fp32 token keys, 6 for fp64 page keys.
+ * for fp32 token keys, 6 for fp64 page keys.  With P = 1, hist_g may be the
+ * same buffer as hist (no copy, no collective).  A row the global histogram
+ * cannot resolve (ranks disagree on k_top / n_global / shard geometry) sets
+ * STS_DEV_SELECT_INCONSISTENT in finish's status word.
  *
  * Output: ascending LOCAL offsets (global = lo + offset) of the selected
  * committed positions, the extras (sink = global 0, recent window, current =
@@ -280,6 +294,8 @@ typedef struct sts_dist_rows {
 #define STS_DIST_BINS 2048
 
 STS_API int32_t sts_dist_select_rounds(int32_t page_size);
+/* histogram bins per radix round (the width of hist_local/hist_global rows) */
+STS_API int32_t sts_dist_select_bins(void);
 STS_API size_t sts_dist_select_workspace_bytes(int64_t rows, int32_t n_local, int32_t page_size);
 STS_API int sts_dist_select_begin(const sts_dist_rows* g, int32_t* hist_local_dev, void* workspace_dev,
                                   size_t workspace_bytes, void* stream);

@@ -326,11 +326,19 @@ def block_attention(q_rows, keys, values, idx, causal_base=None, rows_per_head=1
     <= r % rows_per_head) and (member is None or bit r of member[j]).
     Returns (out fp64 (M, d), lse fp64 (M,)).
     """
+    idx = np.asarray(idx, dtype=np.int64)
+    return block_attention_rows(q_rows, np.asarray(keys)[idx], np.asarray(values)[idx], idx, causal_base,
+                                rows_per_head, member)
+
+
+def block_attention_rows(q_rows, k_sel, v_sel, positions, causal_base=None, rows_per_head=1, member=None):
+    """block_attention over already-gathered key/value rows: k_sel[j], v_sel[j]
+    sit at cache position positions[j] (the causal test uses the positions)."""
     q = np.asarray(q_rows, dtype=np.float64)
     M, d = q.shape
-    idx = np.asarray(idx, dtype=np.int64)
-    k = np.asarray(keys, dtype=np.float64)[idx]
-    v = np.asarray(values, dtype=np.float64)[idx]
+    idx = np.asarray(positions, dtype=np.int64)
+    k = np.asarray(k_sel, dtype=np.float64)
+    v = np.asarray(v_sel, dtype=np.float64)
     s = (q @ k.T) / math.sqrt(d)
     allowed = np.ones_like(s, dtype=bool)
     r = np.arange(M)

@@ -23,6 +23,8 @@ STS_SEL_SINK = 0x2
 STS_DEV_IDX_CAPACITY = 0x1
 STS_DEV_EMPTY_ROW = 0x2
 STS_DEV_BAD_INDEX = 0x4
+STS_DEV_SELECT_INCONSISTENT = 0x8
+ABI_VERSION = 3
 
 _i32, _i64, _u32, _f32, _f64 = C.c_int32, C.c_int64, C.c_uint32, C.c_float, C.c_double
 _p, _sz = C.c_void_p, C.c_size_t
@@ -38,6 +40,7 @@ SIGNATURES = {
     "sts_page_aggregate": (C.c_int, [_p, _i64, _i64, _p, _i32, _i32, _p, _i64, _p]),
     "sts_sparse_decode_workspace_bytes": (_sz, [_i64, _i32, _i32, _i32]),
     "sts_auto_splits": (_i32, [_i64, _i64]),
+    "sts_sparse_decode_schedule": (_i32, [_i64, _i32, _i32, _i64, _i32]),
     "sts_sparse_decode": (C.c_int, [_i32, _i32, _p, _p, _p, _i64, _i64, _i64, _i32, _i32, _p, _i64, _p, _i32, _p,
                                     _i32, _i32, _i32, _f32, _p, _p, _i32, _p, _p, _sz, _p]),
     "sts_sparse_prefill": (C.c_int, [_i32, _i32, _p, _p, _p, _i64, _i64, _i64, _i32, _i32, _i32, _p, _i64, _p,
@@ -55,6 +58,7 @@ SIGNATURES = {
     "sts_topk_bitsets": (C.c_int, [_p, _i64, _p, _i64, _i32, _p, _p]),
     "sts_bitset_overlap": (C.c_int, [_p, _i32, _p, _i32, _i64, _p, _p]),
     "sts_dist_select_rounds": (_i32, [_i32]),
+    "sts_dist_select_bins": (_i32, []),
     "sts_dist_select_workspace_bytes": (_sz, [_i64, _i32, _i32]),
     "sts_dist_select_begin": (C.c_int, [_p, _p, _p, _sz, _p]),
     "sts_dist_select_round": (C.c_int, [_p, _i32, _p, _p, _p, _p, _sz, _p]),
@@ -104,6 +108,13 @@ def load(build_if_missing: bool = False):
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    # a stale build would run a different protocol from this binding: refuse it
+    if lib.sts_abi_version() != ABI_VERSION:
+        raise ImportError(f"{LIB_PATH}: ABI {lib.sts_abi_version()} != {ABI_VERSION}; rebuild "
+                          "(python -m paper_2605_15508_b200.build)")
+    if lib.sts_dist_select_bins() != STS_DIST_BINS:
+        raise ImportError(f"{LIB_PATH}: sharded select uses {lib.sts_dist_select_bins()} bins, binding expects "
+                          f"{STS_DIST_BINS}; rebuild")
     _LIB = lib
     return lib
 

@@ -53,14 +53,36 @@ def nvcc_path() -> str:
     raise RuntimeError("nvcc not found: cannot build libsts_b200.so")
 
 
+def _compile_all(out: Path, extra: list[str], verbose: bool = False) -> None:
+    """nvcc every .cu to an object in parallel (one process per file), then link."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    objdir = LIBDIR / "obj" / out.stem
+    objdir.mkdir(parents=True, exist_ok=True)
+    cflags = [f for f in NVCC_FLAGS if f != "-shared"]
+    srcs = sorted(CSRC.glob("*.cu"))
+
+    def one(src: Path) -> Path:
+        obj = objdir / (src.stem + ".o")
+        cmd = [nvcc_path(), *cflags, *extra, "-c", "-o", str(obj), str(src)]
+        if verbose:
+            cmd.insert(1, "-Xptxas=-v")
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
+        objs = list(ex.map(one, srcs))
+    subprocess.run([nvcc_path(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(out),
+                    *[str(o) for o in objs]], check=True)
+
+
 def build_variant(name: str, defines: list[str]) -> Path:
     """Tuning aid: build a copy of the library with extra -D flags into
     _lib/variants/libsts_b200_<name>.so (select it with STS_B200_LIB)."""
     out = LIBDIR / "variants" / f"libsts_b200_{name}.so"
     out.parent.mkdir(parents=True, exist_ok=True)
-    cmd = [nvcc_path(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", str(out),
-           *[str(p) for p in sorted(CSRC.glob("*.cu"))]]
-    subprocess.run(cmd, check=True)
+    _compile_all(out, [f"-D{d}" for d in defines])
     return out
 
 
@@ -70,11 +92,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         return LIB
     LIBDIR.mkdir(exist_ok=True)
     tmp = LIBDIR / "libsts_b200.so.tmp"
-    cmd = [nvcc_path(), *NVCC_FLAGS, "-o", str(tmp), *[str(p) for p in sorted(CSRC.glob("*.cu"))]]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.run(cmd, check=True)
+    _compile_all(tmp, [], verbose)
     tmp.replace(LIB)
     STAMP.write_text(digest)
     return LIB

@@ -42,22 +42,18 @@ struct DecodeParams {
   int64_t out_ld;
   int probs_mode;       // 0: reduced over rows (mode S), 1: per row (mode R), 2: per-row raw logits
   int idx_cap;
-  // stream-K bookkeeping (sts_stream.cu)
-  int* counters;        // [units], zeroed before each launch
-  // verify kernels: sched[0] = dynamic chunk counter (zeroed per launch);
+  // work schedule of the bf16 kernels: 0 = auto (a thread-block cluster per
+  // unit for short key streams, else persistent stream-K), 1 = stream-K,
+  // 2..8 = clusters of that many CTAs per unit (sts_verify_decode.cu)
+  int schedule;
+  int plan_only;  // nonzero: resolve the schedule (1 or the cluster size) without launching
   // pieces[u] = (first, last) schedule range holding unit u's tiles, written
-  // by the kernel, read by the piece-merge kernel; pref_units = units whose
-  // tile prefix fits in shared memory (dynamic tail enabled), else 0
-  int* sched;
+  // by the stream-K kernel, read by the piece-merge kernel
   int2* pieces;
-  int pref_units;
-  int nch_max;
-  int dyn_chunk;        // minimum tiles per dynamic chunk
-  float dyn_frac;       // fraction of all tiles scheduled dynamically
 };
 
-// Persistent stream-K launch of the bf16 gather kernel in `mode`.
-// Workspace layout: counters [units] int32, then partial (O, lse) slots.
+// Launch of the bf16 gather kernel in `mode`.
+// Workspace layout: piece table [units] int2, then partial (O, lse) slots.
 size_t stream_workspace_bytes(int mode, int64_t units, int M, int d);
 int stream_launch(int mode, DecodeParams& p, void* ws, size_t ws_bytes, cudaStream_t st);
 
@@ -68,7 +64,5 @@ int auto_splits(int64_t units, int64_t keys_per_unit);
 // bf16 decode of the stacked verification rows (sts_verify_decode.cu): the
 // main kernel, then the merge of units split over several schedule ranges
 int verify_decode_launch(int mode, DecodeParams& p, cudaStream_t st);
-constexpr int VERIFY_PREF_MAX_UNITS = 0;
-int gather_launch(int mode, DecodeParams& p, cudaStream_t st);
 
 }  // namespace sts

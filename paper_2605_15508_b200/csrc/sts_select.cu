@@ -543,517 +543,6 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(SelectParams p) 
   }
 }
 
-// ---------------------------------------------------------------------------
-// Select v2 (token mode, rows <= 48K): 16-bit key prefixes in shared memory.
-// Only the top 16 bits of each order key (sign, exponent, 7 mantissa bits)
-// are kept on chip (2 bytes per position: three rows fit on one SM, 256 rows
-// run in one wave on 148 SMs).  Two 8-bit radix passes find the 16-bit
-// threshold prefix (the first one fused into row formation); the low 16 bits
-// are resolved only for the positions in the threshold bin, recomputing their
-// full keys from the score rows (typically a few hundred per row).  Emit walks
-// positions in order: prefix above -> selected, prefix equal -> full-key
-// compare + tie rank (ties to the lowest index), extras always.
-// ---------------------------------------------------------------------------
-constexpr int SV2_THREADS = 512;
-constexpr int SV2_WARPS = SV2_THREADS / 32;
-constexpr int SV2_MAX = 49152;
-
-struct SV2Shared {
-  uint32_t hist[256];
-  int warp_tot[SV2_WARPS];
-  int bcast[4];
-};
-
-__device__ __forceinline__ int sv2_scan(int v, int* warp_tot, int& total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int incl = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += t;
-  }
-  if (lane == 31) warp_tot[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    int x = lane < SV2_WARPS ? warp_tot[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += t;
-    }
-    if (lane < SV2_WARPS) warp_tot[lane] = x;
-  }
-  __syncthreads();
-  const int before = warp > 0 ? warp_tot[warp - 1] : 0;
-  total = warp_tot[SV2_WARPS - 1];
-  __syncthreads();
-  return before + incl - v;
-}
-
-// warp-aggregated shared-memory histogram increment (hot bins: one atomic per
-// distinct bin per warp instead of one per lane)
-__device__ __forceinline__ void sv2_hist_add(uint32_t* hist, int bin, bool active) {
-  const unsigned mask = __ballot_sync(0xffffffffu, active);
-  if (!active) return;
-  const unsigned peers = __match_any_sync(mask, bin);
-  const int leader = __ffs(peers) - 1;
-  if ((int)(threadIdx.x & 31) == leader) atomicAdd(&hist[bin], (unsigned)__popc(peers));
-}
-
-// pick the digit whose descending cumulative count reaches krem (256 bins)
-__device__ __forceinline__ void sv2_pick(SV2Shared& sh, int krem, int& digit, int& above, int& inbin) {
-  const int tid = threadIdx.x;
-  const int v = tid < 256 ? (int)sh.hist[255 - tid] : 0;
-  int tot;
-  const int excl = sv2_scan(v, sh.warp_tot, tot);
-  if (tid < 256 && v > 0 && excl < krem && krem <= excl + v) {
-    sh.bcast[0] = 255 - tid;
-    sh.bcast[1] = excl;
-    sh.bcast[2] = v;
-  }
-  __syncthreads();
-  digit = sh.bcast[0];
-  above = sh.bcast[1];
-  inbin = sh.bcast[2];
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(SV2_THREADS) select_v2_kernel(SelectParams p) {
-  __shared__ SV2Shared sh;
-  extern __shared__ __align__(16) uint16_t k16[];  // [n] key prefixes
-  const int tid = threadIdx.x;
-  const int64_t r = blockIdx.x;
-  const int n = p.row_len ? p.row_len[r] : p.n_common;
-  int32_t* out = p.idx_out + r * p.idx_ld;
-  int32_t srcs[8];
-  if (p.row_src) {
-    for (int q = 0; q < p.nsrc && q < 8; ++q) srcs[q] = p.row_src[r * p.nsrc + q];
-  } else {
-    srcs[0] = (int32_t)r;
-  }
-  int b;
-  if (p.budget_is_fraction) {
-    const double cc = ceil(p.budget * (double)n);
-    b = cc < 1.0 ? 1 : (int)cc;
-  } else {
-    b = (int)p.budget;
-  }
-  const bool cur = (p.flags & STS_SEL_CURRENT) != 0, sink = (p.flags & STS_SEL_SINK) != 0;
-  const int lo_extra = p.recent_window > 0 ? n - p.recent_window : n;
-  auto extra = [&](int j) { return j >= lo_extra || (sink && j == 0) || (cur && j == n - 1); };
-  auto full_key = [&](int j) { return f32_key(row_value(p, srcs, j)); };
-
-  int count = 0;
-  if (n <= 0) {
-  } else if (b >= n) {
-    for (int j = tid; j < n; j += SV2_THREADS) write_idx(p, out, j, j);
-    count = n;
-  } else {
-    // 1. formation: 16-bit prefixes + histogram of their top 8 bits
-    if (tid < 256) sh.hist[tid] = 0;
-    __syncthreads();
-    const bool vec = (p.ld % 4) == 0 && (reinterpret_cast<uintptr_t>(p.scores) % 16) == 0;
-    const int n4 = vec ? n / 4 : 0;
-    for (int v0 = 0; v0 < n4; v0 += SV2_THREADS) {
-      const int v = v0 + tid;
-      const bool ok = v < n4;
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (ok) {
-        a = *reinterpret_cast<const float4*>(p.scores + (int64_t)srcs[0] * p.ld + 4 * v);
-        for (int q = 1; q < p.nsrc; ++q) {
-          const float4 x = *reinterpret_cast<const float4*>(p.scores + (int64_t)srcs[q] * p.ld + 4 * v);
-          a.x = __fadd_rn(a.x, x.x); a.y = __fadd_rn(a.y, x.y); a.z = __fadd_rn(a.z, x.z); a.w = __fadd_rn(a.w, x.w);
-        }
-      }
-      const uint32_t k0 = f32_key(a.x) >> 16, k1 = f32_key(a.y) >> 16, k2 = f32_key(a.z) >> 16, k3 = f32_key(a.w) >> 16;
-      if (ok) {
-        uint2 packed;
-        packed.x = k0 | (k1 << 16);
-        packed.y = k2 | (k3 << 16);
-        *reinterpret_cast<uint2*>(k16 + 4 * v) = packed;
-      }
-      sv2_hist_add(sh.hist, (int)(k0 >> 8), ok);
-      sv2_hist_add(sh.hist, (int)(k1 >> 8), ok);
-      sv2_hist_add(sh.hist, (int)(k2 >> 8), ok);
-      sv2_hist_add(sh.hist, (int)(k3 >> 8), ok);
-    }
-    for (int j0 = 4 * n4; j0 < n; j0 += SV2_THREADS) {
-      const int j = j0 + tid;
-      const bool ok = j < n;
-      const uint32_t k = ok ? full_key(j) >> 16 : 0u;
-      if (ok) k16[j] = (uint16_t)k;
-      sv2_hist_add(sh.hist, (int)(k >> 8), ok);
-    }
-    __syncthreads();
-    int d1, above, inbin;
-    sv2_pick(sh, b, d1, above, inbin);
-    int krem = b - above;
-    // 2. second 8 bits of the prefix
-    uint32_t t16 = (uint32_t)d1 << 8;
-    uint32_t pm16 = 0xff00u;
-    if (krem != inbin) {
-      if (tid < 256) sh.hist[tid] = 0;
-      __syncthreads();
-      for (int j0 = 0; j0 < n; j0 += SV2_THREADS) {
-        const int j = j0 + tid;
-        const uint32_t k = j < n ? k16[j] : 0u;
-        const bool m = j < n && (k >> 8) == (uint32_t)d1;
-        sv2_hist_add(sh.hist, (int)(k & 0xffu), m);
-      }
-      __syncthreads();
-      int d2;
-      sv2_pick(sh, krem, d2, above, inbin);
-      krem -= above;
-      t16 |= (uint32_t)d2;
-      pm16 = 0xffffu;
-    }
-    // 3. low 16 bits among the positions whose prefix equals t16 (full keys
-    //    recomputed from the score rows)
-    uint32_t T = t16 << 16, pmask = pm16 << 16;
-    bool all_bin = krem == inbin;
-    for (int shift = 8; shift >= 0 && !all_bin && pm16 == 0xffffu; shift -= 8) {
-      if (tid < 256) sh.hist[tid] = 0;
-      __syncthreads();
-      for (int j0 = 0; j0 < n; j0 += SV2_THREADS) {
-        const int j = j0 + tid;
-        const bool cand = j < n && k16[j] == t16;
-        uint32_t key = 0;
-        if (cand) key = full_key(j);
-        const bool m = cand && (key & pmask) == T;
-        sv2_hist_add(sh.hist, (int)((key >> shift) & 0xffu), m);
-      }
-      __syncthreads();
-      int d;
-      sv2_pick(sh, krem, d, above, inbin);
-      krem -= above;
-      T |= (uint32_t)d << shift;
-      pmask |= 0xffu << shift;
-      all_bin = krem == inbin;
-    }
-    // here: keys with (key & pmask) > T (prefix-wise) are above; == T are the
-    // threshold ties of which the first krem (index order) are taken
-    // (all of them when all_bin)
-    // 4. emit in index order
-    int run_sel = 0, run_tie = 0;
-    for (int base = 0; base < n; base += 4 * SV2_THREADS) {
-      const int j0 = base + 4 * tid;
-      uint32_t sel = 0, eq = 0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int j = j0 + q;
-        if (j >= n) break;
-        const uint32_t k = k16[j];
-        if ((k & pm16) > (t16 & pm16)) {
-          sel |= 1u << q;
-        } else if ((k & pm16) == (t16 & pm16)) {
-          if (pm16 != 0xffffu || pmask == 0xffff0000u) {
-            eq |= 1u << q;  // resolved at the prefix level
-          } else {
-            const uint32_t mk = full_key(j) & pmask;
-            if (mk > T) sel |= 1u << q;
-            else if (mk == T) eq |= 1u << q;
-          }
-        }
-      }
-      int tie_tot = 0;
-      if (all_bin) {
-        sel |= eq;
-      } else {
-        int rank = run_tie + sv2_scan(__popc(eq), sh.warp_tot, tie_tot);
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if ((eq >> q) & 1u) {
-            if (rank < krem) sel |= 1u << q;
-            ++rank;
-          }
-        run_tie += tie_tot;
-      }
-      if (j0 + 3 >= lo_extra || (sink && j0 == 0) || (cur && j0 + 3 >= n - 1)) {
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (j0 + q < n && extra(j0 + q)) sel |= 1u << q;
-      }
-      int sel_tot;
-      int pos = run_sel + sv2_scan(__popc(sel), sh.warp_tot, sel_tot);
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if ((sel >> q) & 1u) write_idx(p, out, pos++, j0 + q);
-      run_sel += sel_tot;
-    }
-    count = run_sel;
-  }
-  for (int t = tid; t < p.tail_len; t += SV2_THREADS) write_idx(p, out, count + t, max(n, 0) + t);
-  if (tid == 0) p.cnt_out[r] = count + p.tail_len;
-}
-
-// ---------------------------------------------------------------------------
-// Cluster select (token mode): a thread-block cluster of C CTAs per row, CTA c
-// holding the keys of positions [c*n/C, (c+1)*n/C) in its shared memory.  The
-// radix passes exchange 256-bin histograms through distributed shared memory
-// (every CTA sums the same C histograms, so every CTA picks the same digit);
-// after the threshold is known each CTA publishes its tie and selection
-// counts, derives its tie share (ties go to the lowest global index) and its
-// output offset, and emits its range.  Rows are spread over C SMs instead of
-// one: the per-row latency of the single-CTA kernel is what bounds it.
-// ---------------------------------------------------------------------------
-constexpr int CSEL_THREADS = 512;
-constexpr int CSEL_WARPS = CSEL_THREADS / 32;
-constexpr int CSEL_BITS = 8;
-constexpr int CSEL_BINS = 1 << CSEL_BITS;
-constexpr int CSEL_KEYS = 16384;  // keys per CTA held in shared memory (64 KB)
-
-struct CSelShared {
-  uint32_t hist[CSEL_BINS];
-  int xch[8];          // values published to the cluster
-  int warp_tot[CSEL_WARPS];
-  int bcast[4];
-};
-
-__device__ __forceinline__ unsigned csel_rank() {
-  unsigned r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void csel_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t csel_ld(const void* local, unsigned rank) {
-  uint32_t a = (uint32_t)__cvta_generic_to_shared(local), ra, v;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
-  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(ra) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ int csel_block_scan(int v, int* warp_tot, int& total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int incl = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += t;
-  }
-  if (lane == 31) warp_tot[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    int x = lane < CSEL_WARPS ? warp_tot[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int t = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += t;
-    }
-    if (lane < CSEL_WARPS) warp_tot[lane] = x;
-  }
-  __syncthreads();
-  const int before = warp > 0 ? warp_tot[warp - 1] : 0;
-  total = warp_tot[CSEL_WARPS - 1];
-  __syncthreads();
-  return before + incl - v;
-}
-
-template <int C>
-__global__ void __launch_bounds__(CSEL_THREADS) select_cluster_kernel(SelectParams p) {
-  __shared__ CSelShared sh;
-  extern __shared__ __align__(16) uint32_t csel_keys[];  // CSEL_KEYS keys (dynamic shared memory)
-  const unsigned c = csel_rank();
-  const int64_t r = blockIdx.x / C;
-  const int tid = threadIdx.x;
-  const int n = p.row_len ? p.row_len[r] : p.n_common;
-  int32_t* out = p.idx_out + r * p.idx_ld;
-  int32_t srcs[8];
-  if (p.row_src) {
-    for (int q = 0; q < p.nsrc && q < 8; ++q) srcs[q] = p.row_src[r * p.nsrc + q];
-  } else {
-    srcs[0] = (int32_t)r;
-  }
-  int b;
-  if (p.budget_is_fraction) {
-    const double cc = ceil(p.budget * (double)n);
-    b = cc < 1.0 ? 1 : (int)cc;
-  } else {
-    b = (int)p.budget;
-  }
-  const int lo = (int)((int64_t)c * (n > 0 ? n : 0) / C), hi = (int)((int64_t)(c + 1) * (n > 0 ? n : 0) / C);
-  const int len = hi - lo;
-  const bool dense = n > 0 && b >= n;
-  const bool cur = (p.flags & STS_SEL_CURRENT) != 0, sink = (p.flags & STS_SEL_SINK) != 0;
-  const int lo_extra = p.recent_window > 0 ? n - p.recent_window : n;
-  auto extra = [&](int g) { return g >= lo_extra || (sink && g == 0) || (cur && g == n - 1); };
-
-  // 1. keys of this CTA's positions (+ OR / AND of the varying bits)
-  uint32_t k_or = 0u, k_and = 0xffffffffu;
-  if (!dense)
-    for (int j = tid; j < len; j += CSEL_THREADS) {
-      const uint32_t key = f32_key(row_value(p, srcs, lo + j));
-      csel_keys[j] = key;
-      k_or |= key;
-      k_and &= key;
-    }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    k_or |= __shfl_xor_sync(0xffffffffu, k_or, o);
-    k_and &= __shfl_xor_sync(0xffffffffu, k_and, o);
-  }
-  if (tid < CSEL_BINS) sh.hist[tid] = 0;
-  if (tid == 0) {
-    sh.bcast[0] = 0;
-    sh.bcast[1] = -1;
-  }
-  __syncthreads();
-  if ((tid & 31) == 0) {
-    atomicOr(reinterpret_cast<unsigned*>(&sh.bcast[0]), k_or);
-    atomicAnd(reinterpret_cast<unsigned*>(&sh.bcast[1]), k_and);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    sh.xch[0] = sh.bcast[0];
-    sh.xch[1] = sh.bcast[1];
-  }
-  csel_sync();
-  uint32_t g_or = 0u, g_and = 0xffffffffu;
-  for (unsigned q = 0; q < (unsigned)C; ++q) {
-    g_or |= csel_ld(&sh.xch[0], q);
-    g_and &= csel_ld(&sh.xch[1], q);
-  }
-
-  // 2. radix passes over the varying bits, 8 bits per pass, histograms summed
-  //    over the cluster
-  uint32_t prefix = 0u, pmask = 0u;
-  int krem = b, ties_g = 0;
-  bool resolved = dense || n <= 0;
-  const uint32_t diff = g_or ^ g_and;
-  if (!resolved && diff == 0u) {  // every committed key equal: all ties
-    prefix = g_and;
-    pmask = 0xffffffffu;
-    ties_g = n;
-    resolved = true;
-  }
-  int top = resolved ? -1 : 31 - __clz((int)diff);
-  if (!resolved) {
-    pmask = top >= 31 ? 0u : ~((2u << top) - 1u);
-    prefix = g_and & pmask;
-  }
-  while (!resolved) {
-    const int s0 = top - CSEL_BITS + 1 < 0 ? 0 : top - CSEL_BITS + 1;
-    const int width = top - s0 + 1;
-    const uint32_t dm = (1u << width) - 1u;
-    csel_sync();  // every CTA is done reading the previous pass's histograms
-    if (tid < CSEL_BINS) sh.hist[tid] = 0;
-    __syncthreads();
-    for (int j = tid; j < len; j += CSEL_THREADS) {
-      const uint32_t key = csel_keys[j];
-      if ((key & pmask) == prefix) atomicAdd(&sh.hist[(key >> s0) & dm], 1u);
-    }
-    csel_sync();
-    // every CTA sums the same C histograms and finds the same digit
-    int cnt = 0;
-    if (tid < CSEL_BINS)
-      for (unsigned q = 0; q < (unsigned)C; ++q) cnt += (int)csel_ld(&sh.hist[tid], q);
-    // descending inclusive scan over bins (bin 255 first): thread tid holds bin 255 - tid
-    int v = tid < CSEL_BINS ? 0 : 0;
-    __shared__ int s_cnt[CSEL_BINS];
-    if (tid < CSEL_BINS) s_cnt[tid] = cnt;
-    __syncthreads();
-    v = tid < CSEL_BINS ? s_cnt[CSEL_BINS - 1 - tid] : 0;
-    int tot;
-    const int excl = csel_block_scan(v, sh.warp_tot, tot);
-    if (tid < CSEL_BINS && excl < krem && krem <= excl + v) {
-      sh.bcast[2] = CSEL_BINS - 1 - tid;
-      sh.bcast[3] = excl;
-      sh.xch[7] = v;
-    }
-    __syncthreads();
-    const int digit = sh.bcast[2], above = sh.bcast[3], inbin = sh.xch[7];
-    prefix |= (uint32_t)digit << s0;
-    pmask |= dm << s0;
-    krem -= above;
-    if (s0 == 0 || krem == inbin) {
-      ties_g = inbin;
-      resolved = true;
-    }
-    top = s0 - 1;
-  }
-
-  // 3. round A: this CTA's threshold ties -> its share of them (ties go to the
-  //    lowest global index, i.e. to the lower CTAs first)
-  const bool all_ties = krem >= ties_g;  // every key of the final bin is taken
-  int t_loc = 0;
-  if (!dense && n > 0)
-    for (int j = tid; j < len; j += CSEL_THREADS) t_loc += (csel_keys[j] & pmask) == prefix ? 1 : 0;
-  int tt;
-  csel_block_scan(t_loc, sh.warp_tot, tt);
-  if (tid == 0) sh.xch[2] = tt;
-  csel_sync();
-  int tie_before = 0;
-  for (unsigned q = 0; q < c; ++q) tie_before += (int)csel_ld(&sh.xch[2], q);
-  const int need = all_ties ? 0x7fffffff : krem - tie_before;  // ties this CTA takes, by local rank
-
-  // selection flags of 4 consecutive local positions (block-wide tie ranks)
-  auto flags4 = [&](int j0, int& run_tie) -> uint32_t {
-    uint32_t sel = 0, eq = 0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int j = j0 + q;
-      if (j >= len) break;
-      const uint32_t mk = csel_keys[j] & pmask;
-      if (mk > prefix) sel |= 1u << q;
-      else if (mk == prefix) eq |= 1u << q;
-    }
-    int tie_tot;
-    int rank = run_tie + csel_block_scan(__popc(eq), sh.warp_tot, tie_tot);
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if ((eq >> q) & 1u) {
-        if (rank < need) sel |= 1u << q;
-        ++rank;
-      }
-      if (j0 + q < len && extra(lo + j0 + q)) sel |= 1u << q;
-    }
-    run_tie += tie_tot;
-    return sel;
-  };
-
-  // round B: this CTA's selection count -> its output offset
-  int sel_loc = 0;
-  if (dense) {
-    sel_loc = len;
-  } else if (n > 0) {
-    int run_tie = 0, cnt_acc = 0;
-    for (int base = 0; base < len; base += 4 * CSEL_THREADS) cnt_acc += __popc(flags4(base + 4 * tid, run_tie));
-    csel_block_scan(cnt_acc, sh.warp_tot, sel_loc);
-  }
-  if (tid == 0) sh.xch[3] = sel_loc;
-  csel_sync();
-  int out_off = 0, total = 0;
-  for (unsigned q = 0; q < (unsigned)C; ++q) {
-    const int sq = (int)csel_ld(&sh.xch[3], q);
-    out_off += q < c ? sq : 0;
-    total += sq;
-  }
-  csel_sync();  // published counts read by everyone (a CTA may now exit)
-
-  // 4. emit this CTA's positions in ascending order
-  if (dense) {
-    for (int j = tid; j < len; j += CSEL_THREADS) write_idx(p, out, out_off + j, lo + j);
-  } else if (n > 0) {
-    int run_sel = 0, run_tie = 0;
-    for (int base = 0; base < len; base += 4 * CSEL_THREADS) {
-      const int j0 = base + 4 * tid;
-      const uint32_t sel = flags4(j0, run_tie);
-      int sel_tot;
-      int pos = out_off + run_sel + csel_block_scan(__popc(sel), sh.warp_tot, sel_tot);
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if ((sel >> q) & 1u) write_idx(p, out, pos++, lo + j0 + q);
-      run_sel += sel_tot;
-    }
-  }
-  // 5. in-block tail and the count (last CTA of the cluster)
-  if (c == (unsigned)(C - 1)) {
-    for (int t = tid; t < p.tail_len; t += CSEL_THREADS) write_idx(p, out, total + t, (n > 0 ? n : 0) + t);
-    if (tid == 0) p.cnt_out[r] = total + p.tail_len;
-  }
-}
-
 // page_aggregate as a standalone op (src/sparsity.py:72-83): one thread per page
 __global__ void page_aggregate_kernel(SelectParams p, double* out, int64_t out_ld) {
   const int64_t r = blockIdx.y;
@@ -1134,62 +623,6 @@ extern "C" int sts_select_topk(const float* scores_dev, int64_t ld, const int32_
   p.status = status_dev;
   p.buf_bytes = key_buf_bytes(max_len, page_size);
 
-  // experimental (STS_SELECT_V2=1): token-mode rows <= 48K through the 16-bit
-  // prefix select.  Parity-tested, but measured slower at c2 (158 vs 63 us:
-  // the threshold-bin candidates' full keys are recomputed with scattered,
-  // latency-bound loads in three passes), so off by default.
-  {
-    static const int env = getenv("STS_SELECT_V2") ? atoi(getenv("STS_SELECT_V2")) : 0;
-    if (env == 1 && page_size == 1 && max_len > 0 && max_len <= SV2_MAX && rows <= ((int64_t)1 << 31) - 1) {
-      const size_t smem2 = (((size_t)max_len * 2 + 15) & ~size_t(15));
-      static const cudaError_t a2 =
-          cudaFuncSetAttribute(select_v2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SV2_MAX * 2);
-      STS_CUDA_CHECK(a2);
-      select_v2_kernel<<<(unsigned)rows, SV2_THREADS, smem2, static_cast<cudaStream_t>(stream)>>>(p);
-      STS_LAUNCH_CHECK();
-      return STS_OK;
-    }
-  }
-  // experimental (STS_SELECT_CLUSTER=1): token-mode rows that fit C x 16K keys
-  // through one thread-block cluster per row.  Measured slower than the
-  // single-CTA kernel at c2 (150 vs 63 us: 8-bit digits without candidate
-  // compaction serialise on hot shared-memory histogram bins), so off by default.
-  {
-    static const int env = getenv("STS_SELECT_CLUSTER") ? atoi(getenv("STS_SELECT_CLUSTER")) : 0;
-    const int64_t per = CSEL_KEYS;
-    if (env == 1 && page_size == 1 && max_len > 0 && max_len <= 8 * per && rows * 2 <= (int64_t)1 << 30) {
-      int C = (int)((max_len + per - 1) / per);
-      C = C < 2 ? 2 : (C <= 2 ? 2 : (C <= 4 ? 4 : 8));
-      cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3((unsigned)(rows * C));
-      cfg.blockDim = dim3(CSEL_THREADS);
-      cfg.dynamicSmemBytes = CSEL_KEYS * 4;
-      cfg.stream = static_cast<cudaStream_t>(stream);
-      static const bool attr_ok =
-          cudaFuncSetAttribute(select_cluster_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, CSEL_KEYS * 4) ==
-              cudaSuccess &&
-          cudaFuncSetAttribute(select_cluster_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, CSEL_KEYS * 4) ==
-              cudaSuccess &&
-          cudaFuncSetAttribute(select_cluster_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, CSEL_KEYS * 4) ==
-              cudaSuccess;
-      STS_REQUIRE(attr_ok, STS_ERR_CUDA, "cluster select setup failed");
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = C;
-      at[0].val.clusterDim.y = 1;
-      at[0].val.clusterDim.z = 1;
-      cfg.attrs = at;
-      cfg.numAttrs = 1;
-      p.gbuf = nullptr;
-      cudaError_t e;
-      if (C == 2) e = cudaLaunchKernelEx(&cfg, select_cluster_kernel<2>, p);
-      else if (C == 4) e = cudaLaunchKernelEx(&cfg, select_cluster_kernel<4>, p);
-      else e = cudaLaunchKernelEx(&cfg, select_cluster_kernel<8>, p);
-      STS_CUDA_CHECK(e);
-      count_launch();
-      return STS_OK;
-    }
-  }
   const size_t sh_bytes = (sizeof(SelShared) + 15) & ~size_t(15);
   size_t smem = sh_bytes;
   int grid;

@@ -54,7 +54,8 @@ struct DistState {
   int dense;        // 1: budget >= n, every position selected
   int ties_global;  // keys matching the final prefix, all ranks
   int ties_local;   // ... on this rank
-  int pad[3];
+  int bad;          // 1: the global histogram could not place the remaining k (inconsistent ranks)
+  int pad[2];
 };
 
 struct DistParams {
@@ -199,7 +200,7 @@ __global__ void __launch_bounds__(DIST_THREADS) dist_keys_kernel(DistParams p, i
     s.done = s.dense;
     s.ties_global = 0;
     s.ties_local = 0;
-    s.pad[0] = s.pad[1] = s.pad[2] = 0;
+    s.bad = s.pad[0] = s.pad[1] = 0;
     p.state[r] = s;
   }
   __syncthreads();
@@ -325,7 +326,10 @@ __global__ void dist_advance_kernel(DistParams p, int round, const int32_t* hist
   const int excl = incl - lsum;
   const bool mine = excl < st.krem && st.krem <= incl;
   const uint32_t who = __ballot_sync(0xffffffffu, mine);
-  if (who == 0) return;  // inconsistent histogram (cannot happen): leave the row unresolved
+  if (who == 0) {  // inconsistent histogram (ranks disagree on k / shards): flag it, finish reports it
+    if (lane == 0) p.state[r].bad = 1;
+    return;
+  }
   if (lane != __ffs(who) - 1) return;
   int acc = excl, digit = 0, inbin = 0;
   for (int q = 0; q < per; ++q) {
@@ -655,6 +659,10 @@ __global__ void __launch_bounds__(EMIT_THREADS) dist_emit_write_kernel(DistParam
   const int32_t* tc = e.tok_cnt + r * e.tok_chunks;
   const int64_t w = (int64_t)blockIdx.x * (EMIT_CHUNK / 32) + threadIdx.x;
   uint32_t m = sel.ps == 1 ? token_word(sel, w) : 0u;  // issued before the prefix sum
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const DistState st = p.state[r];
+    if (!st.done || st.bad) set_status(e.status, STS_DEV_SELECT_INCONSISTENT);
+  }
   const int base = chunk_prefix(tc, blockIdx.x, red);
   if (sel.ps == 1) {
     // one token word per thread
@@ -812,6 +820,8 @@ __global__ void dist_ties_kernel(const DistState* state, int64_t rows, int32_t* 
 using namespace sts;
 
 extern "C" int32_t sts_dist_select_rounds(int32_t page_size) { return page_size == 1 ? dd_rounds(32) : dd_rounds(64); }
+
+extern "C" int32_t sts_dist_select_bins(void) { return DD_BINS; }
 
 extern "C" size_t sts_dist_select_workspace_bytes(int64_t rows, int32_t n_local, int32_t page_size) {
   return dist_ws_bytes(rows, n_local, page_size < 1 ? 1 : page_size);

@@ -169,11 +169,13 @@ static int sparse_decode_impl(int32_t dtype, int32_t out_dtype, const void* q_de
   STS_REQUIRE(rows_per_head >= 1, STS_ERR_CONTRACT, "rows_per_head must be >= 1");
   STS_REQUIRE(idx_dev ? (cnt_dev != nullptr) : (n_dense >= 0), STS_ERR_CONTRACT,
               "index list needs counts / dense needs n_dense");
-  STS_REQUIRE(splits >= 1 && splits <= 4096, STS_ERR_CONTRACT, "splits must be in [1, 4096]");
+  STS_REQUIRE(dtype == STS_DTYPE_BF16 || (splits >= 1 && splits <= 4096), STS_ERR_CONTRACT,
+              "splits must be in [1, 4096]");
   STS_REQUIRE(dtype != STS_DTYPE_F32 || units <= 65535, STS_ERR_CONTRACT, "f32 path: units must be <= 65535 (grid.y)");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
 
   DecodeParams p;
+  memset(&p, 0, sizeof(p));
   p.q = q_dev;
   p.k = k_cache_dev;
   p.v = v_cache_dev;
@@ -206,14 +208,16 @@ static int sparse_decode_impl(int32_t dtype, int32_t out_dtype, const void* q_de
   p.probs_out = nullptr;
   p.out_ld = 0;
   p.probs_mode = 0;
-  p.counters = nullptr;
-  p.sched = nullptr;
   p.pieces = nullptr;
-  p.pref_units = 0;
-  p.nch_max = p.dyn_chunk = 0;
-  p.dyn_frac = 0.f;
+  p.schedule = 0;
   if (dtype == STS_DTYPE_BF16) {
-    // persistent stream-K kernel; `splits` does not apply
+    // bf16: `splits` picks the work schedule (0 auto, 1 persistent stream-K,
+    // 2/3/4/6/8 thread-block clusters of that many CTAs per unit)
+    STS_REQUIRE(splits == 0 || splits == 1 || splits == 2 || splits == 3 || splits == 4 || splits == 6 ||
+                    splits == 8,
+                STS_ERR_CONTRACT, "bf16 schedule must be 0 (auto), 1 (stream-K) or a cluster size in {2,3,4,6,8}, got %d",
+                splits);
+    p.schedule = splits;
     return stream_launch(MODE_DECODE, p, workspace_dev, workspace_bytes, st);
   }
   if (splits > 1) {
@@ -264,6 +268,21 @@ extern "C" int sts_sparse_prefill(int32_t dtype, int32_t out_dtype, const void* 
   return sparse_decode_impl(dtype, out_dtype, q_dev, k_cache_dev, v_cache_dev, kv_unit_stride, kv_row_stride,
                             kv_units * rows, M, d, idx_dev, idx_ld, cnt_dev, 0, nullptr, -1, 1, 0, scale, out_dev,
                             lse_dev, 1, status_dev, workspace_dev, workspace_bytes, stream, rows > 1 ? rows : 1);
+}
+
+extern "C" int32_t sts_sparse_decode_schedule(int64_t units, int32_t M, int32_t d, int64_t keys_per_unit,
+                                              int32_t schedule) {
+  if (units <= 0 || M < 1 || M > 48 || (d != 64 && d != 128)) return 0;
+  if (schedule != 0) return schedule;
+  DecodeParams p;
+  memset(&p, 0, sizeof(p));
+  p.units = units;
+  p.M = M;
+  p.d = d;
+  p.n_dense = keys_per_unit > 0x7fffffff ? 0x7fffffff : (int)keys_per_unit;
+  p.plan_only = 1;
+  const int r = verify_decode_launch(MODE_DECODE, p, nullptr);
+  return r >= 1 && r <= 8 ? r : 0;
 }
 
 extern "C" int32_t sts_auto_splits(int64_t units, int64_t keys_per_unit) {

@@ -19,8 +19,6 @@
 // Gather: 16-byte cp.async into padded rows (2d+16 bytes: conflict-free
 // ldmatrix), one IMAD.WIDE + LDGSTS per copy (32-bit row offsets), STAGES
 // deep, continuous across unit boundaries; index slices prefetched a ring ahead.
-#include <stdlib.h>
-
 #include "sts_decode.cuh"
 
 namespace sts {
@@ -849,34 +847,42 @@ int launch_cluster(DecodeParams& p, cudaStream_t st) {
   return STS_OK;
 }
 
-#ifndef STS_CLUSTER_MAX
-#define STS_CLUSTER_MAX 8
-#endif
-
-// Cluster mode when the resident CTA slots hold >= 2 CTAs per unit and a CTA
-// would stream few tiles (fixed per-launch costs dominate): the c2 shape
-// (256 units on 888 slots, ~30 tiles per CTA) -> clusters of 3, measured
-// 92.8 vs 98.9 us (sparse) and 670 vs 688 us (dense, ~300 tiles per CTA).  At
-// c4 (~950 tiles per CTA) the 13% of slots a floor(slots / units) cluster
-// grid leaves idle cost more (2.55 vs 2.35 ms), so long streams stay
-// stream-K; the draft LSE pass also measured better as stream-K.
-// STS_VERIFY_CLUSTER=0 disables, =1 forces (when it applies).
+// Schedule (DecodeParams::schedule).  Auto (0): a thread-block cluster per
+// unit when the resident CTA slots hold >= 2 CTAs per unit and a CTA would
+// stream few tiles (fixed per-launch costs dominate): the c2 shape (256 units
+// on 888 slots, ~30 tiles per CTA) -> clusters of 3, measured 92.8 vs 98.9 us
+// (sparse) and 670 vs 688 us (dense, ~300 tiles per CTA).  At c4 (~950 tiles
+// per CTA) the 13% of slots a floor(slots / units) cluster grid leaves idle
+// cost more (2.55 vs 2.35 ms), so long streams stay stream-K; the draft LSE
+// pass also measured better as stream-K.  1: stream-K.  2..8: clusters of
+// exactly that many CTAs (any M; parity tests force every size).
 template <int D, int NW, int KT, int STAGES, int MODE>
 int try_cluster(DecodeParams& p, cudaStream_t st, int per_sm) {
-  static const int env = getenv("STS_VERIFY_CLUSTER") ? atoi(getenv("STS_VERIFY_CLUSTER")) : -1;
-  if (env == 0 || MODE != MODE_DECODE || NW != 2 || p.units <= 0) return -1;
-  const int64_t slots = (int64_t)num_sms() * per_sm;
-  const int64_t cap = p.idx ? p.idx_ld : p.n_dense;  // keys per unit (upper bound)
-  const int64_t tiles_per_slot = p.units * ((cap + KT - 1) / KT) / slots;
-  if (env != 1 && tiles_per_slot > 600) return -1;
-  int64_t cs = slots / p.units;
-  if (cs > STS_CLUSTER_MAX) cs = STS_CLUSTER_MAX;
-  if (cs >= 8) return launch_cluster<D, NW, KT, STAGES, MODE, 8>(p, st);
-  if (cs >= 6) return launch_cluster<D, NW, KT, STAGES, MODE, 6>(p, st);
-  if (cs >= 4) return launch_cluster<D, NW, KT, STAGES, MODE, 4>(p, st);
-  if (cs >= 3) return launch_cluster<D, NW, KT, STAGES, MODE, 3>(p, st);
-  if (cs >= 2) return launch_cluster<D, NW, KT, STAGES, MODE, 2>(p, st);
-  return -1;
+  if (MODE != MODE_DECODE || p.units <= 0 || p.schedule == 1) return -1;
+  int64_t cs = p.schedule;
+  if (cs == 0) {
+    if (NW != 2) return -1;
+    const int64_t slots = (int64_t)num_sms() * per_sm;
+    const int64_t cap = p.idx ? p.idx_ld : p.n_dense;  // keys per unit (upper bound)
+    const int64_t tiles_per_slot = p.units * ((cap + KT - 1) / KT) / slots;
+    if (tiles_per_slot > 600) return -1;
+    cs = slots / p.units;
+    if (cs > 8) cs = 8;
+    cs = cs >= 8 ? 8 : cs >= 6 ? 6 : cs >= 4 ? 4 : cs;
+    if (cs < 2) return -1;
+  }
+  if (p.plan_only) return (int)cs;
+  STS_REQUIRE(p.units * cs <= 0x7fffffffLL, STS_ERR_CONTRACT, "too many units for a cluster grid");
+  switch (cs) {
+    case 2: return launch_cluster<D, NW, KT, STAGES, MODE, 2>(p, st);
+    case 3: return launch_cluster<D, NW, KT, STAGES, MODE, 3>(p, st);
+    case 4: return launch_cluster<D, NW, KT, STAGES, MODE, 4>(p, st);
+    case 6: return launch_cluster<D, NW, KT, STAGES, MODE, 6>(p, st);
+    case 8: return launch_cluster<D, NW, KT, STAGES, MODE, 8>(p, st);
+    default:
+      set_error("unsupported cluster size %d", (int)cs);
+      return STS_ERR_CONTRACT;
+  }
 }
 
 template <int D, int NW, int KT, int STAGES, int MODE>
@@ -890,11 +896,13 @@ int launch_verify(DecodeParams& p, cudaStream_t st) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, L::THREADS, L::SMEM) != cudaSuccess) return -1;
     return n < 1 ? 1 : n;
   }();
+  if (per_sm <= 0 && p.plan_only) return -1;
   STS_REQUIRE(per_sm > 0, STS_ERR_CUDA, "verify kernel setup failed: %s", cudaGetErrorString(cudaGetLastError()));
-  if constexpr (NW == 2 && MODE == MODE_DECODE) {
+  if constexpr (MODE == MODE_DECODE) {
     const int rc = try_cluster<D, NW, KT, STAGES, MODE>(p, st, per_sm);
     if (rc >= 0) return rc;
   }
+  if (p.plan_only) return 1;
   const int smem = L::SMEM;
   kern<<<num_sms() * per_sm, L::THREADS, smem, st>>>(p);
   STS_LAUNCH_CHECK();

@@ -16,6 +16,7 @@ from . import _lib
 from ._lib import call, ptr, stream_handle
 
 STS_DTYPE = {torch.float32: _lib.STS_DTYPE_F32, torch.bfloat16: _lib.STS_DTYPE_BF16}
+SCHEDULES = (0, 1, 2, 3, 4, 6, 8)  # bf16 decode work schedules (see sparse_decode)
 
 
 def _require_cuda(*ts):
@@ -130,7 +131,8 @@ def select_topk(scores: torch.Tensor, *, budget, page_size: int = 1, include_cur
 
 def sparse_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, *, idx=None,
                   cnt=None, n_dense: int = 0, member=None, causal_base: int = -1,
-                  rows_per_head: int = 1, pos_offset: int = 0, scale=None, splits=None, out=None,
+                  rows_per_head: int = 1, pos_offset: int = 0, scale=None, splits=None, schedule: int = 0,
+                  out=None,
                   lse=None, status=None, out_dtype=None, host_kv: bool = False, workspace: Workspace | None = None,
                   stream=None):
     """Gathered-KV sparse flash-decode.
@@ -142,6 +144,9 @@ def sparse_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
     lse fp32 [U, M]).  Semantics: include/sts_b200.h sts_sparse_decode.
     ``host_kv``: the caches may be pinned host tensors (KV offload tier): the
     same kernel then gathers only the selected rows over the host link.
+    ``splits``: fp32 split-K factor.  ``schedule`` (bf16): 0 = auto (one
+    thread-block cluster per unit for short key streams, else persistent
+    stream-K), 1 = stream-K, 2/3/4/6/8 = clusters of that many CTAs per unit.
     """
     _require_cuda(q, idx, cnt, member)
     _require_kv(k_cache, v_cache, host_kv=host_kv)
@@ -157,9 +162,13 @@ def sparse_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
     idx_ld = idx.stride(0) if idx is not None else 0
     if member is not None and (member.stride(0) != idx_ld or member.dtype != torch.int32 and member.dtype != torch.uint32):
         raise ValueError("member must be int32/uint32 with the same row stride as idx")
-    if splits is None:
-        keys = idx.shape[1] if idx is not None else n_dense
-        splits = _lib.load().sts_auto_splits(U, keys) if q.dtype == torch.bfloat16 else 1
+    if q.dtype == torch.bfloat16:
+        # bf16: the argument is the work schedule (0 auto, 1 stream-K, C clusters of C CTAs per unit)
+        if int(schedule) not in SCHEDULES:
+            raise ValueError(f"schedule must be one of {SCHEDULES}")
+        splits = int(schedule)
+    elif splits is None:
+        splits = 1
     dev = q.device
     out_dtype = q.dtype if out_dtype is None else out_dtype
     if out_dtype not in (q.dtype, torch.float32):

@@ -156,7 +156,7 @@ class DistSelector:
         self.ws = torch.empty(int(lib.sts_dist_select_workspace_bytes(rows, n_local, page_size)),
                               dtype=torch.uint8, device=device)
         self.hist_local = torch.zeros((rows, _lib.STS_DIST_BINS), dtype=torch.int32, device=device)
-        self.hist_global = torch.zeros_like(self.hist_local)
+        self.hist_global = torch.zeros_like(self.hist_local) if nranks > 1 else self.hist_local
         self.ties_local = torch.zeros((rows,), dtype=torch.int32, device=device)
         self.ties_all = torch.zeros((nranks, rows), dtype=torch.int32, device=device)
 
@@ -174,6 +174,10 @@ class DistSelector:
         wlen = self.ws.numel()
         call("sts_dist_select_begin", gp, ptr(self.hist_local), ptr(self.ws), wlen, st)
         for r in range(self.rounds):
+            if self.nranks == 1:  # the global histogram IS the local one: no copy, no collective
+                call("sts_dist_select_round", gp, r, ptr(self.hist_local), ptr(self.hist_local),
+                     ptr(self.ties_local) if r == self.rounds - 1 else None, ptr(self.ws), wlen, st)
+                continue
             self.hist_global.copy_(self.hist_local)
             yield (ALL_REDUCE_SUM, self.hist_global)
             last = r == self.rounds - 1

@@ -90,7 +90,7 @@ class STSVerifyStep:
     """Preallocated GPU pipeline for one verify step (see module docstring)."""
 
     def __init__(self, shape: VerifyShape, sparsity: SparsityConfig, mapping_table, mode: str = "S",
-                 device=None, splits=None, long_row_min=None):
+                 device=None, schedule: int = 0, long_row_min=None):
         if mode not in ("S", "R"):
             raise ValueError("mode must be 'S' or 'R'")
         if shape.target_q_heads % shape.target_kv_heads or shape.draft_q_heads % shape.draft_kv_heads:
@@ -159,9 +159,9 @@ class STSVerifyStep:
         self.out = torch.empty((s.target_units, M, s.head_dim), dtype=torch.bfloat16, device=dev)
         self.lse = torch.empty((s.target_units, M), dtype=torch.float32, device=dev)
         self.status = torch.zeros((1,), dtype=torch.int32, device=dev)
-        keys = self.idx_ld
-        self.splits = splits if splits is not None else kernels._lib.load().sts_auto_splits(s.target_units, keys)
-        self.dense_splits = kernels._lib.load().sts_auto_splits(s.target_units, s.n_kv)
+        # attention work schedule (kernels.sparse_decode): 0 = auto; tests force
+        # stream-K (1) or cluster sizes 2..8 to cover every instance
+        self.schedule = int(schedule)
         # unit groups of the host-buffer attention pipeline (see attend_host)
         # (2 measured best at c2: 157 vs 200 µs for 1, 200 for 3 — tools/gpu_e2e_chunks.sh)
         self.host_chunks = int(os.environ.get("STS_HOST_CHUNKS", "2"))
@@ -206,14 +206,14 @@ class STSVerifyStep:
         causal = s.context if self.mode == "S" else -1
         return kernels.sparse_decode(target_q, target_k, target_v, idx=self.idx, cnt=self.cnt,
                                      member=self.member, causal_base=causal, rows_per_head=s.rows,
-                                     splits=self.splits, out=self.out, lse=self.lse, status=self.status,
+                                     schedule=self.schedule, out=self.out, lse=self.lse, status=self.status,
                                      workspace=self.ws_dec, stream=stream)
 
     def attend_dense(self, target_q, target_k, target_v, out=None, lse=None, stream=None):
         """Dense baseline on the same kernel: every cached key, causal tail."""
         s = self.shape
         return kernels.sparse_decode(target_q, target_k, target_v, n_dense=s.n_kv, causal_base=s.context,
-                                     rows_per_head=s.rows, splits=self.dense_splits,
+                                     rows_per_head=s.rows,
                                      out=out if out is not None else self.out,
                                      lse=lse if lse is not None else self.lse, status=self.status,
                                      workspace=self.ws_dec, stream=stream)
@@ -292,7 +292,7 @@ class STSVerifyStep:
                 main.wait_stream(s_in)
             member = self.member[u0:u1] if self.member is not None else None
             kernels.sparse_decode(q[u0:u1], k[u0:u1], v[u0:u1], idx=self.idx[u0:u1], cnt=self.cnt[u0:u1],
-                                  member=member, causal_base=causal, rows_per_head=s.rows,
+                                  member=member, causal_base=causal, rows_per_head=s.rows, schedule=self.schedule,
                                   out=self.out[u0:u1], lse=self.lse[u0:u1], status=self.status,
                                   workspace=self.ws_dec, stream=main)
             s_out.wait_stream(main)

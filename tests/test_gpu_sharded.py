@@ -224,3 +224,35 @@ def test_heads_times_sequence_sharding(cuda_ok):
             want, _ = O.block_attention(qf[b, l, kvh], kf[b, l, kvh], vf[b, l, kvh], want_idx,
                                         causal_base=s.context, rows_per_head=s.rows)
             np.testing.assert_allclose(out[u], want, rtol=2e-2, atol=2e-2)
+
+
+@pytest.mark.parametrize("ps", [1, 16])
+@pytest.mark.parametrize("P", [1, 3])
+def test_dist_select_long_rows_span_chunks(cuda_ok, ps, P):
+    """Rows longer than two CTA chunks of every sharded-select pass (key and
+    histogram passes: 32768 positions per CTA; emit: 16384): the cross-CTA
+    histogram atomics, the per-chunk tie prefix of the bits pass and the
+    token-count prefix of the write pass all run.  Tie-heavy mode-S rows
+    (4 summed sources), sink + recent window + in-block tail; bit-exact vs
+    the single-CTA select_kernel and the oracle."""
+    import torch
+
+    from paper_2605_15508_b200 import kernels
+
+    rng = np.random.default_rng(70001 + ps + P)
+    n, S, rows, tail = 70001, 6, 4, 5
+    x = np.stack([_rows_kind(rng, n + tail + 3, "ties") for _ in range(S)])
+    scores = torch.from_numpy(x).cuda()
+    src = torch.from_numpy(rng.integers(0, S, (rows, 4)).astype(np.int32)).cuda()
+    b = 7001
+    kp = b if ps == 1 else -(-b // ps)
+    got = _dist_select(scores, src, n, kp, P, ps=ps, sink=True, win=33, tail=tail)
+    idx, cnt = kernels.select_topk(scores, row_src=src, budget=b, page_size=ps, include_current=False,
+                                   include_sink=True, recent_window=33, n_common=n, tail_len=tail)
+    cfg = O.OracleSparsityConfig(0.1, ps, False, True, 33)
+    for r in range(rows):
+        want = idx[r, : int(cnt[r])].cpu().numpy()
+        assert np.array_equal(got[r], want), (ps, P, r)
+        red = O.reduce_rows_fp32([x[j] for j in src[r].cpu().numpy()])
+        sel = O.select_committed(red, n, b, cfg)
+        assert np.array_equal(got[r], np.concatenate([sel, np.arange(n, n + tail)]))
