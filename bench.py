@@ -104,8 +104,8 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def workload_key(config, mode, page_size, layout, world):
-    return f"{config}:{mode}:ps{page_size}:{layout}:P{world}"
+def workload_key(config, mode, page_size, layout, world, sparsity=0.9):
+    return f"{config}:{mode}:s{sparsity:g}:ps{page_size}:{layout}:P{world}"
 
 
 def ncu_traffic(key):
@@ -557,7 +557,7 @@ def run_single_gpu(args):
     dense_bytes = algorithmic_bytes(shape, shape.n_kv, dense=True)
     peak, peak_src = peaks()
     achieved = nbytes / (att * 1e-6) / 1e9
-    key = workload_key(args.config, args.mode, args.page_size, args.layout, 1)
+    key = workload_key(args.config, args.mode, args.page_size, args.layout, 1, args.sparsity)
     traffic, traffic_src = ncu_traffic(key)
     sched = int(lib.sts_sparse_decode_schedule(shape.target_units, step.M, shape.head_dim, step.idx_ld,
                                                args.schedule))
@@ -924,7 +924,7 @@ def run_sharded(args, world, rank, local):
     nbytes = algorithmic_bytes(shape, keys_per_unit)
     peak, peak_src = peaks()
     achieved = nbytes / (att * 1e-6) / 1e9 / world  # per GPU
-    key = workload_key(args.config, "S", args.page_size, "separate", world)
+    key = workload_key(args.config, "S", args.page_size, "separate", world, args.sparsity)
     traffic, traffic_src = ncu_traffic(key)
     hp, sp = r["hp"], r["sp"]
     line = {

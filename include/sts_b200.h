@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define STS_ABI_VERSION 3
+#define STS_ABI_VERSION 4
 
 #define STS_OK 0
 #define STS_ERR_INPUT 1
@@ -247,6 +247,35 @@ STS_API int sts_topk_bitsets(const int32_t* idx_dev, int64_t idx_ld, const int32
                              int32_t words, uint32_t* bits_out_dev, void* stream);
 STS_API int sts_bitset_overlap(const uint32_t* a_dev, int32_t Ta, const uint32_t* b_dev, int32_t Tb, int64_t W,
                                unsigned long long* scores_dev, void* stream);
+
+/* ------------------------------------------------------------------------
+ * sts_block_attention_f64 — reference-exact masked block attention with
+ * attention / score recording: the per-head loop of toymodel._run_block
+ * (src/toymodel.py:315-352) for every head of one layer in one launch, math
+ * in fp64 as the reference states it.  Replaces the attention of
+ * forward_prefill / forward_decode / forward_block (:359-455) with
+ * record_attention / record_scores (ForwardRecord.attention / .scores,
+ * :226-240), used by the model-level drop-in (model.py, specdec.py).
+ *   q_dev      fp32 [heads][m][d]: rows r at global position start_pos + r
+ *   k/v_cache  fp32, head h row j at h*kv_head_stride + j*kv_row_stride
+ *   idx/cnt    optional per-row key lists (ascending, <= the row's position);
+ *              row (h, r) uses list list_of_row[h*m + r] (-1: dense causal),
+ *              or list h*m + r when list_of_row is NULL; idx NULL: all dense
+ *   out_dev    fp32 [m][out_ld], head h at columns [h*d, (h+1)*d)
+ *   probs_dev  nullable fp32 [heads*m][rec_ld]: the row's softmax weights over
+ *              [0, start_pos+m) (zero outside its allowed set)
+ *   scores_dev nullable fp32 [heads*m][rec_ld]: raw q.k*scale over the causal
+ *              prefix, zero beyond the row's position (dense for masked rows)
+ * Limits: d <= 256, start_pos + m <= ~28K (a row's fp64 scores in shared
+ * memory).  Device status bits: STS_DEV_BAD_INDEX for list entries outside
+ * [0, position], STS_DEV_EMPTY_ROW for an empty list.
+ * ---------------------------------------------------------------------- */
+STS_API int sts_block_attention_f64(const float* q_dev, const float* k_cache_dev, const float* v_cache_dev,
+                                    int64_t kv_head_stride, int64_t kv_row_stride, int32_t heads, int32_t m,
+                                    int32_t d, int32_t start_pos, double scale, const int32_t* idx_dev,
+                                    int64_t idx_ld, const int32_t* cnt_dev, const int32_t* list_of_row_dev,
+                                    float* out_dev, int64_t out_ld, float* probs_dev, float* scores_dev,
+                                    int64_t rec_ld, int32_t* status_dev, void* stream);
 
 /* ------------------------------------------------------------------------
  * Sequence-sharded selection (context-parallel decode): the

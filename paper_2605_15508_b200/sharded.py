@@ -39,7 +39,7 @@ from . import _lib, kernels
 from ._lib import call, ptr, stream_handle
 from .kernels import Workspace
 from .sparsity import SparsityConfig
-from .verify import VerifyShape
+from .verify import VerifyShape, _nvtx
 
 ALL_REDUCE_SUM = "all_reduce_sum"
 ALL_GATHER = "all_gather"
@@ -278,9 +278,14 @@ class ShardedVerifyStep:
     def capture(self, draft_q, draft_k, stream=None):
         s, R = self.shape, self.shape.rows
         G = s.draft_group
-        kernels.draft_lse(draft_q, draft_k, G=G, R=R, base=s.context, n_keys=self.n_loc, pos_offset=self.lo,
-                          out=self.lse_local, workspace=self.ws_draft, stream=stream)
+        with _nvtx("sts.capture"):
+            kernels.draft_lse(draft_q, draft_k, G=G, R=R, base=s.context, n_keys=self.n_loc, pos_offset=self.lo,
+                              out=self.lse_local, workspace=self.ws_draft, stream=stream)
         yield (ALL_GATHER, self.lse_local, self.lse_all)
+        with _nvtx("sts.capture"):
+            self._capture_probs(draft_q, draft_k, s, G, R, stream)
+
+    def _capture_probs(self, draft_q, draft_k, s, G, R, stream):
         kernels.lse_merge(None, self.lse_all.view(self.nranks, -1), lse_out=self.lse_global, stream=stream)
         kernels.draft_probs(draft_q, draft_k, self.lse_global.view(s.draft_units, -1), G=G, R=R, base=s.context,
                             mode="S", n_keys=self.n_loc, pos_offset=self.lo, out=self.draft_rows, stream=stream)
@@ -339,9 +344,11 @@ class ShardedVerifyStep:
 
     def attend(self, target_q, target_k, target_v, stream=None):
         s = self.shape
-        kernels.sparse_decode(target_q, target_k, target_v, idx=self.idx, cnt=self.cnt, causal_base=s.context,
-                              rows_per_head=s.rows, pos_offset=self.lo, out=self.o_part, lse=self.l_part,
-                              out_dtype=torch.float32, status=self.status, workspace=self.ws_dec, stream=stream)
+        with _nvtx("sts.attend"):
+            kernels.sparse_decode(target_q, target_k, target_v, idx=self.idx, cnt=self.cnt, causal_base=s.context,
+                                  rows_per_head=s.rows, pos_offset=self.lo, out=self.o_part, lse=self.l_part,
+                                  out_dtype=torch.float32, status=self.status, workspace=self.ws_dec,
+                                  stream=stream)
         yield from self._merge(stream)
         return self.out, self.lse
 

@@ -38,6 +38,12 @@ from .kernels import Workspace
 from .sparsity import SparsityConfig
 
 
+def _nvtx(name):
+    """NVTX push/pop range around a stage's launches (``ncu --nvtx
+    --nvtx-include "sts.attend/"`` selects the stage; a no-op cost otherwise)."""
+    return torch.cuda.nvtx.range(name)
+
+
 @dataclass(frozen=True)
 class VerifyShape:
     batch: int
@@ -170,6 +176,10 @@ class STSVerifyStep:
     def capture(self, draft_q, draft_k, stream=None):
         """Stages 1-2: draft log-sum-exp and probability rows (score capture)."""
         s, R = self.shape, self.shape.rows
+        with _nvtx("sts.capture"):
+            self._capture(draft_q, draft_k, s, R, stream)
+
+    def _capture(self, draft_q, draft_k, s, R, stream):
         kernels.draft_lse(draft_q, draft_k, G=s.draft_group, R=R, base=s.context, n_keys=s.n_kv,
                           out=self.draft_lse, workspace=self.ws_draft, stream=stream)
         kernels.draft_probs(draft_q, draft_k, self.draft_lse, G=s.draft_group, R=R, base=s.context,
@@ -177,6 +187,10 @@ class STSVerifyStep:
 
     def build_masks(self, stream=None):
         """Stage 3: radix top-k selection (+ union for mode R)."""
+        with _nvtx("sts.select"):
+            self._build_masks(stream)
+
+    def _build_masks(self, stream):
         s, cfg = self.shape, self.cfg
         if self.mode == "S" and self._dist is not None:
             from .sharded import run_single
@@ -204,19 +218,21 @@ class STSVerifyStep:
         """Stage 4: gathered sparse flash-decode of the stacked rows."""
         s = self.shape
         causal = s.context if self.mode == "S" else -1
-        return kernels.sparse_decode(target_q, target_k, target_v, idx=self.idx, cnt=self.cnt,
-                                     member=self.member, causal_base=causal, rows_per_head=s.rows,
-                                     schedule=self.schedule, out=self.out, lse=self.lse, status=self.status,
-                                     workspace=self.ws_dec, stream=stream)
+        with _nvtx("sts.attend"):
+            return kernels.sparse_decode(target_q, target_k, target_v, idx=self.idx, cnt=self.cnt,
+                                         member=self.member, causal_base=causal, rows_per_head=s.rows,
+                                         schedule=self.schedule, out=self.out, lse=self.lse, status=self.status,
+                                         workspace=self.ws_dec, stream=stream)
 
     def attend_dense(self, target_q, target_k, target_v, out=None, lse=None, stream=None):
         """Dense baseline on the same kernel: every cached key, causal tail."""
         s = self.shape
-        return kernels.sparse_decode(target_q, target_k, target_v, n_dense=s.n_kv, causal_base=s.context,
-                                     rows_per_head=s.rows,
-                                     out=out if out is not None else self.out,
-                                     lse=lse if lse is not None else self.lse, status=self.status,
-                                     workspace=self.ws_dec, stream=stream)
+        with _nvtx("sts.dense"):
+            return kernels.sparse_decode(target_q, target_k, target_v, n_dense=s.n_kv, causal_base=s.context,
+                                         rows_per_head=s.rows,
+                                         out=out if out is not None else self.out,
+                                         lse=lse if lse is not None else self.lse, status=self.status,
+                                         workspace=self.ws_dec, stream=stream)
 
     def step(self, draft_q, draft_k, target_q, target_k, target_v, stream=None):
         self.capture(draft_q, draft_k, stream)

@@ -44,10 +44,11 @@ def summarize(report):
             v = to_float(d.get(m))
             unit = u.get(m, "")
             if v is not None and m.startswith("dram__bytes"):
-                mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+                mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(unit, 1)
                 v = v * mult * scale
             elif v is not None and m == "gpu__time_duration.sum":
-                mult = {"nsecond": 1, "usecond": 1e3, "msecond": 1e6}.get(unit, 1)
+                # -> microseconds
+                mult = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1, "us": 1, "msecond": 1e3, "ms": 1e3}.get(unit, 1)
                 v = v * mult * scale
             item[k] = None if v is None else round(v, 2)
         res.append(item)
