@@ -387,7 +387,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from paper_2605_15508_b200.verify import config_shape
+    from paper_2605_15508_b200.verify_step import config_shape
 
     shape = config_shape(args.config, **shape_overrides(args))
     budget = round(1.0 - args.sparsity, 10)
@@ -453,7 +453,7 @@ def run_single_gpu(args):
 
     from oracle import parity
     from paper_2605_15508_b200 import SparsityConfig, _lib
-    from paper_2605_15508_b200.verify import (STSVerifyStep, algorithmic_bytes, config_shape, random_mapping_table,
+    from paper_2605_15508_b200.verify_step import (STSVerifyStep, algorithmic_bytes, config_shape, random_mapping_table,
                                               synthetic_inputs)
 
     torch.cuda.set_device(0)
@@ -632,7 +632,7 @@ def side_measurements(args, shape, cfg, table, dq, dk, tq, tk, tv, flush, dev):
     import torch
 
     from paper_2605_15508_b200 import kernels
-    from paper_2605_15508_b200.verify import STSVerifyStep
+    from paper_2605_15508_b200.verify_step import STSVerifyStep
 
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     st = torch.cuda.current_stream()
@@ -699,7 +699,7 @@ def measure_sharded(args, world, rank, local, group_world=None):
     import torch.distributed as dist
 
     from paper_2605_15508_b200 import SparsityConfig, _lib, sharded
-    from paper_2605_15508_b200.verify import config_shape, random_mapping_table
+    from paper_2605_15508_b200.verify_step import config_shape, random_mapping_table
 
     dev = torch.device("cuda", local)
     lib = _lib.load()
@@ -880,7 +880,7 @@ def run_sharded(args, world, rank, local):
     import torch
     import torch.distributed as dist
 
-    from paper_2605_15508_b200.verify import algorithmic_bytes
+    from paper_2605_15508_b200.verify_step import algorithmic_bytes
 
     local = 0 if args.one_gpu else local
     torch.cuda.set_device(local)

@@ -248,6 +248,8 @@ STS_API int sts_topk_bitsets(const int32_t* idx_dev, int64_t idx_ld, const int32
 STS_API int sts_bitset_overlap(const uint32_t* a_dev, int32_t Ta, const uint32_t* b_dev, int32_t Tb, int64_t W,
                                unsigned long long* scores_dev, void* stream);
 
+#define STS_BLOCK_INCLUDE_SELF 0x1
+
 /* ------------------------------------------------------------------------
  * sts_block_attention_f64 — reference-exact masked block attention with
  * attention / score recording: the per-head loop of toymodel._run_block
@@ -261,6 +263,9 @@ STS_API int sts_bitset_overlap(const uint32_t* a_dev, int32_t Ta, const uint32_t
  *   idx/cnt    optional per-row key lists (ascending, <= the row's position);
  *              row (h, r) uses list list_of_row[h*m + r] (-1: dense causal),
  *              or list h*m + r when list_of_row is NULL; idx NULL: all dense
+ *   flags      STS_BLOCK_INCLUDE_SELF: a listed row also attends its own
+ *              position (the decode mask ∪ {current} of src/toymodel.py:467-475
+ *              and specdec._clamp_current, src/specdec.py:212-216)
  *   out_dev    fp32 [m][out_ld], head h at columns [h*d, (h+1)*d)
  *   probs_dev  nullable fp32 [heads*m][rec_ld]: the row's softmax weights over
  *              [0, start_pos+m) (zero outside its allowed set)
@@ -274,7 +279,7 @@ STS_API int sts_block_attention_f64(const float* q_dev, const float* k_cache_dev
                                     int64_t kv_head_stride, int64_t kv_row_stride, int32_t heads, int32_t m,
                                     int32_t d, int32_t start_pos, double scale, const int32_t* idx_dev,
                                     int64_t idx_ld, const int32_t* cnt_dev, const int32_t* list_of_row_dev,
-                                    float* out_dev, int64_t out_ld, float* probs_dev, float* scores_dev,
+                                    int32_t flags, float* out_dev, int64_t out_ld, float* probs_dev, float* scores_dev,
                                     int64_t rec_ld, int32_t* status_dev, void* stream);
 
 /* ------------------------------------------------------------------------

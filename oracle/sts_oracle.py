@@ -508,3 +508,78 @@ def find_head_mapping(samples, draft_heads, target_heads, k: int) -> dict:
         best = int(np.argmax(totals[th]))
         out[th] = (draft_heads[best], int(totals[th][best]))
     return out
+
+
+# ---------------------------------------------------------------------------
+# 5. toy-model weights (test fixtures for the model-level drop-in)
+# ---------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class OracleModelConfig:
+    """Fields of src/toymodel.py:38-57 ``ModelConfig``."""
+
+    layers: int
+    heads: int
+    head_dim: int
+    vocab: int
+    max_seq: int
+    page_size: int = 4
+    mlp_ratio: int = 4
+    seed: int = 0
+
+    @property
+    def hidden(self) -> int:
+        return self.heads * self.head_dim
+
+    def to_dict(self) -> dict:
+        return {k: getattr(self, k) for k in ("layers", "heads", "head_dim", "vocab", "max_seq", "page_size",
+                                               "mlp_ratio", "seed")}
+
+
+@dataclass
+class OracleModelWeights:
+    """Field names of src/toymodel.py:89-104 ``ModelWeights``."""
+
+    config: OracleModelConfig
+    token_emb: np.ndarray
+    pos_emb: np.ndarray
+    attn_norm: np.ndarray
+    wq: np.ndarray
+    wk: np.ndarray
+    wv: np.ndarray
+    wo: np.ndarray
+    mlp_norm: np.ndarray
+    w_up: np.ndarray
+    w_down: np.ndarray
+    final_norm: np.ndarray
+    lm_head: np.ndarray
+
+
+def init_model(config: OracleModelConfig) -> OracleModelWeights:
+    """src/toymodel.py:126-160: every parameter drawn, in field order, from one
+    PCG64 stream seeded with ``config.seed`` (numkit.prng_stream,
+    src/numkit.py:89-95); projections scaled by 1/sqrt(hidden), norms 1."""
+    rng = np.random.Generator(np.random.PCG64(config.seed))
+    h = config.hidden
+    mh = config.mlp_ratio * h
+    scale = 1.0 / math.sqrt(h)
+
+    def draw(*shape, s=1.0):
+        return (rng.standard_normal(shape) * s).astype(np.float32)
+
+    return OracleModelWeights(
+        config=config,
+        token_emb=draw(config.vocab, h),
+        pos_emb=draw(config.max_seq, h),
+        attn_norm=np.ones((config.layers, h), dtype=np.float32),
+        wq=draw(config.layers, h, h, s=scale),
+        wk=draw(config.layers, h, h, s=scale),
+        wv=draw(config.layers, h, h, s=scale),
+        wo=draw(config.layers, h, h, s=scale),
+        mlp_norm=np.ones((config.layers, h), dtype=np.float32),
+        w_up=draw(config.layers, h, mh, s=scale),
+        w_down=draw(config.layers, mh, h, s=scale),
+        final_norm=np.ones(h, dtype=np.float32),
+        lm_head=draw(h, config.vocab, s=scale),
+    )

@@ -48,6 +48,7 @@ struct BlockF64Params {
   int64_t idx_ld;
   const int32_t* cnt;
   const int32_t* list_of_row;
+  int flags;
   float* out;
   int64_t out_ld;
   float* probs;
@@ -102,6 +103,9 @@ __global__ void __launch_bounds__(BF_THREADS) block_attention_f64_kernel(BlockF6
       }
       w[j] = score(j);
     }
+    // rows always see their own position (forward_decode's mask ∪ {current},
+    // specdec._clamp_current): src/toymodel.py:467-475, src/specdec.py:212-216
+    if ((p.flags & STS_BLOCK_INCLUDE_SELF) && threadIdx.x == 0) w[pos] = score(pos);
   }
   __syncthreads();
 
@@ -155,7 +159,7 @@ extern "C" int sts_block_attention_f64(const float* q_dev, const float* k_cache_
                                        int64_t kv_head_stride, int64_t kv_row_stride, int32_t heads, int32_t m,
                                        int32_t d, int32_t start_pos, double scale, const int32_t* idx_dev,
                                        int64_t idx_ld, const int32_t* cnt_dev, const int32_t* list_of_row_dev,
-                                       float* out_dev, int64_t out_ld, float* probs_dev, float* scores_dev,
+                                       int32_t flags, float* out_dev, int64_t out_ld, float* probs_dev, float* scores_dev,
                                        int64_t rec_ld, int32_t* status_dev, void* stream) {
   STS_REQUIRE(heads >= 0 && m >= 0 && d >= 1 && d <= BF_THREADS && start_pos >= 0, STS_ERR_CONTRACT,
               "bad block shape (head_dim must be in [1, %d])", BF_THREADS);
@@ -189,6 +193,7 @@ extern "C" int sts_block_attention_f64(const float* q_dev, const float* k_cache_
   p.idx_ld = idx_ld;
   p.cnt = cnt_dev;
   p.list_of_row = list_of_row_dev;
+  p.flags = flags;
   p.out = out_dev;
   p.out_ld = out_ld;
   p.probs = probs_dev;

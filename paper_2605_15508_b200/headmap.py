@@ -37,6 +37,14 @@ class HeadMapping:
         except KeyError:
             raise ContractViolation(f"mapping has no entry for target head {target}") from None
 
+    def layer_distance_stats(self) -> dict:
+        """Distribution of |target layer - draft layer| (src/headmap.py:46-56)."""
+        dists = [abs(t[0] - d[0]) for t, (d, _) in self.entries.items()]
+        hist: dict = {}
+        for v in sorted(dists):
+            hist[str(v)] = hist.get(str(v), 0) + 1
+        return {"mean": float(np.mean(dists)), "max": int(max(dists)), "histogram": hist}
+
     def to_table(self, target_layers: int, target_heads: int, draft_heads: int) -> np.ndarray:
         """int32 [target_layers, target_heads] of flattened draft (layer*H_d + head)."""
         table = np.empty((target_layers, target_heads), dtype=np.int32)
@@ -73,13 +81,40 @@ class MappingSet:
     def nearest(self, budget: int) -> HeadMapping:
         return min(self.mappings, key=lambda m: (abs(m.k - budget), m.k))
 
+    @classmethod
+    def from_paths(cls, paths) -> "MappingSet":
+        """src/headmap.py:184-186."""
+        return cls([load_mapping(p) for p in paths])
+
 
 MAPPING_FORMAT_VERSION = 1
 
 
+def _config_dict(cfg) -> dict:
+    if hasattr(cfg, "to_dict"):
+        return cfg.to_dict()
+    return dict(cfg)
+
+
+def save_mapping(mapping: HeadMapping, path) -> None:
+    """Write a mapping as versioned JSON with layer-distance statistics
+    (src/headmap.py:128-143; byte-identical documents)."""
+    doc = {
+        "format_version": MAPPING_FORMAT_VERSION,
+        "k": mapping.k,
+        "trace_set_id": mapping.trace_set_id,
+        "draft_config": _config_dict(mapping.draft_config),
+        "target_config": _config_dict(mapping.target_config),
+        "entries": [[t[0], t[1], d[0], d[1], score] for t, (d, score) in sorted(mapping.entries.items())],
+        "layer_distance": mapping.layer_distance_stats(),
+    }
+    Path(path).write_text(json.dumps(doc, indent=2, sort_keys=True))
+
+
 def load_mapping(path) -> HeadMapping:
-    """Read the reference's mapping JSON (src/headmap.py:128-165): format_version
-    1, ``entries`` = [[target_layer, target_head, draft_layer, draft_head, score]]."""
+    """Read the reference's mapping JSON (src/headmap.py:146-165): format_version
+    1, ``entries`` = [[target_layer, target_head, draft_layer, draft_head, score]],
+    model configs as ``ModelConfig``."""
     path = Path(path)
     try:
         doc = json.loads(path.read_text())
@@ -91,8 +126,11 @@ def load_mapping(path) -> HeadMapping:
         entries = {(int(tl), int(th)): ((int(dl), int(dh)), int(score)) for tl, th, dl, dh, score in doc["entries"]}
     except (KeyError, TypeError, ValueError) as exc:
         raise InputError(f"bad mapping file {path}: {exc}") from exc
-    return HeadMapping(int(doc["k"]), entries, str(doc.get("trace_set_id", "")),
-                       doc.get("draft_config"), doc.get("target_config"))
+    from .model import ModelConfig
+
+    return HeadMapping(k=int(doc["k"]), entries=entries, trace_set_id=str(doc["trace_set_id"]),
+                       draft_config=ModelConfig.from_dict(doc["draft_config"]),
+                       target_config=ModelConfig.from_dict(doc["target_config"]))
 
 
 def find_head_mapping(ts, k: int) -> HeadMapping:

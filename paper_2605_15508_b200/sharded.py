@@ -39,7 +39,7 @@ from . import _lib, kernels
 from ._lib import call, ptr, stream_handle
 from .kernels import Workspace
 from .sparsity import SparsityConfig
-from .verify import VerifyShape, _nvtx
+from .verify_step import VerifyShape, _nvtx
 
 ALL_REDUCE_SUM = "all_reduce_sum"
 ALL_GATHER = "all_gather"
@@ -388,7 +388,7 @@ class ShardedVerifyStep:
 
 def local_synthetic_inputs(shape: VerifyShape, bounds, rank: int, device, dtype=torch.bfloat16, seed: int = 0,
                            head_groups: int = 1, head_group: int = 0):
-    """This rank's shard of synthetic_inputs (verify.py): the same seeded
+    """This rank's shard of synthetic_inputs (verify_step.py): the same seeded
     values a single GPU would hold at positions [lo, hi), generated shard by
     shard so no rank ever materialises the full cache (1M-token contexts)."""
     s = shape

@@ -5,7 +5,7 @@ same names, arguments, return types (dicts of int64 numpy index arrays,
 fp32 / fp64 numpy results) and exceptions, but every mask / page sum /
 attention is produced by libsts_b200.so kernels.  Inputs may be numpy arrays
 or torch tensors (CUDA tensors avoid the host->device copy).  For batched
-device-resident work use ``kernels`` / ``verify`` directly.
+device-resident work use ``kernels`` / ``verify_step`` directly.
 """
 
 from __future__ import annotations
@@ -57,8 +57,15 @@ class SparsityConfig:
         return self.scope == SCOPE_PREFILL_DECODE
 
     def select_kwargs(self) -> dict:
-        return dict(budget=self.budget, page_size=self.page_size, include_current=self.include_current,
-                    include_sink=self.include_sink, recent_window=self.recent_window)
+        return select_kwargs(self)
+
+
+def select_kwargs(cfg) -> dict:
+    """Selection arguments of any object with the reference ``SparsityConfig``
+    fields (this class, or ``specsparse.sparsity.SparsityConfig`` itself,
+    src/sparsity.py:33-59): the drop-in functions accept either."""
+    return dict(budget=cfg.budget, page_size=cfg.page_size, include_current=cfg.include_current,
+                include_sink=cfg.include_sink, recent_window=cfg.recent_window)
 
 
 def _device():
@@ -68,14 +75,20 @@ def _device():
 
 
 def _pack_rows(rows, dev):
-    """list of 1-D float rows -> (fp32 [R, maxlen] device tensor, int32 lengths)."""
+    """list of 1-D float rows -> (fp32 [R, maxlen] device tensor, int32 lengths),
+    packed on the host (or on the device for CUDA rows) and copied once."""
     lens = [int(r.shape[0]) for r in rows]
     width = max(max(lens), 1)
     width = -(-width // 4) * 4
-    buf = torch.zeros((len(rows), width), dtype=torch.float32, device=dev)
-    for i, r in enumerate(rows):
-        t = r if isinstance(r, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(r, dtype=np.float32))
-        buf[i, : lens[i]] = t.to(device=dev, dtype=torch.float32)
+    if all(isinstance(r, torch.Tensor) and r.is_cuda for r in rows):
+        buf = torch.zeros((len(rows), width), dtype=torch.float32, device=dev)
+        for i, r in enumerate(rows):
+            buf[i, : lens[i]] = r.to(dtype=torch.float32)
+    else:
+        host = np.zeros((len(rows), width), dtype=np.float32)
+        for i, r in enumerate(rows):
+            host[i, : lens[i]] = r.cpu().numpy() if isinstance(r, torch.Tensor) else np.asarray(r, dtype=np.float32)
+        buf = torch.from_numpy(host).to(dev)
     return buf, torch.tensor(lens, dtype=torch.int32, device=dev)
 
 
@@ -91,7 +104,7 @@ def select_rows(rows, cfg: SparsityConfig, tail_len: int = 0):
         return []
     dev = _device()
     buf, lens = _pack_rows(rows, dev)
-    idx, cnt = kernels.select_topk(buf, row_len=lens, tail_len=tail_len, **cfg.select_kwargs())
+    idx, cnt = kernels.select_topk(buf, row_len=lens, tail_len=tail_len, **select_kwargs(cfg))
     return _unpack(idx, cnt)
 
 

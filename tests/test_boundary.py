@@ -139,7 +139,7 @@ def test_mapping_table_and_nearest():
 
 
 def test_verify_shapes_and_algorithmic_bytes():
-    from paper_2605_15508_b200.verify import algorithmic_bytes, config_shape
+    from paper_2605_15508_b200.verify_step import algorithmic_bytes, config_shape
 
     s = config_shape("c2")
     assert s.target_units == 256 and s.rows == 5 and s.target_group == 4

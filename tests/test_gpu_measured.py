@@ -38,7 +38,7 @@ def _run_step(name, schedule=0, page_size=1, sample=32, **overrides):
     import torch
 
     from paper_2605_15508_b200 import SparsityConfig, _lib
-    from paper_2605_15508_b200.verify import STSVerifyStep, config_shape, random_mapping_table, synthetic_inputs
+    from paper_2605_15508_b200.verify_step import STSVerifyStep, config_shape, random_mapping_table, synthetic_inputs
 
     s = config_shape(name, **overrides)
     cfg = SparsityConfig(budget=0.1, page_size=page_size)
@@ -95,7 +95,7 @@ def test_c4_single_gpu_sharded_path(cuda_ok, free_gpu):
     import torch
 
     from paper_2605_15508_b200 import SparsityConfig, sharded
-    from paper_2605_15508_b200.verify import config_shape, random_mapping_table
+    from paper_2605_15508_b200.verify_step import config_shape, random_mapping_table
 
     s = config_shape("c4")
     cfg = SparsityConfig(budget=0.1)
@@ -117,7 +117,7 @@ def test_small_shapes_every_schedule(cuda_ok, schedule, gt, gamma):
     import torch
 
     from paper_2605_15508_b200 import SparsityConfig
-    from paper_2605_15508_b200.verify import STSVerifyStep, VerifyShape, random_mapping_table, synthetic_inputs
+    from paper_2605_15508_b200.verify_step import STSVerifyStep, VerifyShape, random_mapping_table, synthetic_inputs
 
     s = VerifyShape(batch=2, context=2000, gamma=gamma, target_layers=2, target_q_heads=2 * gt, target_kv_heads=2,
                     head_dim=128, draft_layers=2, draft_q_heads=8, draft_kv_heads=2, draft_head_dim=64)

@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 
 
 def _small_shape(**kw):
-    from paper_2605_15508_b200.verify import VerifyShape
+    from paper_2605_15508_b200.verify_step import VerifyShape
 
     d = dict(batch=2, context=1500, gamma=4, target_layers=3, target_q_heads=8, target_kv_heads=2, head_dim=128,
              draft_layers=2, draft_q_heads=8, draft_kv_heads=2, draft_head_dim=64)
@@ -86,7 +86,7 @@ def test_verify_step_mode_s(cuda_ok, ps, sink, win, long_rows):
     import torch
 
     from paper_2605_15508_b200 import SparsityConfig
-    from paper_2605_15508_b200.verify import STSVerifyStep, random_mapping_table, synthetic_inputs
+    from paper_2605_15508_b200.verify_step import STSVerifyStep, random_mapping_table, synthetic_inputs
 
     s = _small_shape()
     cfg = SparsityConfig(budget=0.1, page_size=ps, include_sink=sink, recent_window=win)
@@ -120,7 +120,7 @@ def test_verify_step_mode_r_reference_masks(cuda_ok):
     import torch
 
     from paper_2605_15508_b200 import SparsityConfig
-    from paper_2605_15508_b200.verify import STSVerifyStep, random_mapping_table, synthetic_inputs
+    from paper_2605_15508_b200.verify_step import STSVerifyStep, random_mapping_table, synthetic_inputs
 
     s = _small_shape(batch=1)
     cfg = SparsityConfig(budget=0.1)
@@ -162,7 +162,7 @@ def test_host_buffer_api_matches_device_path(cuda_ok):
     import torch
 
     from paper_2605_15508_b200 import SparsityConfig
-    from paper_2605_15508_b200.verify import STSVerifyStep, random_mapping_table, synthetic_inputs
+    from paper_2605_15508_b200.verify_step import STSVerifyStep, random_mapping_table, synthetic_inputs
 
     s = _small_shape()
     step = STSVerifyStep(s, SparsityConfig(budget=0.1), random_mapping_table(s, seed=2), mode="S")

@@ -116,7 +116,7 @@ def test_sharded_verify_step_matches_oracle(cuda_ok):
     import torch
 
     from paper_2605_15508_b200 import SparsityConfig, kernels, sharded
-    from paper_2605_15508_b200.verify import VerifyShape, random_mapping_table, synthetic_inputs
+    from paper_2605_15508_b200.verify_step import VerifyShape, random_mapping_table, synthetic_inputs
 
     s = VerifyShape(batch=1, context=3000, gamma=4, target_layers=2, target_q_heads=8, target_kv_heads=2,
                     head_dim=128, draft_layers=2, draft_q_heads=8, draft_kv_heads=2, draft_head_dim=64)
@@ -164,7 +164,7 @@ def test_p2p_merge_matches_gather_merge(cuda_ok):
     import torch
 
     from paper_2605_15508_b200 import SparsityConfig, sharded
-    from paper_2605_15508_b200.verify import VerifyShape, random_mapping_table, synthetic_inputs
+    from paper_2605_15508_b200.verify_step import VerifyShape, random_mapping_table, synthetic_inputs
 
     s = VerifyShape(batch=1, context=2500, gamma=4, target_layers=2, target_q_heads=8, target_kv_heads=2,
                     head_dim=128, draft_layers=2, draft_q_heads=8, draft_kv_heads=2, draft_head_dim=64)
@@ -192,7 +192,7 @@ def test_heads_times_sequence_sharding(cuda_ok):
     import torch
 
     from paper_2605_15508_b200 import SparsityConfig, sharded
-    from paper_2605_15508_b200.verify import VerifyShape, random_mapping_table, synthetic_inputs
+    from paper_2605_15508_b200.verify_step import VerifyShape, random_mapping_table, synthetic_inputs
 
     s = VerifyShape(batch=2, context=1800, gamma=4, target_layers=2, target_q_heads=8, target_kv_heads=4,
                     head_dim=128, draft_layers=2, draft_q_heads=8, draft_kv_heads=2, draft_head_dim=64)

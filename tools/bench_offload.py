@@ -11,7 +11,7 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2605_15508_b200 import SparsityConfig, kernels  # noqa: E402
-from paper_2605_15508_b200.verify import (STSVerifyStep, algorithmic_bytes, config_shape,  # noqa: E402
+from paper_2605_15508_b200.verify_step import (STSVerifyStep, algorithmic_bytes, config_shape,  # noqa: E402
                                           random_mapping_table, synthetic_inputs)
 
 layers = int(sys.argv[1]) if len(sys.argv) > 1 else 8

@@ -11,7 +11,7 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2605_15508_b200 import SparsityConfig  # noqa: E402
-from paper_2605_15508_b200.verify import (STSVerifyStep, config_shape, random_mapping_table,  # noqa: E402
+from paper_2605_15508_b200.verify_step import (STSVerifyStep, config_shape, random_mapping_table,  # noqa: E402
                                           synthetic_inputs)
 
 ap = argparse.ArgumentParser()

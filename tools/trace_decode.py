@@ -12,7 +12,7 @@ import torch
 
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 from paper_2605_15508_b200 import SparsityConfig, _lib  # noqa: E402
-from paper_2605_15508_b200.verify import STSVerifyStep, config_shape, random_mapping_table, synthetic_inputs  # noqa: E402
+from paper_2605_15508_b200.verify_step import STSVerifyStep, config_shape, random_mapping_table, synthetic_inputs  # noqa: E402
 
 ctx = int(sys.argv[1]) if len(sys.argv) > 1 else 32768
 lib = _lib.load()
