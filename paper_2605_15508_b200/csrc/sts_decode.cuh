@@ -61,6 +61,13 @@ int lse_merge_launch(const float* o_part, const float* lse_part, int nparts, int
                      int out_dtype, void* out, float* lse_out, cudaStream_t st);
 
 int auto_splits(int64_t units, int64_t keys_per_unit);
+
+// draft-score capture on TMA + tcgen05 (sts_capture.cu): mode 0 = LSE,
+// 1 = probabilities (probs_mode 0 S / 1 R / 2 raw scores)
+size_t capture_workspace_bytes(int64_t units, int M);
+int capture_launch(int mode, const void* q, const void* k, int64_t kv_unit_stride, int64_t units, int G, int R, int d,
+                   int n_keys, int pos_offset, int base, float scale, float* lse, const float* lse_in, int probs_mode,
+                   float* out, int64_t out_ld, void* ws, size_t ws_bytes, cudaStream_t st);
 // bf16 decode of the stacked verification rows (sts_verify_decode.cu): the
 // main kernel, then the merge of units split over several schedule ranges
 int verify_decode_launch(int mode, DecodeParams& p, cudaStream_t st);

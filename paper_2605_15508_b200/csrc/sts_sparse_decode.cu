@@ -292,30 +292,9 @@ extern "C" int32_t sts_auto_splits(int64_t units, int64_t keys_per_unit) {
 // ---------------------------------------------------------------------------
 // draft-score capture
 // ---------------------------------------------------------------------------
-static void draft_params(DecodeParams& p, const void* q_dev, const void* k_cache_dev,
-                         int64_t kv_unit_stride, int64_t units, int32_t G, int32_t R, int32_t d,
-                         int32_t n_keys, int32_t pos_offset, int32_t base, float scale) {
-  memset(&p, 0, sizeof(p));
-  p.q = q_dev;
-  p.k = k_cache_dev;
-  p.v = nullptr;
-  p.kv_stride = kv_unit_stride;
-  p.row_stride = d;
-  p.units = units;
-  p.M = G * R;
-  p.d = d;
-  p.idx = nullptr;
-  p.n_dense = n_keys;
-  p.member = nullptr;
-  p.causal_base = base;
-  p.rows_per_head = R;
-  p.pos_offset = pos_offset;
-  p.scale = scale;
-}
-
 extern "C" size_t sts_draft_workspace_bytes(int64_t units, int32_t GR, int32_t n_keys) {
   (void)n_keys;
-  return stream_workspace_bytes(MODE_LSE, units, GR, 64);
+  return capture_workspace_bytes(units, GR);
 }
 
 extern "C" int sts_draft_lse(int32_t dtype, const void* q_dev, const void* k_cache_dev,
@@ -329,11 +308,8 @@ extern "C" int sts_draft_lse(int32_t dtype, const void* q_dev, const void* k_cac
   STS_REQUIRE(q_dev && k_cache_dev && lse_dev, STS_ERR_CONTRACT, "null buffer");
   if (units == 0) return STS_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  DecodeParams p;
-  draft_params(p, q_dev, k_cache_dev, kv_unit_stride, units, G, R, d, n_keys, pos_offset, base, scale);
-  p.splits = 1;
-  p.lse = lse_dev;
-  return stream_launch(MODE_LSE, p, workspace_dev, workspace_bytes, st);
+  return capture_launch(0, q_dev, k_cache_dev, kv_unit_stride, units, G, R, d, n_keys, pos_offset, base, scale,
+                        lse_dev, nullptr, 0, nullptr, 0, workspace_dev, workspace_bytes, st);
 }
 
 extern "C" int sts_draft_probs(int32_t dtype, const void* q_dev, const void* k_cache_dev,
@@ -349,14 +325,8 @@ extern "C" int sts_draft_probs(int32_t dtype, const void* q_dev, const void* k_c
   STS_REQUIRE(out_ld >= n_keys, STS_ERR_CONTRACT, "out_ld must be >= n_keys");
   if (units == 0) return STS_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  DecodeParams p;
-  draft_params(p, q_dev, k_cache_dev, kv_unit_stride, units, G, R, d, n_keys, pos_offset, base, scale);
-  p.splits = 1;
-  p.lse_in = lse_dev;
-  p.probs_out = out_dev;
-  p.out_ld = out_ld;
-  p.probs_mode = mode;
-  return stream_launch(MODE_PROBS, p, nullptr, 0, st);
+  return capture_launch(1, q_dev, k_cache_dev, kv_unit_stride, units, G, R, d, n_keys, pos_offset, base, scale,
+                        nullptr, lse_dev, mode, out_dev, out_ld, nullptr, 0, st);
 }
 
 extern "C" int sts_draft_scores(int32_t dtype, const void* q_dev, const void* k_cache_dev,
@@ -370,12 +340,6 @@ extern "C" int sts_draft_scores(int32_t dtype, const void* q_dev, const void* k_
   STS_REQUIRE(out_ld >= n_keys, STS_ERR_CONTRACT, "out_ld must be >= n_keys");
   if (units == 0) return STS_OK;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  DecodeParams p;
-  draft_params(p, q_dev, k_cache_dev, kv_unit_stride, units, G, R, d, n_keys, pos_offset, base, scale);
-  p.splits = 1;
-  p.lse_in = nullptr;
-  p.probs_out = out_dev;
-  p.out_ld = out_ld;
-  p.probs_mode = 2;
-  return stream_launch(MODE_PROBS, p, nullptr, 0, st);
+  return capture_launch(1, q_dev, k_cache_dev, kv_unit_stride, units, G, R, d, n_keys, pos_offset, base, scale,
+                        nullptr, nullptr, 2, out_dev, out_ld, nullptr, 0, st);
 }

@@ -982,8 +982,10 @@ extern "C" STS_API int sts_debug_trace(void* host, size_t bytes) {
 
 int verify_decode_launch(int mode, DecodeParams& p, cudaStream_t st) {
   if (mode == MODE_DECODE) return verify_dispatch_d<MODE_DECODE>(p, st);
-  if (mode == MODE_LSE) return verify_dispatch_d<MODE_LSE>(p, st);
-  return verify_dispatch_d<MODE_PROBS>(p, st);
+  // the draft capture runs on TMA + tcgen05 (sts_capture.cu); the LSE / PROBS
+  // instantiations of this kernel are not built
+  set_error("verify_decode_launch: mode %d is served by sts_capture.cu", mode);
+  return STS_ERR_CONTRACT;
 }
 
 }  // namespace sts
