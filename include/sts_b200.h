@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define STS_ABI_VERSION 4
+#define STS_ABI_VERSION 5
 
 #define STS_OK 0
 #define STS_ERR_INPUT 1
@@ -281,6 +281,35 @@ STS_API int sts_block_attention_f64(const float* q_dev, const float* k_cache_dev
                                     int64_t idx_ld, const int32_t* cnt_dev, const int32_t* list_of_row_dev,
                                     int32_t flags, float* out_dev, int64_t out_ld, float* probs_dev, float* scores_dev,
                                     int64_t rec_ld, int32_t* status_dev, void* stream);
+
+/* ------------------------------------------------------------------------
+ * Mask-driven KV prefetch into an HBM page pool: the
+ * strategies of src/offloadsim.py:153-211 ("on_demand" / "prefetch" with
+ * lookahead), pages as in src/specdec.py:236-255 (page = position / P).
+ *
+ * sts_page_plan — per unit, the ascending unique pages of its key list
+ *   (pages_dev[u][0 .. npages_dev[u]), at most pages_ld; overflow sets
+ *   STS_DEV_IDX_CAPACITY) and the list re-expressed as rows of the unit's
+ *   pool slice: idx_pool[u][i] = rank(page(idx[u][i])) * P + idx[u][i] % P.
+ *   Pages >= tail_page0 (the in-block tail; -1: none) take the fixed ranks
+ *   tail_rank0 + (page - tail_page0) in every unit, so pool rows of the tail
+ *   are position - (tail_page0 - tail_rank0) * P for all units and the
+ *   decode's causal test runs with causal_base' = base - that shift.
+ * sts_page_copy — copies the planned pages of units [unit_begin, unit_end)
+ *   from K/V in pinned, device-mapped host memory ([unit][row][d], strides in
+ *   elements) into the pool ([unit][pages_ld * P][d]), with `ctas` CTAs (one
+ *   warp per page, 16-byte loads over the host link) so it runs beside the
+ *   attention of units already resident.
+ * ---------------------------------------------------------------------- */
+STS_API int sts_page_plan(const int32_t* idx_dev, int64_t idx_ld, const int32_t* cnt_dev, int64_t units,
+                          int32_t page_size, int32_t tail_page0, int32_t tail_rank0, int32_t* pages_dev,
+                          int64_t pages_ld, int32_t* npages_dev, int32_t* idx_pool_dev, int32_t* status_dev,
+                          void* stream);
+STS_API int sts_page_copy(const void* host_k, const void* host_v, int64_t host_unit_stride,
+                          int64_t host_row_stride, int32_t n_rows_host, void* pool_k, void* pool_v,
+                          int64_t pool_unit_stride, int32_t d, int32_t elem_bytes, const int32_t* pages_dev,
+                          int64_t pages_ld, const int32_t* npages_dev, int64_t unit_begin, int64_t unit_end,
+                          int32_t page_size, int32_t tail_page0, int32_t tail_rank0, int32_t ctas, void* stream);
 
 /* ------------------------------------------------------------------------
  * Sequence-sharded selection (context-parallel decode): the
