@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define STS_ABI_VERSION 5
+#define STS_ABI_VERSION 6
 
 #define STS_OK 0
 #define STS_ERR_INPUT 1
@@ -310,6 +310,27 @@ STS_API int sts_page_copy(const void* host_k, const void* host_v, int64_t host_u
                           int64_t pool_unit_stride, int32_t d, int32_t elem_bytes, const int32_t* pages_dev,
                           int64_t pages_ld, const int32_t* npages_dev, int64_t unit_begin, int64_t unit_end,
                           int32_t page_size, int32_t tail_page0, int32_t tail_rank0, int32_t ctas, void* stream);
+
+/* ------------------------------------------------------------------------
+ * sts_prefill_blocksparse — block-sparse prefill attention on tcgen05
+ * (STS-PD): the masked prefill of toymodel._run_block
+ * (src/toymodel.py:315-348 via forward_prefill(masks=...) :370-399) with
+ * tile-granular masks: per (kv-head, 128-row query tile T) the committed
+ * 64-key blocks a selection picked (all before the tile) plus the tile's
+ * diagonal blocks under the causal mask; row t sees the selected keys and
+ * the diagonal keys <= t.  idx/cnt: per (kv-head, tile) row hv*tiles + T, the
+ * selected committed tokens as whole 64-key blocks, ascending (page-mode
+ * sts_select_topk output, page_size 64, no extras); idx NULL = dense causal.
+ *   q_dev [heads_q][n][d], k/v_dev [heads_kv][n][d] bf16 (head / row strides
+ *   in elements, rows 16-byte aligned); out_dev [heads_q][n][d] bf16.
+ * d in {64, 128}.  CTA = (tile, q-head): TMA tiles, S = Q.K^T and O += P.V
+ * on tcgen05 with TMEM accumulators, softmax warps one thread per row.
+ * ---------------------------------------------------------------------- */
+STS_API int sts_prefill_blocksparse(const void* q_dev, const void* k_dev, const void* v_dev, int32_t heads_q,
+                                    int32_t heads_kv, int32_t n, int32_t d, int64_t q_head_stride,
+                                    int64_t kv_head_stride, int64_t row_stride, float scale, const int32_t* idx_dev,
+                                    int64_t idx_ld, const int32_t* cnt_dev, void* out_dev, int32_t* status_dev,
+                                    void* stream);
 
 /* ------------------------------------------------------------------------
  * Sequence-sharded selection (context-parallel decode): the

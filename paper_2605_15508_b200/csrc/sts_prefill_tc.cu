@@ -1,0 +1,470 @@
+// sts_prefill_tc.cu — block-sparse prefill attention on tcgen05 (STS-PD,
+// SURVEY §8f row 1): masked prefill of the reference (`forward_prefill(masks=
+// ...)` -> `_run_block`, src/toymodel.py:315-348, :370-399) with the masks of
+// `draft_masks_prefill` (src/sparsity.py:122-130) made tile-granular:
+//
+//   one key-block set per (kv-head, 128-row query tile): the committed blocks
+//   (64 keys, all before the tile) the selection picked for the tile, plus the
+//   tile's two diagonal blocks under the causal mask.  Row t of tile T sees
+//   the selected committed keys and the diagonal keys <= t.
+//
+// CTA = (q-head, query tile), 128 rows = the 128 TMEM lanes.  Warp roles:
+//   warp 0   TMA producer: Q tile once, then K and V blocks of the list
+//            (128B swizzle; ring of STAGES (K, V) blocks)
+//   warp 1   MMA issuer: S_j = Q.K_j^T (M=128 rows, N=64 keys, K=d) into one of
+//            two TMEM S slots; O += P_j.V_j (M=128, N=d, K=64; V as an
+//            MN-major operand) into the TMEM O accumulator
+//   warps 2-5 softmax, thread = query row: tcgen05.ld of its S row, causal
+//            mask on diagonal blocks, online max with lazy rescale (O rows in
+//            TMEM rescaled only when the max grows by > 2^8), P in bf16 to
+//            shared memory (swizzled K-major A operand), row sums in fp32;
+//            at the end O / l to global (bf16)
+#include <cuda.h>
+
+#include "sts_decode.cuh"
+
+namespace sts {
+namespace {
+
+constexpr int PF_ROWS = 128;   // query tile = MMA M = TMEM lanes
+constexpr int PF_BLK = 64;     // keys per block = MMA N of S, K of PV
+constexpr int PF_STAGES = 4;
+constexpr int PF_THREADS = 192;
+constexpr float PF_RESCALE = 8.f;  // log2 growth of the row max that forces an O rescale
+
+__device__ __forceinline__ void pf_mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void pf_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void pf_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void pf_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void pf_tma3(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void pf_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void pf_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void pf_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void pf_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+          d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void pf_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void pf_st32(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])),
+      "r"(__float_as_uint(v[11])), "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])),
+      "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15])), "r"(__float_as_uint(v[16])),
+      "r"(__float_as_uint(v[17])), "r"(__float_as_uint(v[18])), "r"(__float_as_uint(v[19])),
+      "r"(__float_as_uint(v[20])), "r"(__float_as_uint(v[21])), "r"(__float_as_uint(v[22])),
+      "r"(__float_as_uint(v[23])), "r"(__float_as_uint(v[24])), "r"(__float_as_uint(v[25])),
+      "r"(__float_as_uint(v[26])), "r"(__float_as_uint(v[27])), "r"(__float_as_uint(v[28])),
+      "r"(__float_as_uint(v[29])), "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
+      : "memory");
+}
+__device__ __forceinline__ void pf_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void pf_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+
+// K-major operand, 128B swizzle: 8-row groups of 1024 B (SBO), LBO unused
+__device__ __forceinline__ uint64_t pf_desc_k(const void* p) {
+  const uint64_t a = smem_u32(p);
+  return ((a >> 4) & 0x3FFFull) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+// MN-major operand, 128B swizzle: atoms of 64 elements (MN) x 8 rows (K);
+// LBO = bytes between MN atoms, SBO = bytes between 8-row K groups
+__device__ __forceinline__ uint64_t pf_desc_mn(const void* p, uint32_t lbo, uint32_t sbo) {
+  const uint64_t a = smem_u32(p);
+  return ((a >> 4) & 0x3FFFull) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) | ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) |
+         (1ull << 46) | (2ull << 61);
+}
+__host__ __device__ constexpr uint32_t pf_idesc(int M, int N, bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+struct PfParams {
+  int n;             // keys = query rows of the layer
+  int heads_q, group;  // q-heads, q-heads per kv-head
+  int tiles;         // ceil(n / 128)
+  float scale;
+  const int32_t* idx;  // [kv_heads * tiles][idx_ld] committed tokens (whole 64-key blocks, ascending); null = dense
+  int64_t idx_ld;
+  const int32_t* cnt;
+  __nv_bfloat16* out;  // [heads_q][n][d]
+  int32_t* status;
+};
+
+template <int D>
+struct PfLayout {
+  static constexpr int SLABS = D / 64;
+  static constexpr int Q_BYTES = PF_ROWS * 128 * SLABS;
+  static constexpr int KB_BYTES = PF_BLK * 128 * SLABS;     // one K block (= one V block)
+  static constexpr int P_BYTES = PF_ROWS * PF_BLK * 2;       // bf16 P tile, 128B rows
+  static constexpr int OFF_Q = 0;
+  static constexpr int OFF_K = OFF_Q + Q_BYTES;
+  static constexpr int OFF_V = OFF_K + PF_STAGES * KB_BYTES;
+  static constexpr int OFF_P = OFF_V + PF_STAGES * KB_BYTES;
+  static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
+  // full[S], empty[S], sfull[2], sempty[2], pfull[2], odone[2], qfull
+  static constexpr int NBAR = 2 * PF_STAGES + 9;
+  static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
+  static constexpr int S_COLS = PF_BLK;                       // per S slot
+  static constexpr int O_COL = 2 * PF_BLK;                    // O after the two S slots
+  static constexpr int TMEM_COLS = 2 * PF_BLK + D <= 256 ? 256 : 512;
+};
+
+// the tile's block list: committed blocks from the selection, then the diagonal
+__device__ __forceinline__ int pf_nblocks(const PfParams& p, int kvh, int T, int& ncommit) {
+  const int diag0 = 2 * T;
+  const int nblk_total = (p.n + PF_BLK - 1) / PF_BLK;
+  const int ndiag = min(2, nblk_total - diag0);
+  if (!p.idx) {
+    ncommit = diag0;
+  } else {
+    ncommit = p.cnt[(int64_t)kvh * p.tiles + T] / PF_BLK;
+  }
+  return ncommit + ndiag;
+}
+__device__ __forceinline__ int pf_block(const PfParams& p, int kvh, int T, int ncommit, int j) {
+  if (j >= ncommit) return 2 * T + (j - ncommit);
+  if (!p.idx) return j;
+  return p.idx[((int64_t)kvh * p.tiles + T) * p.idx_ld + (int64_t)j * PF_BLK] / PF_BLK;
+}
+
+template <int D>
+__global__ void __launch_bounds__(PF_THREADS, 1) prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap,
+                                                                   const __grid_constant__ CUtensorMap kmap,
+                                                                   const __grid_constant__ CUtensorMap vmap,
+                                                                   PfParams p) {
+  using L = PfLayout<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::OFF_BAR);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + PF_STAGES;
+  uint64_t* sfull = bars + 2 * PF_STAGES;
+  uint64_t* sempty = sfull + 2;
+  uint64_t* pfull = sempty + 2;
+  uint64_t* odone = pfull + 2;  // odone[j & 1]: PV_j landed in O (per buffer: waits stay one phase behind)
+  uint64_t* qfull = odone + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::NBAR);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // heavy (late) tiles first: tile index descending across the grid
+  const int T = p.tiles - 1 - (int)blockIdx.x;
+  const int hq = blockIdx.y;
+  const int kvh = hq / p.group;
+  int ncommit;
+  const int nb = pf_nblocks(p, kvh, T, ncommit);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < PF_STAGES; ++i) {
+      pf_mbar_init(&full[i], 1);
+      pf_mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      pf_mbar_init(&sfull[i], 1);
+      pf_mbar_init(&sempty[i], 128);
+      pf_mbar_init(&pfull[i], 128);
+    }
+    pf_mbar_init(&odone[0], 1);
+    pf_mbar_init(&odone[1], 1);
+    pf_mbar_init(qfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(tmem_slot)),
+                 "n"(L::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  pf_fence_before();
+  __syncthreads();
+  pf_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      pf_expect_tx(qfull, L::Q_BYTES);
+#pragma unroll
+      for (int s = 0; s < L::SLABS; ++s)
+        pf_tma3(smem + L::OFF_Q + s * PF_ROWS * 128, &qmap, qfull, s * 64, T * PF_ROWS, hq);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int j = 0; j < nb; ++j) {
+        const int b = pf_block(p, kvh, T, ncommit, j);
+        pf_wait(&empty[stage], phase ^ 1);
+        pf_expect_tx(&full[stage], 2 * L::KB_BYTES);
+#pragma unroll
+        for (int s = 0; s < L::SLABS; ++s) {
+          pf_tma3(smem + L::OFF_K + stage * L::KB_BYTES + s * PF_BLK * 128, &kmap, &full[stage], s * 64, b * PF_BLK,
+                  kvh);
+          pf_tma3(smem + L::OFF_V + stage * L::KB_BYTES + s * PF_BLK * 128, &vmap, &full[stage], s * 64, b * PF_BLK,
+                  kvh);
+        }
+        if (++stage == PF_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t id_s = pf_idesc(PF_ROWS, PF_BLK, false);
+      constexpr uint32_t id_o = pf_idesc(PF_ROWS, D, true);
+      pf_wait(qfull, 0);
+      pf_fence_after();
+      // S_j for j = 0, then per j: S_{j+1} (overlaps softmax j), PV_j
+      auto issue_s = [&](int j) {
+        const int stage = j % PF_STAGES;
+        const uint32_t slot = j & 1;
+        pf_wait(&sempty[slot], ((j >> 1) & 1) ^ 1);
+        pf_wait(&full[stage], (j / PF_STAGES) & 1);
+        pf_fence_after();
+        const uint32_t d_tmem = tmem + slot * L::S_COLS;
+#pragma unroll
+        for (int s = 0; s < L::SLABS; ++s) {
+          const uint64_t ad = pf_desc_k(smem + L::OFF_Q + s * PF_ROWS * 128);
+          const uint64_t bd = pf_desc_k(smem + L::OFF_K + stage * L::KB_BYTES + s * PF_BLK * 128);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) pf_mma(d_tmem, ad + 2 * k, bd + 2 * k, id_s, (s | k) != 0);
+        }
+        pf_commit(&sfull[slot]);
+      };
+      if (nb > 0) issue_s(0);
+      for (int j = 0; j < nb; ++j) {
+        if (j + 1 < nb) issue_s(j + 1);
+        const int stage = j % PF_STAGES;
+        pf_wait(&pfull[j & 1], (j >> 1) & 1);
+        pf_fence_after();
+        const uint64_t ad = pf_desc_k(smem + L::OFF_P + (j & 1) * L::P_BYTES);
+        // V block [64 keys][D] as an MN-major B operand: MN atoms (64 d) are
+        // the slabs (LBO), K groups of 8 keys are 1024 B apart (SBO)
+        const uint64_t bd = pf_desc_mn(smem + L::OFF_V + stage * L::KB_BYTES, PF_BLK * 128, 1024);
+#pragma unroll
+        for (int k = 0; k < PF_BLK / 16; ++k)
+          pf_mma(tmem + L::O_COL, ad + 2 * k, bd + (uint64_t)((16 * 128) >> 4) * k, id_o, (j | k) != 0);
+        pf_commit(&empty[stage]);   // K and V of this block no longer read
+        pf_commit(&odone[j & 1]);   // O holds blocks 0..j (also frees P buffer j & 1)
+      }
+    }
+  } else {
+    // ===== softmax: thread = query row =====
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;       // row within the tile (TMEM lane)
+    const int row = T * PF_ROWS + r;      // query position
+    const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const float sl2 = p.scale * LOG2E;
+    float m = -INFINITY, l = 0.f;
+    for (int j = 0; j < nb; ++j) {
+      const uint32_t slot = j & 1;
+      const int b = pf_block(p, kvh, T, ncommit, j);
+      pf_wait(&sfull[slot], (j >> 1) & 1);
+      pf_fence_after();
+      float s[PF_BLK];
+      pf_ld32(tmem + lane_off + slot * L::S_COLS, s);
+      pf_ld32(tmem + lane_off + slot * L::S_COLS + 32, s + 32);
+      pf_wait_ld();
+      pf_fence_before();
+      pf_arrive(&sempty[slot]);
+      const bool diag = j >= ncommit;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < PF_BLK; ++c) {
+        const int key = b * PF_BLK + c;
+        const bool ok = !diag || (key <= row && key < p.n);
+        s[c] = ok ? s[c] * sl2 : -INFINITY;
+        mx = fmaxf(mx, s[c]);
+      }
+      // P buffer j&1 was read by PV_{j-2}
+      if (j >= 2) pf_wait(&odone[j & 1], ((j - 2) >> 1) & 1);
+      // lazy rescale, warp-uniform (tcgen05.ld/st are warp-collective): rows
+      // whose max grew by > 2^8 rescale their O row after PV_{j-1} landed
+      const bool need = mx > m + PF_RESCALE;
+      if (__any_sync(0xffffffffu, need)) {
+        if (j == 0) {
+          m = mx;  // first block: every row sees key 128T, O is overwritten by PV_0
+          l = 0.f;
+        } else {
+          pf_wait(&odone[(j - 1) & 1], ((j - 1) >> 1) & 1);
+          pf_fence_after();
+          const float f = need ? fast_exp2(m - mx) : 1.f;
+#pragma unroll
+          for (int c0 = 0; c0 < D; c0 += 32) {
+            float o[32];
+            pf_ld32(tmem + lane_off + L::O_COL + c0, o);
+            pf_wait_ld();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) o[c] *= f;
+            pf_st32(tmem + lane_off + L::O_COL + c0, o);
+          }
+          pf_wait_st();
+          l *= f;
+          if (need) m = mx;
+        }
+      }
+      // P = 2^(s - m) in bf16, K-major 128B-swizzled rows of the A operand
+      uint8_t* prow = smem + L::OFF_P + (j & 1) * L::P_BYTES + r * 128;
+      float rs = 0.f;
+#pragma unroll
+      for (int c8 = 0; c8 < PF_BLK / 8; ++c8) {
+        uint32_t w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float a0 = fast_exp2(s[c8 * 8 + 2 * e] - m), a1 = fast_exp2(s[c8 * 8 + 2 * e + 1] - m);
+          const __nv_bfloat162 h = __floats2bfloat162_rn(a0, a1);
+          rs += __low2float(h) + __high2float(h);  // the row sum of what the MMA multiplies
+          w[e] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+        *reinterpret_cast<uint4*>(prow + ((c8 ^ (r & 7)) * 16)) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      l += rs;
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // P visible to the tensor core
+      pf_fence_before();
+      pf_arrive(&pfull[j & 1]);
+    }
+    // epilogue: O / l after the last PV
+    if (nb > 0) pf_wait(&odone[(nb - 1) & 1], ((nb - 1) >> 1) & 1);
+    pf_fence_after();
+    const float inv = l > 0.f ? 1.f / l : 0.f;
+    __nv_bfloat16* orow = p.out + ((int64_t)hq * p.n + row) * D;
+#pragma unroll
+    for (int c0 = 0; c0 < D; c0 += 32) {
+      float o[32];
+      pf_ld32(tmem + lane_off + L::O_COL + c0, o);  // warp-collective: every row loads
+      pf_wait_ld();
+      if (row < p.n) {
+#pragma unroll
+        for (int c = 0; c < 32; c += 8) {
+          uint4 w;
+          w.x = pack_bf16(o[c] * inv, o[c + 1] * inv);
+          w.y = pack_bf16(o[c + 2] * inv, o[c + 3] * inv);
+          w.z = pack_bf16(o[c + 4] * inv, o[c + 5] * inv);
+          w.w = pack_bf16(o[c + 6] * inv, o[c + 7] * inv);
+          *reinterpret_cast<uint4*>(orow + c0 + c) = w;
+        }
+      }
+    }
+    if (row < p.n && !(l > 0.f)) set_status(p.status, STS_DEV_EMPTY_ROW);
+  }
+  pf_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    pf_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(L::TMEM_COLS));
+  }
+}
+
+typedef CUresult (*PfEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                               const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                               CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int pf_map(CUtensorMap* map, const void* base, int64_t heads, int64_t rows, int d, int64_t head_stride,
+           int64_t row_stride, int box_rows) {
+  static PfEncodeFn fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PfEncodeFn>(f);
+  }
+  STS_REQUIRE(fn, STS_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[3] = {(cuuint64_t)d, (cuuint64_t)rows, (cuuint64_t)heads};
+  const cuuint64_t strides[2] = {(cuuint64_t)row_stride * 2, (cuuint64_t)head_stride * 2};
+  const cuuint32_t box[3] = {64, (cuuint32_t)box_rows, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  STS_REQUIRE(r == CUDA_SUCCESS, STS_ERR_CONTRACT, "tensor map encode failed (%d)", (int)r);
+  return STS_OK;
+}
+
+}  // namespace
+}  // namespace sts
+
+using namespace sts;
+
+extern "C" int sts_prefill_blocksparse(const void* q_dev, const void* k_dev, const void* v_dev, int32_t heads_q,
+                                       int32_t heads_kv, int32_t n, int32_t d, int64_t q_head_stride,
+                                       int64_t kv_head_stride, int64_t row_stride, float scale,
+                                       const int32_t* idx_dev, int64_t idx_ld, const int32_t* cnt_dev, void* out_dev,
+                                       int32_t* status_dev, void* stream) {
+  STS_REQUIRE(d == 128 || d == 64, STS_ERR_CONTRACT, "block-sparse prefill supports head_dim 64 or 128");
+  STS_REQUIRE(heads_q >= 1 && heads_kv >= 1 && heads_q % heads_kv == 0 && n >= 0, STS_ERR_CONTRACT,
+              "bad prefill shape");
+  if (n == 0) return STS_OK;
+  STS_REQUIRE(q_dev && k_dev && v_dev && out_dev, STS_ERR_CONTRACT, "null buffer");
+  STS_REQUIRE(!idx_dev || cnt_dev, STS_ERR_CONTRACT, "block lists need counts");
+  STS_REQUIRE(row_stride % 8 == 0 && q_head_stride % 8 == 0 && kv_head_stride % 8 == 0, STS_ERR_CONTRACT,
+              "strides must be multiples of 8 elements");
+  PfParams p;
+  memset(&p, 0, sizeof(p));
+  p.n = n;
+  p.heads_q = heads_q;
+  p.group = heads_q / heads_kv;
+  p.tiles = (n + PF_ROWS - 1) / PF_ROWS;
+  p.scale = scale;
+  p.idx = idx_dev;
+  p.idx_ld = idx_ld;
+  p.cnt = cnt_dev;
+  p.out = static_cast<__nv_bfloat16*>(out_dev);
+  p.status = status_dev;
+  CUtensorMap qm, km, vm;
+  int rc = pf_map(&qm, q_dev, heads_q, n, d, q_head_stride, row_stride, PF_ROWS);
+  if (rc == STS_OK) rc = pf_map(&km, k_dev, heads_kv, n, d, kv_head_stride, row_stride, PF_BLK);
+  if (rc == STS_OK) rc = pf_map(&vm, v_dev, heads_kv, n, d, kv_head_stride, row_stride, PF_BLK);
+  if (rc != STS_OK) return rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  dim3 grid((unsigned)p.tiles, (unsigned)heads_q);
+  if (d == 128) {
+    STS_CUDA_CHECK(cudaFuncSetAttribute(prefill_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        PfLayout<128>::SMEM));
+    prefill_tc_kernel<128><<<grid, PF_THREADS, PfLayout<128>::SMEM, st>>>(qm, km, vm, p);
+  } else {
+    STS_CUDA_CHECK(cudaFuncSetAttribute(prefill_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        PfLayout<64>::SMEM));
+    prefill_tc_kernel<64><<<grid, PF_THREADS, PfLayout<64>::SMEM, st>>>(qm, km, vm, p);
+  }
+  STS_LAUNCH_CHECK();
+  return STS_OK;
+}

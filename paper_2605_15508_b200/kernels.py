@@ -313,3 +313,48 @@ def row_union(idx, cnt, src, *, M: int, n_max: int, out_ld=None, bitmap=None, st
     call("sts_row_union", ptr(idx), idx.stride(0), ptr(cnt), ptr(src), U, M, n_max, ptr(bitmap),
          ptr(idx_out), ptr(member), out_ld, ptr(cnt_out), ptr(status), stream_handle(stream))
     return idx_out, member, cnt_out
+
+
+PREFILL_TILE = 128   # query rows per tile of the block-sparse prefill
+PREFILL_BLOCK = 64   # keys per selectable block
+
+
+def prefill_tile_select(tile_scores: torch.Tensor, *, budget, n: int, out=None, cnt=None, status=None,
+                        workspace: Workspace | None = None, stream=None):
+    """Block selection of the block-sparse prefill: for every (kv-head, query
+    tile T) score row (fp32 [Hkv * tiles, ld], keys = positions), the top
+    ``ceil(b / 64)`` 64-key blocks among the committed positions [0, 128 T)
+    (budget b of that context, src/sparsity.py:62-66, numkit tie rule), as
+    whole blocks of ascending tokens.  Tile 0 has no committed blocks."""
+    tiles = -(-n // PREFILL_TILE)
+    rows = tile_scores.shape[0]
+    if rows % tiles:
+        raise ValueError("tile_scores must hold heads_kv * tiles rows")
+    T = torch.arange(tiles, dtype=torch.int32, device=tile_scores.device).repeat(rows // tiles)
+    row_len = torch.clamp(T * PREFILL_TILE, min=1)
+    idx, cnt = select_topk(tile_scores, budget=budget, page_size=PREFILL_BLOCK, include_current=False,
+                           row_len=row_len, out=out, cnt=cnt, status=status, workspace=workspace, stream=stream)
+    cnt.masked_fill_(T == 0, 0)
+    return idx, cnt
+
+
+def prefill_blocksparse(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, idx=None, cnt=None, scale=None,
+                        out=None, status=None, stream=None):
+    """Block-sparse causal prefill on tcgen05 (include/sts_b200.h
+    sts_prefill_blocksparse): q [Hq, n, d], k/v [Hkv, n, d] bf16 (unit inner
+    stride, rows 16-byte aligned); idx/cnt from ``prefill_tile_select`` (None:
+    dense causal).  Returns out [Hq, n, d] bf16."""
+    _require_cuda(q, k, v, idx, cnt)
+    if q.dtype != torch.bfloat16 or k.dtype != torch.bfloat16 or v.dtype != torch.bfloat16:
+        raise ValueError("block-sparse prefill runs on bf16 q / k / v")
+    Hq, n, d = q.shape
+    Hkv = k.shape[0]
+    if k.shape != (Hkv, n, d) or v.stride() != k.stride() or q.stride(1) != k.stride(1):
+        raise ValueError("q [Hq, n, d] and k/v [Hkv, n, d] must share the row stride")
+    scale = 1.0 / math.sqrt(d) if scale is None else float(scale)
+    if out is None:
+        out = torch.empty((Hq, n, d), dtype=torch.bfloat16, device=q.device)
+    call("sts_prefill_blocksparse", ptr(q), ptr(k), ptr(v), Hq, Hkv, n, d, q.stride(0), k.stride(0), k.stride(1),
+         scale, ptr(idx), idx.stride(0) if idx is not None else 0, ptr(cnt), ptr(out), ptr(status),
+         stream_handle(stream))
+    return out
