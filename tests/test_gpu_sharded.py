@@ -256,3 +256,24 @@ def test_dist_select_long_rows_span_chunks(cuda_ok, ps, P):
         red = O.reduce_rows_fp32([x[j] for j in src[r].cpu().numpy()])
         sel = O.select_committed(red, n, b, cfg)
         assert np.array_equal(got[r], np.concatenate([sel, np.arange(n, n + tail)]))
+
+
+def test_two_process_sharded_step_parity(cuda_ok, tmp_path):
+    """ShardedVerifyStep in two processes (torch.distributed, gloo, both ranks
+    on cuda:0): bench.py's N=2 path end to end — local capture, the
+    histogram all-reduce rounds, tie-count all-gather, attention and the LSE
+    merge — with its sampled-unit oracle check (masks bit-exact, outputs
+    within 2e-2)."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parent.parent
+    cmd = [sys.executable, str(root / "bench.py"), "--gpus", "2", "--one-gpu", "--dist-backend", "gloo",
+           "--context", "65536", "--steps", "1", "--warmup", "3", "--no-single-ref", "--parity-units", "8"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=str(root))
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-3000:]
+    line = json.loads([x for x in r.stdout.splitlines() if x.startswith("{")][-1])
+    assert line["n_gpus"] == 2
+    assert line["parity"]["masks_bit_exact"] and line["parity"]["attention_ok"], line["parity"]
