@@ -72,6 +72,8 @@ def parse():
     ap.add_argument("--no-extras", action="store_true", help="skip the c2 mode-R and fp32 side measurements")
     ap.add_argument("--parity-units", type=int, default=32, help="units checked against the oracle after timing")
     ap.add_argument("--eager", action="store_true", help="time stages as eager launches instead of CUDA graphs")
+    ap.add_argument("--graph-collectives", action="store_true",
+                    help="N > 1: capture each sharded stage, NCCL collectives included, in a CUDA graph")
     ap.add_argument("--flush", default="clean", choices=["clean", "write", "none"], help="L2 flush between stages")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="collective backend for N > 1 (gloo + --one-gpu: functional check on a single GPU)")
@@ -749,11 +751,13 @@ def measure_sharded(args, world, rank, local, group_world=None):
     assert step.status.item() == 0, f"device status {step.status.item()}"
     stages = {"capture": lambda: drive(step.capture(dqv, dkv)), "select": lambda: drive(step.build_masks()),
               "attend": lambda: drive(step.attend(q, k, v)), "dense": lambda: drive(step.attend_dense(q, k, v))}
-    # CUDA graph per stage, collectives included (NCCL kernels are capturable);
-    # any capture failure (e.g. gloo: host-side collectives) -> eager replays
+    # one GPU: a CUDA graph per stage.  Several ranks: eager launches unless
+    # --graph-collectives (NCCL collectives inside graph capture are not
+    # exercised in this environment's single-GPU runs; a capture failing on
+    # one rank only would hang the others, so it is opt-in)
     launch_mode = "eager"
     run_stage = dict(stages)
-    if not args.eager:
+    if not args.eager and (world == 1 or args.graph_collectives):
         try:
             graphs = {name: graph_of(fn) for name, fn in stages.items()}
             for fn in graphs.values():
