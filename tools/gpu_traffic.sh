@@ -3,7 +3,7 @@
 # `ncu --set full` capture per bench workload, restricted to the sts.attend
 # NVTX range of an eager bench run. Reports land in gpurun_out/traffic/;
 # `python tools/ncu_traffic.py KEY=REPORT ...` folds them into profiles/ncu_traffic.json.
-OUT=gpurun_out/traffic
+OUT=${OUT:-gpurun_out/traffic}
 mkdir -p $OUT
 B="python bench.py --eager --steps 1 --warmup 3 --no-cpu-baseline --no-extras --parity-units 0"
 NCU="ncu --set full --clock-control none --import-source on --nvtx --nvtx-include sts.attend/ -c ${NCU_COUNT:-2}"
