@@ -29,7 +29,7 @@ namespace {
 constexpr int PF_ROWS = 128;   // query tile = MMA M = TMEM lanes
 constexpr int PF_BLK = 64;     // keys per block = MMA N of S, K of PV
 constexpr int PF_STAGES = 4;
-constexpr int PF_THREADS = 192;
+constexpr int PF_THREADS = 320;  // TMA, MMA, two softmax warp groups (even / odd key blocks)
 constexpr float PF_RESCALE = 8.f;  // log2 growth of the row max that forces an O rescale
 
 __device__ __forceinline__ void pf_mbar_init(uint64_t* bar, uint32_t count) {
@@ -143,13 +143,14 @@ struct PfLayout {
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + PF_STAGES * KB_BYTES;
   static constexpr int OFF_P = OFF_V + PF_STAGES * KB_BYTES;
-  static constexpr int OFF_BAR = OFF_P + 2 * P_BYTES;
+  static constexpr int OFF_X = OFF_P + 2 * P_BYTES;          // [128 rows] (m, l) of the odd group
+  static constexpr int OFF_BAR = OFF_X + PF_ROWS * 8;
   // full[S], empty[S], sfull[2], sempty[2], pfull[2], odone[2], qfull
   static constexpr int NBAR = 2 * PF_STAGES + 9;
   static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
   static constexpr int S_COLS = PF_BLK;                       // per S slot
-  static constexpr int O_COL = 2 * PF_BLK;                    // O after the two S slots
-  static constexpr int TMEM_COLS = 2 * PF_BLK + D <= 256 ? 256 : 512;
+  static constexpr int O_COL = 2 * PF_BLK;                    // O_even, O_odd after the two S slots
+  static constexpr int TMEM_COLS = 2 * PF_BLK + 2 * D <= 256 ? 256 : 512;
 };
 
 // the tile's block list: committed blocks from the selection, then the diagonal
@@ -281,21 +282,24 @@ __global__ void __launch_bounds__(PF_THREADS, 1) prefill_tc_kernel(const __grid_
         const uint64_t bd = pf_desc_mn(smem + L::OFF_V + stage * L::KB_BYTES, PF_BLK * 128, 1024);
 #pragma unroll
         for (int k = 0; k < PF_BLK / 16; ++k)
-          pf_mma(tmem + L::O_COL, ad + 2 * k, bd + (uint64_t)((16 * 128) >> 4) * k, id_o, (j | k) != 0);
+          pf_mma(tmem + L::O_COL + (j & 1) * D, ad + 2 * k, bd + (uint64_t)((16 * 128) >> 4) * k, id_o,
+                 (j >= 2 || k != 0) ? 1u : 0u);
         pf_commit(&empty[stage]);   // K and V of this block no longer read
-        pf_commit(&odone[j & 1]);   // O holds blocks 0..j (also frees P buffer j & 1)
+        pf_commit(&odone[j & 1]);   // O_{j&1} holds its group's blocks up to j (frees P buffer j & 1)
       }
     }
   } else {
-    // ===== softmax: thread = query row =====
+    // ===== softmax: thread = query row; group g takes the blocks j = g mod 2 =====
     const int quad = warp & 3;
+    const int grp = (warp - 2) >> 2;
     const int r = quad * 32 + lane;       // row within the tile (TMEM lane)
     const int row = T * PF_ROWS + r;      // query position
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
+    const uint32_t o_col = L::O_COL + grp * D;
     const float sl2 = p.scale * LOG2E;
     float m = -INFINITY, l = 0.f;
-    for (int j = 0; j < nb; ++j) {
-      const uint32_t slot = j & 1;
+    for (int j = grp; j < nb; j += 2) {
+      const uint32_t slot = grp;  // S_j sits in slot j & 1
       const int b = pf_block(p, kvh, T, ncommit, j);
       pf_wait(&sfull[slot], (j >> 1) & 1);
       pf_fence_after();
@@ -314,42 +318,42 @@ __global__ void __launch_bounds__(PF_THREADS, 1) prefill_tc_kernel(const __grid_
         s[c] = ok ? s[c] * sl2 : -INFINITY;
         mx = fmaxf(mx, s[c]);
       }
-      // P buffer j&1 was read by PV_{j-2}
-      if (j >= 2) pf_wait(&odone[j & 1], ((j - 2) >> 1) & 1);
+      // this group's previous PV (j - 2) read P buffer j&1 and wrote O_grp
+      if (j >= 2) pf_wait(&odone[slot], ((j - 2) >> 1) & 1);
       // lazy rescale, warp-uniform (tcgen05.ld/st are warp-collective): rows
-      // whose max grew by > 2^8 rescale their O row after PV_{j-1} landed
+      // whose max grew by > 2^8 rescale their O row
       const bool need = mx > m + PF_RESCALE;
       if (__any_sync(0xffffffffu, need)) {
-        if (j == 0) {
-          m = mx;  // first block: every row sees key 128T, O is overwritten by PV_0
+        if (j < 2) {
+          m = mx;  // the group's first block: its PV overwrites O_grp
           l = 0.f;
         } else {
-          pf_wait(&odone[(j - 1) & 1], ((j - 1) >> 1) & 1);
           pf_fence_after();
           const float f = need ? fast_exp2(m - mx) : 1.f;
 #pragma unroll
           for (int c0 = 0; c0 < D; c0 += 32) {
             float o[32];
-            pf_ld32(tmem + lane_off + L::O_COL + c0, o);
+            pf_ld32(tmem + lane_off + o_col + c0, o);
             pf_wait_ld();
 #pragma unroll
             for (int c = 0; c < 32; ++c) o[c] *= f;
-            pf_st32(tmem + lane_off + L::O_COL + c0, o);
+            pf_st32(tmem + lane_off + o_col + c0, o);
           }
           pf_wait_st();
           l *= f;
           if (need) m = mx;
         }
       }
+      const float mb = m == -INFINITY ? 0.f : m;  // a row with no key yet: P = 0, not NaN
       // P = 2^(s - m) in bf16, K-major 128B-swizzled rows of the A operand
-      uint8_t* prow = smem + L::OFF_P + (j & 1) * L::P_BYTES + r * 128;
+      uint8_t* prow = smem + L::OFF_P + slot * L::P_BYTES + r * 128;
       float rs = 0.f;
 #pragma unroll
       for (int c8 = 0; c8 < PF_BLK / 8; ++c8) {
         uint32_t w[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float a0 = fast_exp2(s[c8 * 8 + 2 * e] - m), a1 = fast_exp2(s[c8 * 8 + 2 * e + 1] - m);
+          const float a0 = fast_exp2(s[c8 * 8 + 2 * e] - mb), a1 = fast_exp2(s[c8 * 8 + 2 * e + 1] - mb);
           const __nv_bfloat162 h = __floats2bfloat162_rn(a0, a1);
           rs += __low2float(h) + __high2float(h);  // the row sum of what the MMA multiplies
           w[e] = *reinterpret_cast<const uint32_t*>(&h);
@@ -359,31 +363,52 @@ __global__ void __launch_bounds__(PF_THREADS, 1) prefill_tc_kernel(const __grid_
       l += rs;
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // P visible to the tensor core
       pf_fence_before();
-      pf_arrive(&pfull[j & 1]);
+      pf_arrive(&pfull[slot]);
     }
-    // epilogue: O / l after the last PV
-    if (nb > 0) pf_wait(&odone[(nb - 1) & 1], ((nb - 1) >> 1) & 1);
-    pf_fence_after();
-    const float inv = l > 0.f ? 1.f / l : 0.f;
-    __nv_bfloat16* orow = p.out + ((int64_t)hq * p.n + row) * D;
+    // epilogue: the odd group hands its (m, l) to the even group, which merges
+    // O_even and O_odd (both in its TMEM lanes) and writes O / l
+    float2* xch = reinterpret_cast<float2*>(smem + L::OFF_X);
+    if (grp == 1) xch[r] = make_float2(m, l);
+    asm volatile("bar.sync 1, 256;\n" ::: "memory");
+    if (grp == 0) {
+      const int last0 = ((nb - 1) & 1) == 0 ? nb - 1 : nb - 2;  // last even / odd block
+      const int last1 = ((nb - 1) & 1) == 1 ? nb - 1 : nb - 2;
+      if (last0 >= 0) pf_wait(&odone[0], (last0 >> 1) & 1);
+      if (last1 >= 1) pf_wait(&odone[1], (last1 >> 1) & 1);
+      pf_fence_after();
+      const float2 x1 = xch[r];
+      const bool has1 = last1 >= 1;
+      const float m1 = has1 ? x1.x : -INFINITY, l1 = has1 ? x1.y : 0.f;
+      const float mm = fmaxf(m, m1);
+      const float a0 = (m == -INFINITY) ? 0.f : fast_exp2(m - mm);
+      const float a1 = (m1 == -INFINITY) ? 0.f : fast_exp2(m1 - mm);
+      const float L = l * a0 + l1 * a1;
+      const float inv = L > 0.f ? 1.f / L : 0.f;
+      const float w0 = a0 * inv, w1 = a1 * inv;
+      __nv_bfloat16* orow = p.out + ((int64_t)hq * p.n + row) * D;
 #pragma unroll
-    for (int c0 = 0; c0 < D; c0 += 32) {
-      float o[32];
-      pf_ld32(tmem + lane_off + L::O_COL + c0, o);  // warp-collective: every row loads
-      pf_wait_ld();
-      if (row < p.n) {
+      for (int c0 = 0; c0 < D; c0 += 32) {
+        float o[32], o1[32];
+        pf_ld32(tmem + lane_off + L::O_COL + c0, o);  // warp-collective: every row loads
+        pf_ld32(tmem + lane_off + L::O_COL + D + c0, o1);
+        pf_wait_ld();
+        if (row < p.n) {
 #pragma unroll
-        for (int c = 0; c < 32; c += 8) {
-          uint4 w;
-          w.x = pack_bf16(o[c] * inv, o[c + 1] * inv);
-          w.y = pack_bf16(o[c + 2] * inv, o[c + 3] * inv);
-          w.z = pack_bf16(o[c + 4] * inv, o[c + 5] * inv);
-          w.w = pack_bf16(o[c + 6] * inv, o[c + 7] * inv);
-          *reinterpret_cast<uint4*>(orow + c0 + c) = w;
+          for (int c = 0; c < 32; c += 8) {
+            uint4 w;
+            w.x = pack_bf16(o[c] * w0 + (has1 ? o1[c] * w1 : 0.f), o[c + 1] * w0 + (has1 ? o1[c + 1] * w1 : 0.f));
+            w.y = pack_bf16(o[c + 2] * w0 + (has1 ? o1[c + 2] * w1 : 0.f),
+                            o[c + 3] * w0 + (has1 ? o1[c + 3] * w1 : 0.f));
+            w.z = pack_bf16(o[c + 4] * w0 + (has1 ? o1[c + 4] * w1 : 0.f),
+                            o[c + 5] * w0 + (has1 ? o1[c + 5] * w1 : 0.f));
+            w.w = pack_bf16(o[c + 6] * w0 + (has1 ? o1[c + 6] * w1 : 0.f),
+                            o[c + 7] * w0 + (has1 ? o1[c + 7] * w1 : 0.f));
+            *reinterpret_cast<uint4*>(orow + c0 + c) = w;
+          }
         }
       }
+      if (row < p.n && !(L > 0.f)) set_status(p.status, STS_DEV_EMPTY_ROW);
     }
-    if (row < p.n && !(l > 0.f)) set_status(p.status, STS_DEV_EMPTY_ROW);
   }
   pf_fence_before();
   __syncthreads();
