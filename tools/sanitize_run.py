@@ -15,7 +15,8 @@ from paper_2605_15508_b200.model import block_attention  # noqa: E402
 from paper_2605_15508_b200.sharded import DistSelector, run_single  # noqa: E402
 from paper_2605_15508_b200.verify_step import STSVerifyStep, VerifyShape, random_mapping_table, synthetic_inputs  # noqa: E402
 
-which = set(sys.argv[1:]) or {"capture", "select", "decode", "dist", "merge", "prefill", "block", "union"}
+which = set(sys.argv[1:]) or {"capture", "select", "decode", "dist", "merge", "prefill", "block", "union",
+                              "prefill_tc", "offload"}
 dev = torch.device("cuda", 0)
 g = torch.Generator(device=dev).manual_seed(0)
 s = VerifyShape(batch=1, context=1000, gamma=4, target_layers=2, target_q_heads=8, target_kv_heads=2, head_dim=128,
@@ -74,5 +75,26 @@ if "union" in which:
     idx = torch.sort(torch.randint(0, 500, (8, 60), generator=g, device=dev, dtype=torch.int32), dim=1).values
     cnt = torch.full((8,), 60, dtype=torch.int32, device=dev)
     kernels.row_union(idx, cnt, torch.arange(8, dtype=torch.int32, device=dev).reshape(2, 4), M=4, n_max=500)
+if "prefill_tc" in which:
+    n, hq, hkv, d = 300, 2, 1, 128
+    q = torch.randn((hq, n, d), generator=g, device=dev).bfloat16()
+    kk = torch.randn((hkv, n, d), generator=g, device=dev).bfloat16()
+    vv = torch.randn((hkv, n, d), generator=g, device=dev).bfloat16()
+    tiles = -(-n // 128)
+    sc = torch.rand((hkv * tiles, -(-n // 4) * 4), generator=g, device=dev)
+    idx, cnt = kernels.prefill_tile_select(sc, budget=0.3, n=n)
+    kernels.prefill_blocksparse(q, kk, vv, idx=idx, cnt=cnt)
+    kernels.prefill_blocksparse(q, kk, vv)
+if "offload" in which:
+    from paper_2605_15508_b200.offload import PagedKVOffload
+
+    step = STSVerifyStep(s, SparsityConfig(budget=0.1, page_size=16), random_mapping_table(s, 1), mode="S",
+                         device=dev)
+    q, k, v = step.target_views(tq, tk, tv)
+    step.capture(*step.draft_views(dq, dk))
+    step.build_masks()
+    off = PagedKVOffload(step, k.cpu().pin_memory(), v.cpu().pin_memory(), page_size=16, copy_ctas=4)
+    off.attend_on_demand(q)
+    off.attend_prefetch(q)
 torch.cuda.synchronize()
 print("sanitize_run ok:", ",".join(sorted(which)))
