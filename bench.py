@@ -527,6 +527,8 @@ def run_single_gpu(args):
         torch.cuda.synchronize()
         units = parity.sample_units(shape.batch, shape.target_layers, shape.target_kv_heads, args.parity_units)
         par = parity.check_units(step, q, k, v, step.out, units)
+        # the device masks vs masks from fp64 reference draft rows
+        par["mask_agreement"] = parity.mask_agreement(step, dq, dk, units[:8])
 
     # end to end through the public API with host buffers (pinned), copies inside
     # the timed region: (a) the metric itself — target attention with Q from the

@@ -96,3 +96,53 @@ def check_units(step, q, k, v, out, units, cfg=None, pos_offset: int = 0, tol: f
         max_err = max(max_err, err)
     return {"units": len(units), "masks_bit_exact": not bad, "mask_mismatch_units": bad[:8],
             "max_abs_err": round(max_err, 6), "tol": tol, "attention_ok": max_err <= tol}
+
+
+def mask_agreement(step, draft_q, draft_k, units, cfg=None) -> dict:
+    """Agreement of the device masks with masks built from fp64 reference
+    draft rows (overlap as in evalkit.mask_recall,
+    src/evalkit.py:40-96).  For each sampled unit the reference path is
+    restated from the device's bf16 inputs: every mapped draft head's γ+1
+    rows are fp64 softmaxes (draft_attention_rows, src/toymodel.py:315-352),
+    summed over the rows on the committed positions, reduced over the head
+    group, selected with the reference rule.  Returns the mean recall
+    |S_dev ∩ S_ref| / |S_ref| and Jaccard over the committed selections
+    (the in-block tail is common to both) and the count of identical masks.
+
+    draft_q [B, Ld, Hqd, R, dd], draft_k [B, Ld, Hkvd, N, dd] (device)."""
+    import torch
+
+    s = step.shape
+    cfg = cfg if cfg is not None else step.cfg
+    R, base = s.rows, s.context
+    nd = s.draft_layers * s.draft_q_heads
+    Gd = s.draft_group
+    src = step.row_src.cpu().numpy()
+    idx = step.idx.index_select(0, torch.tensor(units, device=step.idx.device)).cpu().numpy()
+    cnt = step.cnt.index_select(0, torch.tensor(units, device=step.cnt.device)).cpu().numpy()
+    rec, jac, same = [], [], 0
+    cache = {}
+    for j, u in enumerate(units):
+        rows = []
+        for hj in src[u]:
+            hj = int(hj)
+            if hj not in cache:
+                b, rest = divmod(hj, nd)
+                dl, dh = divmod(rest, s.draft_q_heads)
+                q = draft_q[b, dl, dh].float().cpu().numpy()                       # [R, dd]
+                keys = draft_k[b, dl, dh // Gd, : base + R].float().cpu().numpy()   # [n_kv, dd]
+                p = O.draft_attention_rows(q, keys, base, R)
+                cache[hj] = O.reduce_rows_fp32([x[:base] for x in p])              # committed positions
+            rows.append(cache[hj])
+        red = O.reduce_rows_fp32(rows)
+        ref = O.select_committed(red, base, int(step.budget), oracle_config(cfg))
+        dev = idx[j, : cnt[j]].astype(np.int64)
+        dev = dev[dev < base]
+        inter = np.intersect1d(dev, ref).size
+        rec.append(inter / max(1, ref.size))
+        jac.append(inter / max(1, np.union1d(dev, ref).size))
+        same += int(np.array_equal(dev, ref))
+    return {"units": len(units), "recall": round(float(np.mean(rec)), 5), "jaccard": round(float(np.mean(jac)), 5),
+            "identical_masks": same, "min_recall": round(float(np.min(rec)), 5),
+            "what": "device masks (bf16 capture -> fp32 rows -> select) vs masks from fp64 reference draft rows "
+                    "on the same bf16 inputs, committed positions"}

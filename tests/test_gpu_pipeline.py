@@ -203,3 +203,21 @@ def test_host_buffer_api_matches_device_path(cuda_ok):
         got.append(h_out.clone())
     assert torch.equal(got[0], got[1])
     torch.testing.assert_close(got[0].float(), want.cpu().float(), rtol=2e-2, atol=2e-2)
+
+
+def test_mask_agreement_with_fp64_reference_rows(cuda_ok):
+    """masks from the device capture (bf16 inputs, fp32 rows)
+    against masks from fp64 reference draft rows on the same inputs."""
+    import torch
+
+    from oracle import parity
+    from paper_2605_15508_b200 import SparsityConfig
+    from paper_2605_15508_b200.verify_step import STSVerifyStep, random_mapping_table, synthetic_inputs
+
+    s = _small_shape()
+    step = STSVerifyStep(s, SparsityConfig(budget=0.1), random_mapping_table(s, seed=4), mode="S")
+    dq, dk, tq, tk, tv = synthetic_inputs(s, "cuda", seed=9)
+    step.step(*step.draft_views(dq, dk), *step.target_views(tq, tk, tv))
+    torch.cuda.synchronize()
+    agree = parity.mask_agreement(step, dq, dk, list(range(s.target_units)))
+    assert agree["recall"] >= 0.99 and agree["min_recall"] >= 0.97, agree

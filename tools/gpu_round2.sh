@@ -20,5 +20,11 @@ timeout 600 python tools/bench_generate.py > $O/generate.log 2>&1
 P="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-extras --eager --parity-units 0"
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $P > $O/ncu_launches.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:verify_decode|merge_pieces|select_kernel|capture_kernel" -s 10 -c 6 -o $O/prof_step -f $P > $O/ncu_step.log 2>&1
+python tools/ncu_summary.py $O/prof_step.ncu-rep --json $O/ncu_step_summary.json > /dev/null 2>&1
+python tools/ncu_hot.py $O/prof_step.ncu-rep --top 40 > $O/ncu_step_hot.txt 2>&1
+rm -f $O/prof_step.ncu-rep
 OUT=$O/traffic CFGS="c2 c2R c3 c4" bash tools/gpu_traffic.sh
+python tools/ncu_traffic.py --out=$O/ncu_traffic.json "c2:S:s0.9:ps1:separate:P1=$O/traffic/c2.ncu-rep" "c2:R:s0.9:ps1:separate:P1=$O/traffic/c2R.ncu-rep" "c3:S:s0.9:ps1:separate:P1=$O/traffic/c3.ncu-rep" "c4:S:s0.9:ps1:separate:P1=$O/traffic/c4.ncu-rep" > $O/traffic.log 2>&1
+rm -f $O/traffic/*.ncu-rep
+du -sh $O
 for f in $O/pytest_gpu.log $O/smoke.log $O/bench.log $O/bench_ref.log $O/bench_c4.log; do tail -n 2 $f | cut -c1-300; done

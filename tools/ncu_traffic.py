@@ -22,6 +22,9 @@ from ncu_summary import summarize  # noqa: E402
 
 def main(argv):
     out = ROOT / "profiles" / "ncu_traffic.json"
+    if argv and argv[0].startswith("--out="):
+        out = Path(argv[0].split("=", 1)[1])
+        argv = argv[1:]
     db = json.loads(out.read_text()) if out.exists() else {}
     for arg in argv:
         key, rep = arg.split("=", 1)
