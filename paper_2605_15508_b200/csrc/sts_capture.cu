@@ -28,8 +28,9 @@ namespace {
 
 // epilogue warps: groups of four (one warp per TMEM lane quadrant) taking
 // alternate tiles; two groups for N = 32 (registers allow), one for N = 48
-constexpr int cap_epi_warps(int ncol) { return ncol <= 32 ? 8 : 4; }
-constexpr int cap_threads(int ncol) { return 64 + 32 * cap_epi_warps(ncol); }
+// (the LSE pass at N = 48 keeps 3 x 48 row registers per thread: one group)
+constexpr int cap_epi_warps(int ncol, int mode) { return (ncol <= 32 || mode != 0) ? 8 : 4; }
+constexpr int cap_threads(int ncol, int mode) { return 64 + 32 * cap_epi_warps(ncol, mode); }
 constexpr int CAP_KEYS = 128;  // keys per tile = MMA M = TMEM lanes
 constexpr int CAP_MODE_LSE = 0, CAP_MODE_PROBS = 1;
 constexpr float CAP_LN2 = 0.6931471805599453f;
@@ -162,7 +163,7 @@ __device__ __forceinline__ int64_t owner_of(int64_t t, int64_t tiles, int64_t gr
   return c;
 }
 
-template <int D, int NCOL>
+template <int D, int NCOL, int MODE>
 struct CapLayout {
   static constexpr int SLABS = D / 64;                    // 128-byte K-major slabs
   static constexpr int KTILE = CAP_KEYS * 128 * SLABS;    // bytes per K tile
@@ -177,9 +178,9 @@ struct CapLayout {
   static constexpr int QTILE = NCOL * 128 * SLABS;        // bytes per Q tile (N rows)
   static constexpr int OFF_K = 0;
   static constexpr int OFF_Q = OFF_K + STAGES * STEP;
-  static constexpr int EPI = cap_epi_warps(NCOL);
+  static constexpr int EPI = cap_epi_warps(NCOL, MODE);
   static constexpr int GROUPS = EPI / 4;
-  static constexpr int THREADS = cap_threads(NCOL);
+  static constexpr int THREADS = cap_threads(NCOL, MODE);
   static constexpr int OFF_RED = OFF_Q + 2 * QTILE;       // [epilogue warps][NCOL] (m, l) float2
   static constexpr int OFF_BAR = OFF_RED + EPI * NCOL * 8;
   static constexpr int NBAR = 2 * STAGES + 2 * NSLOT + 4;
@@ -218,9 +219,9 @@ struct StepIter {
 // RT: rows per head at compile time (5 = gamma 4, the configured depth), 0 = runtime p.R;
 // MODE: CAP_MODE_LSE or CAP_MODE_PROBS (p.mode is ignored)
 template <int D, int NCOL, int RT, int MODE>
-__global__ void __launch_bounds__(cap_threads(NCOL), 1)
+__global__ void __launch_bounds__(cap_threads(NCOL, MODE), 1)
     capture_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap qmap, CapParams p) {
-  using L = CapLayout<D, NCOL>;
+  using L = CapLayout<D, NCOL, MODE>;
   constexpr int TPS = L::TPS;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -626,7 +627,7 @@ int make_map(CUtensorMap* map, const void* base, int64_t units, int64_t rows, in
 
 template <int D, int NCOL, int RT, int MODE>
 int launch_m(const CUtensorMap& km, const CUtensorMap& qm, const CapParams& p, cudaStream_t st) {
-  using L = CapLayout<D, NCOL>;
+  using L = CapLayout<D, NCOL, MODE>;
   static_assert(L::SMEM <= 227 * 1024, "capture shared memory");
   STS_CUDA_CHECK(
       cudaFuncSetAttribute(capture_kernel<D, NCOL, RT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM));
