@@ -90,14 +90,11 @@ struct VL {
   static constexpr int PITCH = D * 2 + 16;        // padded row
   static constexpr int KV = KT * PITCH;           // K block -> V block
   static constexpr int STAGE = (K_ONLY ? 1 : 2) * KV;
-  static constexpr int MP = NW * 16;              // padded stacked rows
-  static constexpr int KPS = KT + 4;              // staged probability row pitch (floats)
-  static constexpr int PROB = MODE == MODE_PROBS ? MP * KPS * 4 : 0;  // staged probabilities [row][key]
   static constexpr int RING = STAGES <= 2 ? 4 : 8;  // index ring (power of 2, >= 2*STAGES)
   static constexpr int IDX_BYTES = RING * KT * 4;
   static constexpr int META_BYTES = RING * 32;
   static constexpr int MERGE = NW * 16 * 2 * 4;
-  static constexpr int SMEM = STAGES * STAGE + 2 * IDX_BYTES + META_BYTES + MERGE + PROB + 16;
+  static constexpr int SMEM = STAGES * STAGE + 2 * IDX_BYTES + META_BYTES + MERGE + 16;
   // resident CTAs per SM the register allocation must allow: the shared-memory
   // limit, capped so a warp keeps ~168 registers (O, Q fragments, S, P)
   static constexpr int SMEM_CTAS = (227 * 1024) / (SMEM + 1024);
@@ -135,8 +132,7 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
   uint32_t* s_mem = reinterpret_cast<uint32_t*>(s_idx + L::RING * KT);
   int* s_meta = reinterpret_cast<int*>(s_mem + L::RING * KT);
   float* s_merge = reinterpret_cast<float*>(s_meta + L::RING * 8);
-  float* s_prob = s_merge + L::MERGE / 4;
-  int* s_flag = reinterpret_cast<int*>(s_prob + L::PROB / 4);
+  int* s_flag = reinterpret_cast<int*>(s_merge + L::MERGE / 4);
   const uint32_t stage_base = smem_u32(s_stage);
   const uint32_t idx_base = smem_u32(s_idx);
   const uint32_t mem_base = smem_u32(s_mem);
@@ -144,7 +140,6 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
   // ---- units with no keys (striped over CTAs): zero rows, LSE -inf ----
   for (int64_t u = blockIdx.x; u < U; u += gridDim.x) {
     if (unit_tiles(p, u, KT) != 0) continue;
-    if constexpr (MODE == MODE_PROBS) continue;
     if constexpr (MODE == MODE_DECODE) {
       if (p.out_f32) {
         float* og = static_cast<float*>(p.out) + u * (int64_t)M * D;
@@ -324,12 +319,10 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
   const int rmodA = rA % p.rows_per_head, rmodB = rB % p.rows_per_head;
   const bool rB_live = warp * 16 + 8 < M;  // warp-uniform: this warp's rB rows hold queries
   const float sl2 = p.scale * LOG2E;
-  [[maybe_unused]] const int probs_G = M / p.rows_per_head;  // q-heads per unit (MODE_PROBS)
   const int causal_shift = p.pos_offset - p.causal_base;
   const bool causal = p.causal_base >= 0;
   float o[MODE == MODE_DECODE ? D / 8 : 1][4];
   float m_a = -INFINITY, m_b = -INFINITY, l_a = 0.f, l_b = 0.f;
-  float lse2A = 0.f, lse2B = 0.f;  // MODE_PROBS: the rows' LSE in log2 units
   uint32_t qa[D / 16][4];
   // ldmatrix lane offsets: K (B of QK^T, non-trans): key (lane&7), dim block (lane>>3)*8
   const uint32_t offK = (uint32_t)((lane & 7) * PITCH + (lane >> 3) * 16);
@@ -358,15 +351,10 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
       qa[kk][2] = okA ? __ldg(qA + kk * 8 + 4) : 0u;
       qa[kk][3] = okB ? __ldg(qB + kk * 8 + 4) : 0u;
     }
-    if constexpr (MODE == MODE_PROBS) {
-      lse2A = okA && p.lse_in ? p.lse_in[u * M + rA] * LOG2E : 0.f;  // (raw-logit mode: no LSE)
-      lse2B = okB && p.lse_in ? p.lse_in[u * M + rB] * LOG2E : 0.f;
-    }
   };
 
   // ---- finish unit u for this CTA: final rows, or partial + last-CTA merge ----
   auto flush = [&](int64_t u, int P_u, int cnt_u, int64_t range) {
-    if constexpr (MODE == MODE_PROBS) return;  // probabilities are written per tile
     float la = l_a, lb = l_b;
     la += __shfl_xor_sync(0xffffffffu, la, 1);
     la += __shfl_xor_sync(0xffffffffu, la, 2);
@@ -513,140 +501,83 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
 #pragma unroll
       for (int c = 0; c < 4; ++c) s[nt][c] *= sl2;
 
-    if constexpr (MODE == MODE_PROBS) {
-      // p = 2^(s - lse) staged as s_prob[row][key], then written per row
-      // (mode R) or summed over each head's speculative rows in row order
-      // (mode S, committed positions only); one thread per key, no divides
-      constexpr int KPS = L::KPS;
-      if (p.probs_mode == 2) {  // raw logits q.k * scale (ForwardRecord.scores), natural units
+    if (!simple) {
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const int key = nt * 8 + 2 * (lane & 3);
-          *reinterpret_cast<float2*>(s_prob + rA * KPS + key) = make_float2(s[nt][0] * LN2, s[nt][1] * LN2);
-          if (rB_live)
-            *reinterpret_cast<float2*>(s_prob + rB * KPS + key) = make_float2(s[nt][2] * LN2, s[nt][3] * LN2);
-        }
-      } else {
+      for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          const int key = nt * 8 + 2 * (lane & 3);
-          *reinterpret_cast<float2*>(s_prob + rA * KPS + key) =
-              make_float2(fast_exp2(s[nt][0] - lse2A), fast_exp2(s[nt][1] - lse2A));
-          if (rB_live)
-            *reinterpret_cast<float2*>(s_prob + rB * KPS + key) =
-                make_float2(fast_exp2(s[nt][2] - lse2B), fast_exp2(s[nt][3] - lse2B));
-        }
-      }
-      __syncthreads();
-      const int R = p.rows_per_head;
-      const int G = probs_G;
-      const int lim = p.causal_base - p.pos_offset;  // committed: pos < lim
-      for (int key = tid; key < KT; key += NTH) {
-        if (key >= nvalid) continue;
-        const int pos = p.idx ? ring[key] : j0 + key;
-        if (p.probs_mode == 0) {
-          if (pos >= lim) continue;
-          float* outp = p.probs_out + (u * G) * p.out_ld + j0 + key;
-          if (R == 5) {  // gamma = 4: all five loads issued before the in-order sum
-            for (int hh = 0; hh < G; ++hh) {
-              const float* sp = s_prob + hh * 5 * KPS + key;
-              const float x0 = sp[0], x1 = sp[KPS], x2 = sp[2 * KPS], x3 = sp[3 * KPS], x4 = sp[4 * KPS];
-              outp[hh * p.out_ld] = __fadd_rn(__fadd_rn(__fadd_rn(__fadd_rn(x0, x1), x2), x3), x4);
-            }
-          } else {
-            for (int hh = 0; hh < G; ++hh) {
-              const float* sp = s_prob + hh * R * KPS + key;
-              float acc = sp[0];
-              for (int ii = 1; ii < R; ++ii) acc = __fadd_rn(acc, sp[ii * KPS]);
-              outp[hh * p.out_ld] = acc;
-            }
+        for (int e = 0; e < 2; ++e) {
+          const int key = nt * 8 + 2 * (lane & 3) + e;
+          const bool valid = key < nvalid;
+          const int pos = valid ? (p.idx ? ring[key] : j0 + key) : 0;
+          const uint32_t mem = p.member ? s_mem[slot * KT + key] : 0xffffffffu;
+          bool okA = valid && ((mem >> (rA & 31)) & 1u);
+          bool okB = valid && ((mem >> (rB & 31)) & 1u);
+          if (causal) {
+            okA = okA && (pos + causal_shift <= rmodA);
+            okB = okB && (pos + causal_shift <= rmodB);
           }
-        } else {
-          float* outp = p.probs_out + (u * M) * p.out_ld + j0 + key;
-          for (int r = 0; r < M; ++r)
-            if (pos <= lim + r % R) outp[r * p.out_ld] = s_prob[r * KPS + key];
+          if (!okA) s[nt][e] = -INFINITY;
+          if (!okB) s[nt][2 + e] = -INFINITY;
         }
-      }
-      // the next iteration's loop-top barrier orders these reads before reuse
+    }
+    // online softmax (rows rA: s[.][0..1], rB: s[.][2..3])
+    float tA = -INFINITY, tB = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      tA = fmaxf(tA, fmaxf(s[nt][0], s[nt][1]));
+      tB = fmaxf(tB, fmaxf(s[nt][2], s[nt][3]));
+    }
+    tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, 1));
+    tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, 2));
+    if (rB_live) {
+      tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 1));
+      tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 2));
     } else {
-      if (!simple) {
+      tB = 0.f;  // padding rows: keep their state constant (m = 0, nothing accumulated)
+    }
+    const float nA = fmaxf(m_a, tA), nB = rB_live ? fmaxf(m_b, tB) : 0.f;
+    // rows with no admissible key yet keep everything at zero
+    const float bA = nA == -INFINITY ? 0.f : nA, bB = nB == -INFINITY ? 0.f : nB;
+    const float alA = fast_exp2(m_a - bA), alB = rB_live ? fast_exp2(m_b - bB) : 1.f;
+    m_a = nA;
+    m_b = nB;
+    float sumA = 0.f, sumB = 0.f;
+    uint32_t pa[KS][4];
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int key = nt * 8 + 2 * (lane & 3) + e;
-            const bool valid = key < nvalid;
-            const int pos = valid ? (p.idx ? ring[key] : j0 + key) : 0;
-            const uint32_t mem = p.member ? s_mem[slot * KT + key] : 0xffffffffu;
-            bool okA = valid && ((mem >> (rA & 31)) & 1u);
-            bool okB = valid && ((mem >> (rB & 31)) & 1u);
-            if (causal) {
-              okA = okA && (pos + causal_shift <= rmodA);
-              okB = okB && (pos + causal_shift <= rmodB);
-            }
-            if (!okA) s[nt][e] = -INFINITY;
-            if (!okB) s[nt][2 + e] = -INFINITY;
-          }
-      }
-      // online softmax (rows rA: s[.][0..1], rB: s[.][2..3])
-      float tA = -INFINITY, tB = -INFINITY;
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        tA = fmaxf(tA, fmaxf(s[nt][0], s[nt][1]));
-        tB = fmaxf(tB, fmaxf(s[nt][2], s[nt][3]));
-      }
-      tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, 1));
-      tA = fmaxf(tA, __shfl_xor_sync(0xffffffffu, tA, 2));
-      if (rB_live) {
-        tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 1));
-        tB = fmaxf(tB, __shfl_xor_sync(0xffffffffu, tB, 2));
-      } else {
-        tB = 0.f;  // padding rows: keep their state constant (m = 0, nothing accumulated)
-      }
-      const float nA = fmaxf(m_a, tA), nB = rB_live ? fmaxf(m_b, tB) : 0.f;
-      // rows with no admissible key yet keep everything at zero
-      const float bA = nA == -INFINITY ? 0.f : nA, bB = nB == -INFINITY ? 0.f : nB;
-      const float alA = fast_exp2(m_a - bA), alB = rB_live ? fast_exp2(m_b - bB) : 1.f;
-      m_a = nA;
-      m_b = nB;
-      float sumA = 0.f, sumB = 0.f;
-      uint32_t pa[KS][4];
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        const float p0 = fast_exp2(s[nt][0] - bA), p1 = fast_exp2(s[nt][1] - bA);
-        // rows rB of the last warp are often all padding (M = 20: rows 24..31)
-        const float p2 = rB_live ? fast_exp2(s[nt][2] - bB) : 0.f, p3 = rB_live ? fast_exp2(s[nt][3] - bB) : 0.f;
-        sumA += p0 + p1;
-        sumB += p2 + p3;
-        if constexpr (MODE == MODE_DECODE) {
-          pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(p0, p1);
-          pa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(p2, p3);
-        }
-      }
-      l_a = l_a * alA + sumA;
-      l_b = l_b * alB + sumB;
+    for (int nt = 0; nt < NT; ++nt) {
+      const float p0 = fast_exp2(s[nt][0] - bA), p1 = fast_exp2(s[nt][1] - bA);
+      // rows rB of the last warp are often all padding (M = 20: rows 24..31)
+      const float p2 = rB_live ? fast_exp2(s[nt][2] - bB) : 0.f, p3 = rB_live ? fast_exp2(s[nt][3] - bB) : 0.f;
+      sumA += p0 + p1;
+      sumB += p2 + p3;
       if constexpr (MODE == MODE_DECODE) {
-        if (__any_sync(0xffffffffu, alA != 1.f || alB != 1.f)) {
+        pa[nt >> 1][(nt & 1) * 2 + 0] = pack_bf16(p0, p1);
+        pa[nt >> 1][(nt & 1) * 2 + 1] = pack_bf16(p2, p3);
+      }
+    }
+    l_a = l_a * alA + sumA;
+    l_b = l_b * alB + sumB;
+    if constexpr (MODE == MODE_DECODE) {
+      if (__any_sync(0xffffffffu, alA != 1.f || alB != 1.f)) {
 #pragma unroll
-          for (int nt = 0; nt < D / 8; ++nt) {
-            o[nt][0] *= alA;
-            o[nt][1] *= alA;
-            o[nt][2] *= alB;
-            o[nt][3] *= alB;
-          }
+        for (int nt = 0; nt < D / 8; ++nt) {
+          o[nt][0] *= alA;
+          o[nt][1] *= alA;
+          o[nt][2] *= alB;
+          o[nt][3] *= alB;
         }
-        // O += P V
+      }
+      // O += P V
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          const uint32_t av = sk + L::KV + ks * 16 * PITCH + offV;
+      for (int ks = 0; ks < KS; ++ks) {
+        const uint32_t av = sk + L::KV + ks * 16 * PITCH + offV;
 #pragma unroll
-          for (int n2 = 0; n2 < D / 16; ++n2) {
-            uint32_t b[4];
-            ldmatrix_x4_trans(b[0], b[1], b[2], b[3], av + n2 * 32);
-            const uint32_t b0[2] = {b[0], b[1]}, b1[2] = {b[2], b[3]};
-            mma_bf16_16816(o[2 * n2], pa[ks], b0);
-            mma_bf16_16816(o[2 * n2 + 1], pa[ks], b1);
-          }
+        for (int n2 = 0; n2 < D / 16; ++n2) {
+          uint32_t b[4];
+          ldmatrix_x4_trans(b[0], b[1], b[2], b[3], av + n2 * 32);
+          const uint32_t b0[2] = {b[0], b[1]}, b1[2] = {b[2], b[3]};
+          mma_bf16_16816(o[2 * n2], pa[ks], b0);
+          mma_bf16_16816(o[2 * n2 + 1], pa[ks], b1);
         }
       }
     }
@@ -655,79 +586,77 @@ __global__ void __launch_bounds__(NW * 32, (VL<D, NW, KT, STAGES, MODE>::MINB)) 
   STS_TRACE_AT(3);
   if constexpr (CS > 1) {
     // ---- merge the cluster's shares of the unit through DSMEM ----
-    if constexpr (MODE != MODE_PROBS) {
-      constexpr int NO = MODE == MODE_DECODE ? D / 8 : 0;  // float4 of O per thread
-      float la = l_a, lb = l_b;
-      la += __shfl_xor_sync(0xffffffffu, la, 1);
-      la += __shfl_xor_sync(0xffffffffu, la, 2);
-      lb += __shfl_xor_sync(0xffffffffu, lb, 1);
-      lb += __shfl_xor_sync(0xffffffffu, lb, 2);
-      __syncthreads();  // the stage buffers are free: reuse them as the exchange area
-      float4* xb = reinterpret_cast<float4*>(smem);  // [NO + 1][NTH] float4
-      if (crank != 0) {
+    constexpr int NO = MODE == MODE_DECODE ? D / 8 : 0;  // float4 of O per thread
+    float la = l_a, lb = l_b;
+    la += __shfl_xor_sync(0xffffffffu, la, 1);
+    la += __shfl_xor_sync(0xffffffffu, la, 2);
+    lb += __shfl_xor_sync(0xffffffffu, lb, 1);
+    lb += __shfl_xor_sync(0xffffffffu, lb, 2);
+    __syncthreads();  // the stage buffers are free: reuse them as the exchange area
+    float4* xb = reinterpret_cast<float4*>(smem);  // [NO + 1][NTH] float4
+    if (crank != 0) {
+      if constexpr (MODE == MODE_DECODE) {
+#pragma unroll
+        for (int j = 0; j < NO; ++j) xb[j * NTH + tid] = make_float4(o[j][0], o[j][1], o[j][2], o[j][3]);
+      }
+      xb[NO * NTH + tid] = make_float4(m_a, m_b, la, lb);
+    }
+    cluster_sync_all();
+    if (crank == 0 && iu < U && icnt > 0) {
+      const uint32_t xa = smem_u32(xb);
+      for (unsigned q = 1; q < (unsigned)CS; ++q) {
+        const uint32_t ra = dsmem_map(xa, q);
+        const float4 st = dsmem_ld4(ra + (uint32_t)((NO * NTH + tid) * 16));
+        const float nA = fmaxf(m_a, st.x), nB = fmaxf(m_b, st.y);
+        const float bA = nA == -INFINITY ? 0.f : nA, bB = nB == -INFINITY ? 0.f : nB;
+        const float fA = fast_exp2(m_a - bA), gA = fast_exp2(st.x - bA);
+        const float fB = fast_exp2(m_b - bB), gB = fast_exp2(st.y - bB);
+        la = la * fA + st.z * gA;
+        lb = lb * fB + st.w * gB;
+        m_a = nA;
+        m_b = nB;
         if constexpr (MODE == MODE_DECODE) {
 #pragma unroll
-          for (int j = 0; j < NO; ++j) xb[j * NTH + tid] = make_float4(o[j][0], o[j][1], o[j][2], o[j][3]);
-        }
-        xb[NO * NTH + tid] = make_float4(m_a, m_b, la, lb);
-      }
-      cluster_sync_all();
-      if (crank == 0 && iu < U && icnt > 0) {
-        const uint32_t xa = smem_u32(xb);
-        for (unsigned q = 1; q < (unsigned)CS; ++q) {
-          const uint32_t ra = dsmem_map(xa, q);
-          const float4 st = dsmem_ld4(ra + (uint32_t)((NO * NTH + tid) * 16));
-          const float nA = fmaxf(m_a, st.x), nB = fmaxf(m_b, st.y);
-          const float bA = nA == -INFINITY ? 0.f : nA, bB = nB == -INFINITY ? 0.f : nB;
-          const float fA = fast_exp2(m_a - bA), gA = fast_exp2(st.x - bA);
-          const float fB = fast_exp2(m_b - bB), gB = fast_exp2(st.y - bB);
-          la = la * fA + st.z * gA;
-          lb = lb * fB + st.w * gB;
-          m_a = nA;
-          m_b = nB;
-          if constexpr (MODE == MODE_DECODE) {
-#pragma unroll
-            for (int j = 0; j < NO; ++j) {
-              const float4 x = dsmem_ld4(ra + (uint32_t)((j * NTH + tid) * 16));
-              o[j][0] = o[j][0] * fA + x.x * gA;
-              o[j][1] = o[j][1] * fA + x.y * gA;
-              o[j][2] = o[j][2] * fB + x.z * gB;
-              o[j][3] = o[j][3] * fB + x.w * gB;
-            }
-          }
-        }
-        const float inv_a = la > 0.f ? 1.f / la : 0.f, inv_b = lb > 0.f ? 1.f / lb : 0.f;
-        const int dc = 2 * (lane & 3);
-        const int64_t u = iu;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int r = h ? rB : rA;
-          if (r >= M) continue;
-          const float inv = h ? inv_b : inv_a;
-          if constexpr (MODE == MODE_DECODE) {
-            if (p.out_f32) {
-              float* og = static_cast<float*>(p.out) + (u * M + r) * (int64_t)D + dc;
-#pragma unroll
-              for (int nt = 0; nt < D / 8; ++nt)
-                *reinterpret_cast<float2*>(og + nt * 8) = make_float2(o[nt][2 * h] * inv, o[nt][2 * h + 1] * inv);
-            } else {
-              __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + (u * M + r) * (int64_t)D + dc;
-#pragma unroll
-              for (int nt = 0; nt < D / 8; ++nt)
-                *reinterpret_cast<__nv_bfloat162*>(og + nt * 8) =
-                    __floats2bfloat162_rn(o[nt][2 * h] * inv, o[nt][2 * h + 1] * inv);
-            }
-          }
-          if ((lane & 3) == 0) {
-            const float l = h ? lb : la;
-            const float m = h ? m_b : m_a;
-            if (p.lse) p.lse[u * M + r] = l > 0.f ? (m + __log2f(l)) * LN2 : -INFINITY;
-            if (MODE == MODE_DECODE && !(l > 0.f)) set_status(p.status, STS_DEV_EMPTY_ROW);
+          for (int j = 0; j < NO; ++j) {
+            const float4 x = dsmem_ld4(ra + (uint32_t)((j * NTH + tid) * 16));
+            o[j][0] = o[j][0] * fA + x.x * gA;
+            o[j][1] = o[j][1] * fA + x.y * gA;
+            o[j][2] = o[j][2] * fB + x.z * gB;
+            o[j][3] = o[j][3] * fB + x.w * gB;
           }
         }
       }
-      cluster_sync_all();  // partners keep their shared memory until rank 0 has read it
+      const float inv_a = la > 0.f ? 1.f / la : 0.f, inv_b = lb > 0.f ? 1.f / lb : 0.f;
+      const int dc = 2 * (lane & 3);
+      const int64_t u = iu;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = h ? rB : rA;
+        if (r >= M) continue;
+        const float inv = h ? inv_b : inv_a;
+        if constexpr (MODE == MODE_DECODE) {
+          if (p.out_f32) {
+            float* og = static_cast<float*>(p.out) + (u * M + r) * (int64_t)D + dc;
+#pragma unroll
+            for (int nt = 0; nt < D / 8; ++nt)
+              *reinterpret_cast<float2*>(og + nt * 8) = make_float2(o[nt][2 * h] * inv, o[nt][2 * h + 1] * inv);
+          } else {
+            __nv_bfloat16* og = static_cast<__nv_bfloat16*>(p.out) + (u * M + r) * (int64_t)D + dc;
+#pragma unroll
+            for (int nt = 0; nt < D / 8; ++nt)
+              *reinterpret_cast<__nv_bfloat162*>(og + nt * 8) =
+                  __floats2bfloat162_rn(o[nt][2 * h] * inv, o[nt][2 * h + 1] * inv);
+          }
+        }
+        if ((lane & 3) == 0) {
+          const float l = h ? lb : la;
+          const float m = h ? m_b : m_a;
+          if (p.lse) p.lse[u * M + r] = l > 0.f ? (m + __log2f(l)) * LN2 : -INFINITY;
+          if (MODE == MODE_DECODE && !(l > 0.f)) set_status(p.status, STS_DEV_EMPTY_ROW);
+        }
+      }
     }
+    cluster_sync_all();  // partners keep their shared memory until rank 0 has read it
   } else {
     if (cur_u >= 0) flush(cur_u, cur_P, cur_cnt, cur_range);
   }
@@ -906,7 +835,7 @@ int launch_verify(DecodeParams& p, cudaStream_t st) {
   const int smem = L::SMEM;
   kern<<<num_sms() * per_sm, L::THREADS, smem, st>>>(p);
   STS_LAUNCH_CHECK();
-  if (MODE != MODE_PROBS && p.pieces) {
+  if (p.pieces) {
     // one thread per (row, 4 dims) output element: every piece load in flight at once
     // (optional, -DSTS_PDL) programmatic dependent launch: the merge grid is
     // launched while the main kernel runs and waits (griddepcontrol.wait)
