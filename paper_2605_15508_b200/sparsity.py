@@ -6,6 +6,14 @@ fp32 / fp64 numpy results) and exceptions, but every mask / page sum /
 attention is produced by libsts_b200.so kernels.  Inputs may be numpy arrays
 or torch tensors (CUDA tensors avoid the host->device copy).  For batched
 device-resident work use ``kernels`` / ``verify_step`` directly.
+
+These functions are API glue around the kernels and pay per-call host costs
+the batched paths do not: numpy inputs are packed and copied to the device
+per call, results come back to the host as dicts, ``verification_masks``
+clamps on the host (``np.union1d`` per row), and ``sparse_attention`` ships
+the whole K/V it is given to the device on every call.  They exist so a
+reference caller can switch imports; the device pipelines
+(``verify_step.STSVerifyStep``, ``specdec.generate``) keep everything resident.
 """
 
 from __future__ import annotations
@@ -169,7 +177,9 @@ def remap_masks(draft_masks: dict, mapping: HeadMapping) -> dict:
 
 def sparse_attention(q, keys, values, mask) -> np.ndarray:
     """Single-query attention over the masked subset (src/sparsity.py:152-173),
-    computed by the fp32 gather kernel."""
+    computed by the fp32 gather kernel.  Slow path (API glue): copies the
+    given K/V to the device on every call; batched callers use
+    ``kernels.sparse_decode`` on resident caches."""
     idx = np.asarray(mask, dtype=np.int64).ravel()
     if idx.size == 0:
         raise ContractViolation("sparse attention needs a non-empty mask")
