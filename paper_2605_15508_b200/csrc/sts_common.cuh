@@ -52,9 +52,10 @@ int num_sms();
 // (-0.0 canonicalised to +0.0, NaN -> 0 i.e. below -inf)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t f32_key(float x) {
-  if (x != x) return 0u;
-  uint32_t b = __float_as_uint(x + 0.0f);
-  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+  // order-preserving: negatives -> ~bits, non-negatives -> bits | sign; -0 -> +0; NaN -> 0
+  const uint32_t b = __float_as_uint(x + 0.0f);
+  const uint32_t k = b ^ ((uint32_t)((int32_t)b >> 31) | 0x80000000u);
+  return x != x ? 0u : k;
 }
 
 __device__ __forceinline__ uint64_t f64_key(double x) {

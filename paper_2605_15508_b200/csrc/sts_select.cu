@@ -1,6 +1,13 @@
 // sts_select.cu — sparsity-mask construction on sm_100a.
 //
-// One CTA (1024 threads) per logical row.  The row's values are formed on the
+// Two kernels, one CTA (1024 threads) per logical row:
+//   select_reg_kernel  token mode, rows <= 32K keys: the row lives in
+//                      registers (32 keys per thread), see below;
+//   select_kernel      page mode and longer rows: keys in shared memory or a
+//                      global slot.
+// Both give identical results (same keys, same radix rule, same emit order).
+//
+// select_kernel: the row's values are formed on the
 // fly (fp32 sum of nsrc source rows: identity for mode R, head-group sum for
 // mode S), turned into order-preserving integer keys, and the k-th largest
 // key is found by an MSB-first radix select with 12-bit digits and 4096-bin
@@ -543,6 +550,328 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(SelectParams p) 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Token mode with the row in registers (rows <= 32 * KPT * 32 keys).
+//
+// One 1024-thread CTA per row.  Warp w owns the contiguous slice
+// [w*32*KPT, (w+1)*32*KPT) of the row; lane l holds positions
+// w*32*KPT + 128*g + 4*l + e (g < KPT/4, e < 4), so each source is read with
+// KPT/4 coalesced 16-byte loads per thread.  The radix passes read the keys
+// from registers (no key buffer, no candidate compaction); a pass stops early
+// when the threshold bin is taken whole.  Emit: per-g lane prefixes by a
+// packed warp scan (8-bit fields), warp totals -> one cross-warp scan, so
+// indices come out ascending and ties at the threshold go to the lowest
+// positions (src/numkit.py:84), exactly as select_kernel.  (A row split over
+// a 2-CTA cluster with DSMEM histograms measured slower: 51 vs 44 us at c2.)
+// ---------------------------------------------------------------------------
+// exclusive prefix over the CTA's NW warps of a warp-uniform value (1 barrier;
+// the caller syncs before scratch is reused)
+template <int NW>
+__device__ __forceinline__ int warp_excl_scan_of_warps(int v, int* scratch, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  int x = lane < NW ? scratch[lane] : 0;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += t;
+  }
+  total = __shfl_sync(0xffffffffu, x, 31);
+  return __shfl_sync(0xffffffffu, x, warp) - v;
+}
+
+// block-wide exclusive scan in thread order for NW warps (3 barriers)
+template <int NW>
+__device__ __forceinline__ int block_scan_nw(int v, int* warp_tot, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int x = lane < NW ? warp_tot[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += t;
+    }
+    if (lane < NW) warp_tot[lane] = x;  // inclusive prefix over warps
+  }
+  __syncthreads();
+  const int before = warp > 0 ? warp_tot[warp - 1] : 0;
+  total = warp_tot[NW - 1];
+  __syncthreads();
+  return before + incl - v;
+}
+
+// Lane-exclusive prefixes and warp totals of per-g nibble popcounts, packed
+// 4 groups per word in 8-bit fields (a lane count is <= 4, a warp's <= 128).
+template <int G>
+struct NibbleScan {
+  static constexpr int W = (G + 3) / 4;
+  uint32_t excl[W], tot[W];
+  __device__ __forceinline__ NibbleScan(uint32_t bits) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      uint32_t v = 0u;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (4 * w + q < G) v |= (uint32_t)__popc((bits >> (4 * (4 * w + q))) & 15u) << (8 * q);
+      uint32_t x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += t;
+      }
+      excl[w] = x - v;
+      tot[w] = __shfl_sync(0xffffffffu, x, 31);
+    }
+  }
+  __device__ __forceinline__ int before(int g) const { return (int)((excl[g >> 2] >> (8 * (g & 3))) & 255u); }
+  __device__ __forceinline__ int total(int g) const { return (int)((tot[g >> 2] >> (8 * (g & 3))) & 255u); }
+};
+
+// one histogram pass over the register keys; FULL: every key of the thread is
+// in the row, FIRST: every valid key matches the prefix (common bits)
+template <int KPT, bool FULL, bool FIRST>
+__device__ __forceinline__ void hist_pass(const uint32_t (&key)[KPT], uint32_t valid, uint32_t pmask,
+                                          uint32_t prefix, int s, uint32_t bmask, uint32_t* hist) {
+#pragma unroll
+  for (int i = 0; i < KPT; ++i) {
+    bool m = FIRST ? true : (key[i] & pmask) == prefix;
+    if (!FULL) m = m && ((valid >> i) & 1u);
+    if (m) atomicAdd(&hist[(key[i] >> s) & bmask], 1u);
+  }
+}
+
+template <int KPT, int NSRC>
+__global__ void __launch_bounds__(SEL_THREADS, 1) select_reg_kernel(SelectParams p) {
+  constexpr int NT = SEL_THREADS, NW = SEL_WARPS, G = KPT / 4;
+  constexpr int BPT = NBINS / NT;  // histogram bins per thread in the scan
+  static_assert(KPT % 4 == 0 && KPT <= 32 && NW == 32 && BPT * NT == NBINS, "layout");
+  __shared__ uint32_t hist[NBINS];
+  __shared__ int scan_a[NW], scan_b[NW];
+  __shared__ int bc[3];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool vec = (p.ld % 4) == 0 && (reinterpret_cast<uintptr_t>(p.scores) % 16) == 0;
+  const int nsrc = NSRC > 0 ? NSRC : p.nsrc;
+
+  for (int64_t r = blockIdx.x; r < p.rows; r += gridDim.x) {
+    const int n = p.row_len ? p.row_len[r] : p.n_common;
+    int32_t* out = p.idx_out + r * p.idx_ld;
+    int b;
+    if (p.budget_is_fraction) {
+      const double c = ceil(p.budget * (double)n);
+      b = c < 1.0 ? 1 : (int)c;
+    } else {
+      b = (int)p.budget;
+    }
+    int count = 0;
+    if (n <= 0) {
+    } else if (b >= n) {  // dense fallback (src/sparsity.py:90-91)
+      for (int j = threadIdx.x; j < n; j += SEL_THREADS) write_idx(p, out, j, j);
+      count = n;
+    } else {
+      const int wbase = warp * 32 * KPT;
+      const int jl = wbase + 4 * lane;  // position of (g, e) = jl + 128 g + e
+      const bool full = wbase + 32 * KPT <= n;  // warp-uniform
+      const float* srcp[NSRC > 0 ? NSRC : 8];
+#pragma unroll
+      for (int s = 0; s < (NSRC > 0 ? NSRC : 8); ++s)
+        if (s < nsrc) srcp[s] = p.scores + (int64_t)(p.row_src ? p.row_src[r * nsrc + s] : (int32_t)r) * p.ld;
+      // row values: fp32 sum over the sources in order (mode-S group reduction)
+      uint32_t key[KPT];
+      if (full && vec) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          float4 a = __ldg(reinterpret_cast<const float4*>(srcp[0] + jl + 128 * g));
+#pragma unroll
+          for (int s = 1; s < (NSRC > 0 ? NSRC : 8); ++s)
+            if (s < nsrc) {
+              const float4 x = __ldg(reinterpret_cast<const float4*>(srcp[s] + jl + 128 * g));
+              a.x = __fadd_rn(a.x, x.x);
+              a.y = __fadd_rn(a.y, x.y);
+              a.z = __fadd_rn(a.z, x.z);
+              a.w = __fadd_rn(a.w, x.w);
+            }
+          key[4 * g] = f32_key(a.x);
+          key[4 * g + 1] = f32_key(a.y);
+          key[4 * g + 2] = f32_key(a.z);
+          key[4 * g + 3] = f32_key(a.w);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < KPT; ++i) {
+          const int j = jl + 128 * (i >> 2) + (i & 3);
+          float a = 0.f;
+          if (j < n) {
+            a = __ldg(srcp[0] + j);
+            for (int s = 1; s < nsrc; ++s) a = __fadd_rn(a, __ldg(srcp[s] + j));
+          }
+          key[i] = f32_key(a);
+        }
+      }
+      uint32_t valid = 0xffffffffu;
+      if (!full) {
+        valid = 0u;
+#pragma unroll
+        for (int i = 0; i < KPT; ++i) valid |= (jl + 128 * (i >> 2) + (i & 3) < n ? 1u : 0u) << i;
+      }
+      uint32_t k_or = 0u, k_and = 0xffffffffu;
+      if (full) {
+#pragma unroll
+        for (int i = 0; i < KPT; ++i) {
+          k_or |= key[i];
+          k_and &= key[i];
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < KPT; ++i)
+          if ((valid >> i) & 1u) {
+            k_or |= key[i];
+            k_and &= key[i];
+          }
+      }
+      k_or = __reduce_or_sync(0xffffffffu, k_or);
+      k_and = __reduce_and_sync(0xffffffffu, k_and);
+      if (lane == 0) {
+        scan_a[warp] = (int)k_or;
+        scan_b[warp] = (int)k_and;
+      }
+      __syncthreads();
+      k_or = __reduce_or_sync(0xffffffffu, lane < NW ? (uint32_t)scan_a[lane] : 0u);
+      k_and = __reduce_and_sync(0xffffffffu, lane < NW ? (uint32_t)scan_b[lane] : 0xffffffffu);
+      __syncthreads();  // scan scratch is rewritten below
+
+      // MSB-first radix select over the bits that vary across the row;
+      // afterwards the threshold class is {key : (key & pmask) == prefix}
+      uint32_t pmask = 0xffffffffu, prefix = k_and;
+      int need = b, ties = n;
+      const uint32_t diff = k_or ^ k_and;
+      if (diff != 0u) {
+        int top = 31 - __clz((int)diff);
+        pmask = top >= 31 ? 0u : ~((2u << top) - 1u);
+        prefix = k_and & pmask;
+        int krem = b;
+        for (bool first = true;; top -= DIGIT_BITS, first = false) {
+          const int s = top - DIGIT_BITS + 1 < 0 ? 0 : top - DIGIT_BITS + 1;
+          const int nb = 1 << (top - s + 1);
+          uint32_t* h = hist;
+          if (!first) __syncthreads();  // previous pass's readers of hist are done
+          for (int q = threadIdx.x; q < nb; q += NT) h[q] = 0u;
+          __syncthreads();
+          const uint32_t bmask = (uint32_t)(nb - 1);
+          if (first) {
+            if (full) hist_pass<KPT, true, true>(key, valid, pmask, prefix, s, bmask, h);
+            else hist_pass<KPT, false, true>(key, valid, pmask, prefix, s, bmask, h);
+          } else {
+            if (full) hist_pass<KPT, true, false>(key, valid, pmask, prefix, s, bmask, h);
+            else hist_pass<KPT, false, false>(key, valid, pmask, prefix, s, bmask, h);
+          }
+          __syncthreads();
+          int local[BPT], lsum = 0;
+#pragma unroll
+          for (int q = 0; q < BPT; ++q) {
+            const int bin = nb - 1 - BPT * (int)threadIdx.x - q;
+            local[q] = bin >= 0 ? (int)h[bin] : 0;
+            lsum += local[q];
+          }
+          int total;
+          const int excl = block_scan_nw<NW>(lsum, scan_a, total);
+          if (excl < krem && krem <= excl + lsum) {
+            int a = excl;
+#pragma unroll
+            for (int q = 0; q < BPT; ++q) {
+              if (a < krem && krem <= a + local[q]) {
+                bc[0] = nb - 1 - BPT * (int)threadIdx.x - q;
+                bc[1] = a;
+                bc[2] = local[q];
+              }
+              a += local[q];
+            }
+          }
+          __syncthreads();
+          const int digit = bc[0], above = bc[1], inbin = bc[2];
+          prefix |= (uint32_t)digit << s;
+          pmask |= bmask << s;
+          krem -= above;
+          if (s == 0 || inbin == krem) {  // exact key, or the whole bin is taken
+            need = krem;
+            ties = inbin;
+            break;
+          }
+        }
+      }
+
+      // emit ascending: above-threshold keys, the first `need` of the class, extras
+      uint32_t gt = 0u, eq = 0u;
+#pragma unroll
+      for (int i = 0; i < KPT; ++i) {
+        const uint32_t hk = key[i] & pmask;
+        gt |= (hk > prefix ? 1u : 0u) << i;
+        eq |= (hk == prefix ? 1u : 0u) << i;
+      }
+      gt &= valid;
+      eq &= valid;
+      uint32_t sel = gt;
+      const int lo_extra = p.recent_window > 0 ? n - p.recent_window : n;
+      const bool cur = (p.flags & STS_SEL_CURRENT) != 0, sink = (p.flags & STS_SEL_SINK) != 0;
+      const int whi = wbase + 32 * KPT - 1;
+      if (whi >= lo_extra || (sink && wbase == 0) || (cur && whi >= n - 1 && wbase <= n - 1)) {
+#pragma unroll
+        for (int i = 0; i < KPT; ++i) {
+          const int j = jl + 128 * (i >> 2) + (i & 3);
+          if (j < n && (j >= lo_extra || (sink && j == 0) || (cur && j == n - 1))) sel |= 1u << i;
+        }
+      }
+      if (need == ties) {
+        sel |= eq;
+      } else {
+        int tot;
+        int rank = warp_excl_scan_of_warps<NW>(__reduce_add_sync(0xffffffffu, (uint32_t)__popc(eq)), scan_b, tot);
+        const NibbleScan<G> ns(eq);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          int rr = rank + ns.before(g);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if ((eq >> (4 * g + e)) & 1u) {
+              if (rr < need) sel |= 1u << (4 * g + e);
+              ++rr;
+            }
+          rank += ns.total(g);
+        }
+      }
+      int pos = warp_excl_scan_of_warps<NW>(__reduce_add_sync(0xffffffffu, (uint32_t)__popc(sel)), scan_a, count);
+      const NibbleScan<G> ns(sel);
+      const bool fits = count <= p.idx_ld;
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        int q = pos + ns.before(g);
+        uint32_t nib = (sel >> (4 * g)) & 15u;
+        while (nib) {  // set bits only (a tenth of the keys at 90% sparsity)
+          const int e = __ffs(nib) - 1;
+          if (fits) out[q] = jl + 128 * g + e;
+          else write_idx(p, out, q, jl + 128 * g + e);
+          ++q;
+          nib &= nib - 1u;
+        }
+        pos += ns.total(g);
+      }
+    }
+    // in-block tail (mode S: the verify block's own positions)
+    for (int t = threadIdx.x; t < p.tail_len; t += NT) write_idx(p, out, count + t, max(n, 0) + t);
+    if (threadIdx.x == 0) p.cnt_out[r] = count + p.tail_len;
+    __syncthreads();
+  }
+}
+
 // page_aggregate as a standalone op (src/sparsity.py:72-83): one thread per page
 __global__ void page_aggregate_kernel(SelectParams p, double* out, int64_t out_ld) {
   const int64_t r = blockIdx.y;
@@ -566,6 +895,14 @@ int64_t key_buf_bytes(int32_t max_len, int32_t page_size) {
 }
 
 constexpr int64_t SEL_SMEM_BUDGET = 227 * 1024 - (int64_t)sizeof(SelShared) - 256;
+
+// one CTA per row (grid-stride over rows beyond 2^30)
+template <int KPT, int NSRC>
+int launch_reg(const SelectParams& p, int64_t rows, cudaStream_t st) {
+  select_reg_kernel<KPT, NSRC><<<(unsigned)rows, SEL_THREADS, 0, st>>>(p);
+  STS_LAUNCH_CHECK();
+  return STS_OK;
+}
 
 }  // namespace
 }  // namespace sts
@@ -623,6 +960,17 @@ extern "C" int sts_select_topk(const float* scores_dev, int64_t ld, const int32_
   p.status = status_dev;
   p.buf_bytes = key_buf_bytes(max_len, page_size);
 
+  // token rows that fit in registers (<= 32K keys): select_reg_kernel
+  // (c2: 44 us vs 63 us for select_kernel, profiles/r02/select/)
+  if (page_size == 1 && max_len <= 32 * 32 * SEL_WARPS) {
+    const int64_t grid = rows < ((int64_t)1 << 30) ? rows : ((int64_t)1 << 30);
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (max_len <= 8 * 32 * SEL_WARPS) return launch_reg<8, 0>(p, grid, st);
+    if (max_len <= 16 * 32 * SEL_WARPS) return launch_reg<16, 0>(p, grid, st);
+    if (nsrc == 1) return launch_reg<32, 1>(p, grid, st);
+    if (nsrc == 4) return launch_reg<32, 4>(p, grid, st);
+    return launch_reg<32, 0>(p, grid, st);
+  }
   const size_t sh_bytes = (sizeof(SelShared) + 15) & ~size_t(15);
   size_t smem = sh_bytes;
   int grid;

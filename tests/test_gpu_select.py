@@ -186,37 +186,43 @@ def test_capacity_status_flag(cuda_ok):
     assert status.item() & 0x1
 
 
-def test_cluster_select_variant(cuda_ok):
-    """The selection parity suite again through the experimental cluster select
-    (STS_SELECT_CLUSTER=1: token-mode rows split over a thread-block cluster,
-    histograms exchanged through DSMEM), in a subprocess because the library
-    reads the knob once."""
-    import os
-    import subprocess
-    import sys
-    from pathlib import Path
+@pytest.mark.parametrize("n", [8192, 8193, 16384, 16385, 32767, 32768, 32769])
+def test_register_select_boundaries(cuda_ok, n):
+    """Token rows around the register kernel's capacity steps (8K / 16K / 32K
+    keys per CTA; 32769 falls back to select_kernel): every row kind, ties
+    spanning many warps (coarse rows), extras — bit-exact vs the oracle."""
+    from paper_2605_15508_b200 import SparsityConfig
+    from paper_2605_15508_b200.sparsity import select_rows
 
-    root = Path(__file__).resolve().parent.parent
-    env = dict(os.environ, STS_SELECT_CLUSTER="1")
-    r = subprocess.run([sys.executable, "-m", "pytest", str(root / "tests" / "test_gpu_select.py"), "-q", "-x",
-                        "-p", "no:cacheprovider", "-k", "not variant"],
-                       env=env, cwd=root, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    rng = np.random.default_rng(n)
+    rows = [_rows_kind(rng, n, k) for k in ("softmax", "ties", "coarse", "special")]
+    rows.append(_rows_kind(rng, n - 5, "coarse"))  # ragged last warp
+    for budget, cur, sink, win in ((0.1, True, False, 0), (0.3, False, True, 300), (4096, True, True, 1)):
+        cfg = SparsityConfig(budget=budget, page_size=1, include_current=cur, include_sink=sink,
+                             recent_window=win)
+        got = select_rows(rows, cfg)
+        ocfg = O.OracleSparsityConfig(budget, 1, cur, sink, win)
+        for r, m in zip(rows, got):
+            np.testing.assert_array_equal(m, O.select_row(r, ocfg))
 
 
-def test_prefix16_select_variant(cuda_ok):
-    """The selection parity suite again through the experimental 16-bit prefix
-    select (STS_SELECT_V2=1: token-mode rows <= 48K keep 2-byte key prefixes on
-    chip, full keys recomputed for the threshold bin), in a subprocess because
-    the library reads the knob once."""
-    import os
-    import subprocess
-    import sys
-    from pathlib import Path
+@pytest.mark.parametrize("nsrc", [1, 2, 3, 4, 5])
+def test_register_select_head_groups_32k(cuda_ok, nsrc):
+    """Mode-S group sums at the c2 row length (32K committed keys) through the
+    register kernel's per-nsrc instances, tie-heavy sources included."""
+    import torch
 
-    root = Path(__file__).resolve().parent.parent
-    env = dict(os.environ, STS_SELECT_V2="1")
-    r = subprocess.run([sys.executable, "-m", "pytest", str(root / "tests" / "test_gpu_select.py"), "-q", "-x",
-                        "-p", "no:cacheprovider", "-k", "not variant"],
-                       env=env, cwd=root, capture_output=True, text=True, timeout=600)
-    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    from paper_2605_15508_b200 import kernels
+
+    rng = np.random.default_rng(100 + nsrc)
+    S, base, tail = 12, 32768, 5
+    D = np.stack([_rows_kind(rng, base + tail, "softmax" if s % 3 else "coarse") for s in range(S)])
+    src = rng.integers(0, S, size=(6, nsrc)).astype(np.int32)
+    ocfg = O.OracleSparsityConfig(0.1, 1, False, False, 0)
+    b = ocfg.tokens_for_context(base + 1)
+    idx, cnt = kernels.select_topk(torch.from_numpy(D).cuda(), row_src=torch.from_numpy(src), n_common=base,
+                                   budget=int(b), page_size=1, include_current=False, tail_len=tail)
+    idx, cnt = idx.cpu().numpy(), cnt.cpu().numpy()
+    for r in range(src.shape[0]):
+        red = O.reduce_rows_fp32([D[s] for s in src[r]])
+        np.testing.assert_array_equal(idx[r, : cnt[r]], O.mode_s_index_list(red, base, tail, ocfg))

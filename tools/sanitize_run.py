@@ -40,6 +40,10 @@ if "select" in which:
     for ps in (1, 16):
         kernels.select_topk(rows, budget=0.1, page_size=ps, row_len=torch.full((6,), 1500, dtype=torch.int32, device=dev),
                             include_sink=True, recent_window=4)
+    # register kernel at 32K keys (4-source group sums, tie-heavy rows -> ranked ties across warps)
+    coarse = torch.floor(torch.rand((4, 32776), generator=g, device=dev) * 4) / 4
+    src = torch.tensor([[0, 1, 2, 3], [3, 2, 1, 0]], dtype=torch.int32, device=dev)
+    kernels.select_topk(coarse, budget=3277, row_src=src, n_common=32768, include_current=False, tail_len=5)
 if "dist" in which:
     n = 70001
     rows = torch.rand((3, -(-n // 4) * 4), generator=g, device=dev)
