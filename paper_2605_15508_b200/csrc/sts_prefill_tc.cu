@@ -270,9 +270,13 @@ __global__ void __launch_bounds__(PF_THREADS, 1) prefill_tc_kernel(const __grid_
         }
         pf_commit(&sfull[slot]);
       };
+      // S_{j+2} reuses S_j's TMEM slot: it is issued as soon as group j&1 has
+      // read S_j into registers (early in softmax j), not after PV_j, so the
+      // group's next scores are ready when its softmax finishes
       if (nb > 0) issue_s(0);
+      if (nb > 1) issue_s(1);
       for (int j = 0; j < nb; ++j) {
-        if (j + 1 < nb) issue_s(j + 1);
+        if (j + 2 < nb) issue_s(j + 2);
         const int stage = j % PF_STAGES;
         pf_wait(&pfull[j & 1], (j >> 1) & 1);
         pf_fence_after();
@@ -309,27 +313,51 @@ __global__ void __launch_bounds__(PF_THREADS, 1) prefill_tc_kernel(const __grid_
       pf_wait_ld();
       pf_fence_before();
       pf_arrive(&sempty[slot]);
-      const bool diag = j >= ncommit;
+      // row max of the raw scores (the scale is folded into the exponent's FFMA)
       float mx = -INFINITY;
+      if (j >= ncommit) {  // diagonal block: causal mask (and the ragged end of the prompt)
 #pragma unroll
-      for (int c = 0; c < PF_BLK; ++c) {
-        const int key = b * PF_BLK + c;
-        const bool ok = !diag || (key <= row && key < p.n);
-        s[c] = ok ? s[c] * sl2 : -INFINITY;
-        mx = fmaxf(mx, s[c]);
+        for (int c = 0; c < PF_BLK; ++c) {
+          const int key = b * PF_BLK + c;
+          s[c] = (key <= row && key < p.n) ? s[c] : -INFINITY;
+          mx = fmaxf(mx, s[c]);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < PF_BLK; ++c) mx = fmaxf(mx, s[c]);
       }
-      // this group's previous PV (j - 2) read P buffer j&1 and wrote O_grp
-      if (j >= 2) pf_wait(&odone[slot], ((j - 2) >> 1) & 1);
+      mx *= sl2;
       // lazy rescale, warp-uniform (tcgen05.ld/st are warp-collective): rows
       // whose max grew by > 2^8 rescale their O row
       const bool need = mx > m + PF_RESCALE;
-      if (__any_sync(0xffffffffu, need)) {
+      const bool any = __any_sync(0xffffffffu, need);
+      float m_new = m, f = 1.f;
+      if (any) {
         if (j < 2) {
-          m = mx;  // the group's first block: its PV overwrites O_grp
+          m_new = mx;  // the group's first block: its PV overwrites O_grp
+        } else if (need) {
+          f = fast_exp2(m - mx);
+          m_new = mx;
+        }
+      }
+      const float mb = m_new == -INFINITY ? 0.f : m_new;  // a row with no key yet: P = 0, not NaN
+      // P = 2^(s - m) in bf16 (before waiting for the group's previous PV)
+      uint32_t w[PF_BLK / 2];
+      float rs = 0.f;
+#pragma unroll
+      for (int e = 0; e < PF_BLK / 2; ++e) {
+        const float a0 = fast_exp2(fmaf(s[2 * e], sl2, -mb)), a1 = fast_exp2(fmaf(s[2 * e + 1], sl2, -mb));
+        rs += a0 + a1;
+        const __nv_bfloat162 h = __floats2bfloat162_rn(a0, a1);
+        w[e] = *reinterpret_cast<const uint32_t*>(&h);
+      }
+      // this group's previous PV (j - 2) read P buffer j&1 and wrote O_grp
+      if (j >= 2) pf_wait(&odone[slot], ((j - 2) >> 1) & 1);
+      if (any) {
+        if (j < 2) {
           l = 0.f;
         } else {
           pf_fence_after();
-          const float f = need ? fast_exp2(m - mx) : 1.f;
 #pragma unroll
           for (int c0 = 0; c0 < D; c0 += 32) {
             float o[32];
@@ -341,25 +369,15 @@ __global__ void __launch_bounds__(PF_THREADS, 1) prefill_tc_kernel(const __grid_
           }
           pf_wait_st();
           l *= f;
-          if (need) m = mx;
         }
       }
-      const float mb = m == -INFINITY ? 0.f : m;  // a row with no key yet: P = 0, not NaN
-      // P = 2^(s - m) in bf16, K-major 128B-swizzled rows of the A operand
+      m = m_new;
+      // K-major 128B-swizzled rows of the A operand
       uint8_t* prow = smem + L::OFF_P + slot * L::P_BYTES + r * 128;
-      float rs = 0.f;
 #pragma unroll
-      for (int c8 = 0; c8 < PF_BLK / 8; ++c8) {
-        uint32_t w[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float a0 = fast_exp2(s[c8 * 8 + 2 * e] - mb), a1 = fast_exp2(s[c8 * 8 + 2 * e + 1] - mb);
-          const __nv_bfloat162 h = __floats2bfloat162_rn(a0, a1);
-          rs += __low2float(h) + __high2float(h);  // the row sum of what the MMA multiplies
-          w[e] = *reinterpret_cast<const uint32_t*>(&h);
-        }
-        *reinterpret_cast<uint4*>(prow + ((c8 ^ (r & 7)) * 16)) = make_uint4(w[0], w[1], w[2], w[3]);
-      }
+      for (int c8 = 0; c8 < PF_BLK / 8; ++c8)
+        *reinterpret_cast<uint4*>(prow + ((c8 ^ (r & 7)) * 16)) =
+            make_uint4(w[4 * c8], w[4 * c8 + 1], w[4 * c8 + 2], w[4 * c8 + 3]);
       l += rs;
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // P visible to the tensor core
       pf_fence_before();
