@@ -11,10 +11,11 @@
 // CTA = (q-head, query tile), 128 rows = the 128 TMEM lanes.  Warp roles:
 //   warp 0   TMA producer: Q tile once, then K and V blocks of the list
 //            (128B swizzle; ring of STAGES (K, V) blocks)
-//   warp 1   MMA issuer: S_j = Q.K_j^T (M=128 rows, N=64 keys, K=d) into one of
-//            two TMEM S slots; O += P_j.V_j (M=128, N=d, K=64; V as an
-//            MN-major operand) into the TMEM O accumulator
-//   warps 2-5 softmax, thread = query row: tcgen05.ld of its S row, causal
+//   warps 1-2 MMA issuers, one per softmax group (even / odd key blocks):
+//            S_j = Q.K_j^T (M=128 rows, N=64 keys, K=d) into the group's
+//            TMEM S slot, issued as soon as the group has read S_{j-2};
+//            O_g += P_j.V_j (M=128, N=d, K=64; V as an MN-major operand)
+//   warps 3-10 softmax (two groups of 4), thread = query row: tcgen05.ld of its S row, causal
 //            mask on diagonal blocks, online max with lazy rescale (O rows in
 //            TMEM rescaled only when the max grows by > 2^8), P in bf16 to
 //            shared memory (swizzled K-major A operand), row sums in fp32;
@@ -29,7 +30,7 @@ namespace {
 constexpr int PF_ROWS = 128;   // query tile = MMA M = TMEM lanes
 constexpr int PF_BLK = 64;     // keys per block = MMA N of S, K of PV
 constexpr int PF_STAGES = 4;
-constexpr int PF_THREADS = 320;  // TMA, MMA, two softmax warp groups (even / odd key blocks)
+constexpr int PF_THREADS = 352;  // TMA, two MMA issuers, two softmax warp groups (even / odd key blocks)
 constexpr float PF_RESCALE = 8.f;  // log2 growth of the row max that forces an O rescale
 
 __device__ __forceinline__ void pf_mbar_init(uint64_t* bar, uint32_t count) {
@@ -247,17 +248,19 @@ __global__ void __launch_bounds__(PF_THREADS, 1) prefill_tc_kernel(const __grid_
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 || warp == 2) {
+    // one MMA issuer per softmax group (warp 1: even blocks, warp 2: odd
+    // blocks), so neither group's next S waits behind the other group's P
     if (lane == 0) {
+      const int g = warp - 1;
       constexpr uint32_t id_s = pf_idesc(PF_ROWS, PF_BLK, false);
       constexpr uint32_t id_o = pf_idesc(PF_ROWS, D, true);
       pf_wait(qfull, 0);
       pf_fence_after();
-      // S_j for j = 0, then per j: S_{j+1} (overlaps softmax j), PV_j
-      auto issue_s = [&](int j) {
+      auto issue_s = [&](int j) {  // S_j into TMEM slot j & 1 (= g)
         const int stage = j % PF_STAGES;
         const uint32_t slot = j & 1;
-        pf_wait(&sempty[slot], ((j >> 1) & 1) ^ 1);
+        pf_wait(&sempty[slot], ((j >> 1) & 1) ^ 1);  // the group has read S_{j-2}
         pf_wait(&full[stage], (j / PF_STAGES) & 1);
         pf_fence_after();
         const uint32_t d_tmem = tmem + slot * L::S_COLS;
@@ -270,32 +273,30 @@ __global__ void __launch_bounds__(PF_THREADS, 1) prefill_tc_kernel(const __grid_
         }
         pf_commit(&sfull[slot]);
       };
-      // S_{j+2} reuses S_j's TMEM slot: it is issued as soon as group j&1 has
-      // read S_j into registers (early in softmax j), not after PV_j, so the
-      // group's next scores are ready when its softmax finishes
-      if (nb > 0) issue_s(0);
-      if (nb > 1) issue_s(1);
-      for (int j = 0; j < nb; ++j) {
+      // S_{j+2} reuses S_j's slot: issued as soon as the group has read S_j
+      // (early in softmax j), so its next scores are ready when it finishes
+      if (g < nb) issue_s(g);
+      for (int j = g; j < nb; j += 2) {
         if (j + 2 < nb) issue_s(j + 2);
         const int stage = j % PF_STAGES;
-        pf_wait(&pfull[j & 1], (j >> 1) & 1);
+        pf_wait(&pfull[g], (j >> 1) & 1);
         pf_fence_after();
-        const uint64_t ad = pf_desc_k(smem + L::OFF_P + (j & 1) * L::P_BYTES);
+        const uint64_t ad = pf_desc_k(smem + L::OFF_P + g * L::P_BYTES);
         // V block [64 keys][D] as an MN-major B operand: MN atoms (64 d) are
         // the slabs (LBO), K groups of 8 keys are 1024 B apart (SBO)
         const uint64_t bd = pf_desc_mn(smem + L::OFF_V + stage * L::KB_BYTES, PF_BLK * 128, 1024);
 #pragma unroll
         for (int k = 0; k < PF_BLK / 16; ++k)
-          pf_mma(tmem + L::O_COL + (j & 1) * D, ad + 2 * k, bd + (uint64_t)((16 * 128) >> 4) * k, id_o,
+          pf_mma(tmem + L::O_COL + g * D, ad + 2 * k, bd + (uint64_t)((16 * 128) >> 4) * k, id_o,
                  (j >= 2 || k != 0) ? 1u : 0u);
-        pf_commit(&empty[stage]);   // K and V of this block no longer read
-        pf_commit(&odone[j & 1]);   // O_{j&1} holds its group's blocks up to j (frees P buffer j & 1)
+        pf_commit(&empty[stage]);  // K and V of this block no longer read
+        pf_commit(&odone[g]);      // O_g holds the group's blocks up to j (frees P buffer g)
       }
     }
   } else {
     // ===== softmax: thread = query row; group g takes the blocks j = g mod 2 =====
     const int quad = warp & 3;
-    const int grp = (warp - 2) >> 2;
+    const int grp = (warp - 3) >> 2;
     const int r = quad * 32 + lane;       // row within the tile (TMEM lane)
     const int row = T * PF_ROWS + r;      // query position
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
