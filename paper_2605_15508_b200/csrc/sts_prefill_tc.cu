@@ -29,7 +29,7 @@ namespace {
 
 constexpr int PF_ROWS = 128;   // query tile = MMA M = TMEM lanes
 constexpr int PF_BLK = 64;     // keys per block = MMA N of S, K of PV
-constexpr int PF_STAGES = 4;
+constexpr int PF_STAGES = 5;
 constexpr int PF_THREADS = 352;  // TMA, two MMA issuers, two softmax warp groups (even / odd key blocks)
 constexpr float PF_RESCALE = 8.f;  // log2 growth of the row max that forces an O rescale
 
