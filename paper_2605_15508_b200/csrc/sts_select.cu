@@ -343,6 +343,48 @@ __device__ double pairwise_vals(const float* vals, int start, int n) {
   return __dadd_rn(pairwise_vals(vals, start, n2), pairwise_vals(vals, start + n2, n - n2));
 }
 
+// np.add.reduceat segment of page pg, x[start] + pairwise(x[start+1 : start+len]),
+// computed by the 8 lanes (lane & 7) of an aligned octet for pages whose
+// pairwise part has 8..128 elements: lane j accumulates chain r[j] (elements
+// j, j+8, ... of the 8-aligned body), the octet combines
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) by shuffles, lane 0 adds the tail and
+// x[start] — the same operations in the same order as pairwise_vals.  Every
+// lane of the warp must call it (shuffles); pages >= P return 0.
+__device__ __forceinline__ uint64_t page_key_lanes(const float* vals, int pg, int P, int n_row, int ps) {
+  const int j = threadIdx.x & 7;
+  const bool live = pg < P;
+  const int start = live ? pg * ps : 0;
+  const int len = live ? min(ps, n_row - start) : 1;
+  const int m = len - 1;  // pairwise part
+  const bool chains = m >= 8;  // (m <= 128 by the caller's page size)
+  const int body = m - m % 8;
+  double r = 0.0;
+  if (chains) {
+    r = (double)vals[start + 1 + j];
+    for (int i = 8; i < body; i += 8) r = __dadd_rn(r, (double)vals[start + 1 + i + j]);
+  }
+  double o = __shfl_xor_sync(0xffffffffu, r, 1);
+  r = __dadd_rn(r, o);  // lanes 0,2,4,6: (r0+r1), (r2+r3), ...
+  o = __shfl_xor_sync(0xffffffffu, r, 2);
+  r = __dadd_rn(r, o);  // lanes 0,4
+  o = __shfl_xor_sync(0xffffffffu, r, 4);
+  r = __dadd_rn(r, o);  // lane 0: the tree
+  uint64_t key = 0ull;
+  if (j == 0 && live) {
+    double res;
+    if (chains) {
+      res = r;
+      for (int i = body; i < m; ++i) res = __dadd_rn(res, (double)vals[start + 1 + i]);
+    } else {
+      res = 0.0;
+      for (int i = 0; i < m; ++i) res = __dadd_rn(res, (double)vals[start + 1 + i]);
+    }
+    const double x0 = (double)vals[start];
+    key = f64_key(len == 1 ? x0 : __dadd_rn(x0, res));
+  }
+  return key;
+}
+
 // Emit pass over `len` candidates in index order, 4 per thread per chunk.
 // sel(j, tie_rank_before_j_is_lt_need) decides membership; writes ascending.
 template <typename KeyAt, typename Extra>
@@ -458,6 +500,37 @@ __device__ int emit_tokens(const SelectParams& p, SelShared& sh, int32_t* out, c
   return run_sel;
 }
 
+constexpr int RANK_PAGES = SEL_THREADS / 4;  // page rows up to this many pages use all-pairs ranks
+
+// Tokens of the selected pages (pbits) in ascending order: a block scan over
+// the pages gives each selected page its output slot; the page's positions
+// are written by a quarter-warp (8 lanes x 16 B).  Returns the token count.
+__device__ int expand_pages(const SelectParams& p, SelShared& sh, int32_t* out, const uint32_t* pbits, int P, int n,
+                            int ps) {
+  const int lane = threadIdx.x & 31;
+  int run = 0;
+  for (int base = 0; base < P; base += SEL_THREADS) {
+    const int pg = base + threadIdx.x;
+    const bool sel = pg < P && ((pbits[pg >> 5] >> (pg & 31)) & 1u);
+    int tot;
+    const int rank = run + block_scan_int(sel ? 1 : 0, sh.warp_tot, tot);
+    // every selected page but the row's last is whole: slot = rank * ps
+    uint32_t m = __ballot_sync(0xffffffffu, sel);
+    while (m) {  // the warp's selected pages, one at a time, 32 lanes per page
+      const int src = __ffs(m) - 1;
+      m &= m - 1;
+      const int g = __shfl_sync(0xffffffffu, pg, src), rk = __shfl_sync(0xffffffffu, rank, src);
+      const int len = min(ps, n - g * ps);
+      for (int e = lane; e < len; e += 32) write_idx(p, out, rk * ps + e, g * ps + e);
+    }
+    run += tot;
+  }
+  // the row's last page may be partial: it is the last selected page if selected
+  const int last_len = n - (P - 1) * ps;
+  const bool last_sel = P > 0 && ((pbits[(P - 1) >> 5] >> ((P - 1) & 31)) & 1u);
+  return run * ps - (last_sel ? ps - last_len : 0);
+}
+
 __global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(SelectParams p) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   SelShared& sh = *reinterpret_cast<SelShared*>(smem_raw);
@@ -519,28 +592,72 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(SelectParams p) 
         for_row_values(p, srcs, n, [&](int j, float v) { vals[j] = v; });
         __syncthreads();
         uint64_t p_or = 0ull, p_and = ~0ull;
-        for (int pg = threadIdx.x; pg < P; pg += SEL_THREADS) {
-          const int start = pg * ps;
-          const int len = min(ps, n - start);
-          // np.add.reduceat segment: x[start] + pairwise(x[start+1 : start+len])
-          const double x0 = (double)vals[start];
-          const uint64_t key = f64_key(len == 1 ? x0 : __dadd_rn(x0, pairwise_vals(vals, start + 1, len - 1)));
-          pkeys[pg] = key;
-          p_or |= key;
-          p_and &= key;
+        if (ps >= 9 && ps <= 129) {
+          // 8 lanes per page: lane j sums pairwise chain j, the chains meet in
+          // numpy's fixed tree order through shuffles (see page_key_lanes)
+          for (int base = 0; base < P; base += SEL_THREADS / 8) {
+            const int pg = base + (int)(threadIdx.x >> 3);
+            const uint64_t key = page_key_lanes(vals, pg, P, n, ps);
+            if ((threadIdx.x & 7) == 0 && pg < P) {
+              pkeys[pg] = key;
+              p_or |= key;
+              p_and &= key;
+            }
+          }
+        } else {
+          for (int pg = threadIdx.x; pg < P; pg += SEL_THREADS) {
+            const int start = pg * ps;
+            const int len = min(ps, n - start);
+            // np.add.reduceat segment: x[start] + pairwise(x[start+1 : start+len])
+            const double x0 = (double)vals[start];
+            const uint64_t key = f64_key(len == 1 ? x0 : __dadd_rn(x0, pairwise_vals(vals, start + 1, len - 1)));
+            pkeys[pg] = key;
+            p_or |= key;
+            p_and &= key;
+          }
         }
-        block_or_and(p_or, p_and, sh);
-        uint64_t T;
-        int need, ties;
-        radix_select<uint64_t>(pkeys, P, kp, p_or, p_and, sh, reinterpret_cast<uint64_t*>(sh.cand), CAND_BYTES / 8, T,
-                               need, ties);
-        emit_sorted(p, sh, out, P, [&](int j) { return pkeys[j]; }, T, need, [](int) { return false; }, 0, true,
-                    pbits, need == ties);
+        block_or_and(p_or, p_and, sh);  // (its barriers also publish pkeys[])
+        if (P <= RANK_PAGES) {
+          // few pages: exact ranks by all-pairs comparison (4 threads per page,
+          // a quarter of the keys each) instead of 64-bit radix passes; rank =
+          // #greater + #equal at a lower index (the stable tie rule)
+          int* part = reinterpret_cast<int*>(sh.cand);  // [4][RANK_PAGES]
+          const int t = threadIdx.x % RANK_PAGES, q = threadIdx.x / RANK_PAGES;
+          if (t < P) {
+            const uint64_t kt = pkeys[t];
+            const int i0 = q * P / 4, i1 = (q + 1) * P / 4;
+            int c = 0;
+            for (int i = i0; i < i1; ++i) {
+              const uint64_t ki = pkeys[i];
+              c += (ki > kt || (ki == kt && i < t)) ? 1 : 0;
+            }
+            part[q * RANK_PAGES + t] = c;
+          }
+          __syncthreads();
+          if (q == 0) {
+            const bool sel = t < P && part[t] + part[RANK_PAGES + t] + part[2 * RANK_PAGES + t] +
+                                              part[3 * RANK_PAGES + t] < kp;
+            const uint32_t bal = __ballot_sync(0xffffffffu, sel);
+            if ((threadIdx.x & 31) == 0 && threadIdx.x < ((P + 31) & ~31)) pbits[threadIdx.x >> 5] = bal;
+          }
+        } else {
+          uint64_t T;
+          int need, ties;
+          radix_select<uint64_t>(pkeys, P, kp, p_or, p_and, sh, reinterpret_cast<uint64_t*>(sh.cand), CAND_BYTES / 8,
+                                 T, need, ties);
+          emit_sorted(p, sh, out, P, [&](int j) { return pkeys[j]; }, T, need, [](int) { return false; }, 0, true,
+                      pbits, need == ties);
+        }
       }
       __syncthreads();
-      count = emit_sorted(p, sh, out, n,
-                          [&](int j) { return (uint64_t)((pbits[(j / ps) >> 5] >> ((j / ps) & 31)) & 1u); },
-                          0ull, 0, extra, 0, false, nullptr);  // selected iff page bit (key) > 0
+      if (p.flags == 0 && p.recent_window == 0) {
+        // no extras: the tokens are the selected pages, expanded in page order
+        count = expand_pages(p, sh, out, pbits, P, n, ps);
+      } else {
+        count = emit_sorted(p, sh, out, n,
+                            [&](int j) { return (uint64_t)((pbits[(j / ps) >> 5] >> ((j / ps) & 31)) & 1u); },
+                            0ull, 0, extra, 0, false, nullptr);  // selected iff page bit (key) > 0
+      }
     }
     // in-block tail (mode S: the verify block's own positions)
     for (int t = threadIdx.x; t < p.tail_len; t += SEL_THREADS) write_idx(p, out, count + t, max(n, 0) + t);

@@ -47,6 +47,11 @@ for n in a.n:
     scores = torch.softmax(2 * torch.randn((Hkv * tiles, -(-n // 4) * 4), generator=g, device=dev), -1).contiguous()
     sel = {}
     t_sel = timeit(lambda: sel.update(zip(("idx", "cnt"), kernels.prefill_tile_select(scores, budget=0.1, n=n))))
+    # the same selection replayed as a CUDA graph (no host launch gaps)
+    gsel = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gsel):
+        gi, gc = kernels.prefill_tile_select(scores, budget=0.1, n=n)
+    t_sel_graph = timeit(gsel.replay)
     out = torch.empty_like(q)
     t_sp = timeit(lambda: kernels.prefill_blocksparse(q, k, v, idx=sel["idx"], cnt=sel["cnt"], out=out))
     t_dn = timeit(lambda: kernels.prefill_blocksparse(q, k, v, out=out))
@@ -55,7 +60,8 @@ for n in a.n:
     flops_dense = 4.0 * Hq * d * sum(min(128 * T + 128, n) * 128 - 64 * 127 for T in range(tiles))
     line = {"workload": f"block-sparse prefill, one Llama-3.1-8B layer (32 q / 8 kv heads, d=128), n={n}, "
                         "budget 0.1 per 128-row tile, 64-key blocks",
-            "tile_select_us": round(t_sel, 1), "sparse_prefill_us": round(t_sp, 1),
+            "tile_select_us": round(t_sel, 1), "tile_select_graph_us": round(t_sel_graph, 1),
+            "sparse_prefill_us": round(t_sp, 1),
             "sparse_incl_select_us": round(t_sel + t_sp, 1), "dense_same_kernel_us": round(t_dn, 1),
             "block_fraction": round(blocks / dense_blocks, 3),
             "dense_same_kernel_TFLOPs": round(flops_dense / (t_dn * 1e-6) / 1e12, 1)}
