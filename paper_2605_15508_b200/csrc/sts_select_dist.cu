@@ -184,7 +184,28 @@ __device__ __forceinline__ double page_sum_regs(const DistParams& p, const int32
 // position chunk of every row, so a draft row mapped into several target rows
 // (mode S sums each target row's mapped draft rows) is read from HBM once and
 // from L2 for its other targets
-template <typename K>
+// token keys of 4 consecutive positions j..j+3: one 16-byte load per source
+// row (NS sources; NS = 0: p.nsrc at run time), summed in source order
+template <int NS>
+__device__ __forceinline__ float4 dist_sum4(const DistParams& p, const int32_t* srcs, int j) {
+  constexpr int MAXS = NS > 0 ? NS : 8;
+  float4 v[MAXS];
+#pragma unroll
+  for (int q = 0; q < MAXS; ++q)
+    if (NS > 0 || q < p.nsrc) v[q] = __ldg(reinterpret_cast<const float4*>(p.scores + (int64_t)srcs[q] * p.ld + j));
+  float4 a = v[0];
+#pragma unroll
+  for (int q = 1; q < MAXS; ++q)
+    if (NS > 0 || q < p.nsrc) {
+      a.x = __fadd_rn(a.x, v[q].x);
+      a.y = __fadd_rn(a.y, v[q].y);
+      a.z = __fadd_rn(a.z, v[q].z);
+      a.w = __fadd_rn(a.w, v[q].w);
+    }
+  return a;
+}
+
+template <typename K, int NS = 0>
 __global__ void __launch_bounds__(DIST_THREADS) dist_keys_kernel(DistParams p, int32_t* hist) {
   __shared__ uint32_t sh[DD_BINS];
   const int64_t r = (int64_t)blockIdx.x % p.rows;
@@ -214,27 +235,25 @@ __global__ void __launch_bounds__(DIST_THREADS) dist_keys_kernel(DistParams p, i
     if (p.vec4) {
       // 4 consecutive positions per thread: one 16-byte load per source row
       // (rows are padded to a multiple of 4), sources summed in order
-      for (int j = chunk * DIST_CHUNK + 4 * threadIdx.x; j < j_end; j += 4 * DIST_THREADS) {
-        float4 v[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (q < p.nsrc) v[q] = *reinterpret_cast<const float4*>(p.scores + (int64_t)srcs[q] * p.ld + j);
-        float4 a = v[0];
-#pragma unroll
-        for (int q = 1; q < 8; ++q)
-          if (q < p.nsrc) {
-            a.x = __fadd_rn(a.x, v[q].x);
-            a.y = __fadd_rn(a.y, v[q].y);
-            a.z = __fadd_rn(a.z, v[q].z);
-            a.w = __fadd_rn(a.w, v[q].w);
-          }
+      // two 4-position groups per iteration: both groups' loads in flight together
+      auto put = [&](int j, const float4& a) {
         const uint4 k4 = make_uint4(f32_key(a.x), f32_key(a.y), f32_key(a.z), f32_key(a.w));
         *reinterpret_cast<uint4*>(keys + j) = k4;
         atomicAdd(&sh[digit_of<K>(k4.x, 0)], 1u);
         if (j + 1 < j_end) atomicAdd(&sh[digit_of<K>(k4.y, 0)], 1u);
         if (j + 2 < j_end) atomicAdd(&sh[digit_of<K>(k4.z, 0)], 1u);
         if (j + 3 < j_end) atomicAdd(&sh[digit_of<K>(k4.w, 0)], 1u);
+      };
+      constexpr int STEP = 4 * DIST_THREADS;
+      int j = chunk * DIST_CHUNK + 4 * threadIdx.x;
+      if constexpr (NS > 0) {
+        for (; j + STEP < j_end; j += 2 * STEP) {
+          const float4 a = dist_sum4<NS>(p, srcs, j), b = dist_sum4<NS>(p, srcs, j + STEP);
+          put(j, a);
+          put(j + STEP, b);
+        }
       }
+      for (; j < j_end; j += STEP) put(j, dist_sum4<NS>(p, srcs, j));
       __syncthreads();
       int32_t* h = hist + r * DD_BINS;
       for (int i = threadIdx.x; i < DD_BINS; i += DIST_THREADS)
@@ -596,7 +615,42 @@ __global__ void __launch_bounds__(EMIT_THREADS) dist_emit_bits_kernel(DistParams
   } else {
     const K* keys = reinterpret_cast<const K*>(p.keys + r * p.keys_ld * sizeof(K));
     uint32_t gt, eq;
-    key_words(keys, nk, j0, (K)st.pmask, (K)st.prefix, gt, eq);
+    if constexpr (sizeof(K) == 4) {
+      // the CTA's 64 KB key chunk arrives by one bulk copy into shared memory
+      // (no registers held while in flight; ~3 CTAs' chunks per SM at once)
+      extern __shared__ __align__(16) uint8_t kbuf[];
+      __shared__ __align__(8) uint64_t kbar;
+      const int64_t c0 = (int64_t)blockIdx.x * EMIT_CHUNK;
+      const int64_t padded = ((int64_t)nk + 3) & ~int64_t(3);
+      const int cn = (int)min((int64_t)EMIT_CHUNK, max((int64_t)0, padded - c0));
+      if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&kbar)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      }
+      __syncthreads();
+      if (cn > 0) {
+        if (threadIdx.x == 0) {
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(&kbar)),
+                       "r"((uint32_t)cn * 4u) : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                  smem_u32(kbuf)),
+              "l"(reinterpret_cast<uint64_t>(keys + c0)), "r"((uint32_t)cn * 4u), "r"(smem_u32(&kbar))
+              : "memory");
+        }
+        uint32_t done = 0;
+        while (!done)
+          asm volatile(
+              "{\n .reg .pred q;\n mbarrier.try_wait.parity.shared::cta.b64 q, [%1], 0;\n selp.u32 %0, 1, 0, q;\n}\n"
+              : "=r"(done)
+              : "r"(smem_u32(&kbar))
+              : "memory");
+      }
+      key_words(reinterpret_cast<const uint32_t*>(kbuf), (int)(nk - c0), (int64_t)warp * 1024, (uint32_t)st.pmask,
+                (uint32_t)st.prefix, gt, eq);
+    } else {
+      key_words(keys, nk, j0, (K)st.pmask, (K)st.prefix, gt, eq);
+    }
     sel = gt;
     if (er.all_ties) {
       sel |= eq;
@@ -839,7 +893,9 @@ extern "C" int sts_dist_select_begin(const sts_dist_rows* g, int32_t* hist_local
   const dim3 g2 = dist_grid(p);
   STS_REQUIRE((int64_t)g2.x * g2.y < (int64_t(1) << 31), STS_ERR_CONTRACT, "rows x position chunks too large");
   const unsigned lin = (unsigned)((int64_t)g2.x * g2.y);  // rows x chunks, row-fastest
-  if (p.page_size == 1) dist_keys_kernel<uint32_t><<<lin, DIST_THREADS, 0, st>>>(p, hist_local_dev);
+  if (p.page_size == 1 && p.nsrc == 4 && p.vec4) dist_keys_kernel<uint32_t, 4><<<lin, DIST_THREADS, 0, st>>>(p, hist_local_dev);
+  else if (p.page_size == 1 && p.nsrc == 7 && p.vec4) dist_keys_kernel<uint32_t, 7><<<lin, DIST_THREADS, 0, st>>>(p, hist_local_dev);
+  else if (p.page_size == 1) dist_keys_kernel<uint32_t><<<lin, DIST_THREADS, 0, st>>>(p, hist_local_dev);
   else dist_keys_kernel<uint64_t><<<lin, DIST_THREADS, 0, st>>>(p, hist_local_dev);
   STS_LAUNCH_CHECK();
   return STS_OK;
@@ -904,7 +960,11 @@ extern "C" int sts_dist_select_finish(const sts_dist_rows* g, int32_t rank, int3
   if (p.page_size == 1) {
     dist_emit_ties_kernel<uint32_t><<<kgrid, EMIT_THREADS, 0, st>>>(p, e);
     STS_LAUNCH_CHECK();
-    dist_emit_bits_kernel<uint32_t><<<kgrid, EMIT_THREADS, 0, st>>>(p, e);
+    constexpr int kbytes = EMIT_CHUNK * 4;
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(dist_emit_bits_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, kbytes);
+    STS_CUDA_CHECK(attr);
+    dist_emit_bits_kernel<uint32_t><<<kgrid, EMIT_THREADS, kbytes, st>>>(p, e);
   } else {
     dist_emit_ties_kernel<uint64_t><<<kgrid, EMIT_THREADS, 0, st>>>(p, e);
     STS_LAUNCH_CHECK();
