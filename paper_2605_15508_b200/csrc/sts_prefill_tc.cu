@@ -15,11 +15,12 @@
 //            S_j = Q.K_j^T (M=128 rows, N=64 keys, K=d) into the group's
 //            TMEM S slot, issued as soon as the group has read S_{j-2};
 //            O_g += P_j.V_j (M=128, N=d, K=64; V as an MN-major operand)
-//   warps 3-10 softmax (two groups of 4), thread = query row: tcgen05.ld of its S row, causal
-//            mask on diagonal blocks, online max with lazy rescale (O rows in
-//            TMEM rescaled only when the max grows by > 2^8), P in bf16 to
-//            shared memory (swizzled K-major A operand), row sums in fp32;
-//            at the end O / l to global (bf16)
+//   warps 3-10 softmax (two groups of 4), thread = query row: tcgen05.ld of
+//            its S row, causal mask on diagonal blocks, online max with lazy
+//            rescale (O rows in TMEM rescaled only when the max grows by
+//            > 2^8), P in bf16 written back to TMEM (tcgen05.st: the A operand
+//            of PV comes from TMEM, no shared-memory round trip), row sums in
+//            fp32; at the end O / l to global (bf16)
 #include <cuda.h>
 
 #include "sts_decode.cuh"
@@ -29,7 +30,7 @@ namespace {
 
 constexpr int PF_ROWS = 128;   // query tile = MMA M = TMEM lanes
 constexpr int PF_BLK = 64;     // keys per block = MMA N of S, K of PV
-constexpr int PF_STAGES = 5;
+constexpr int PF_STAGES = 6;  // P lives in TMEM, so shared memory holds Q + 6 K/V stages
 constexpr int PF_THREADS = 352;  // TMA, two MMA issuers, two softmax warp groups (even / odd key blocks)
 constexpr float PF_RESCALE = 8.f;  // log2 growth of the row max that forces an O rescale
 
@@ -102,6 +103,25 @@ __device__ __forceinline__ void pf_st32(uint32_t taddr, const float* v) {
       "r"(__float_as_uint(v[29])), "r"(__float_as_uint(v[30])), "r"(__float_as_uint(v[31]))
       : "memory");
 }
+// D += A.B with A (M x 16, bf16 pairs per 32-bit column) in TMEM, B from shared memory
+__device__ __forceinline__ void pf_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                          uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(
+          d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void pf_st32u(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
 __device__ __forceinline__ void pf_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
 __device__ __forceinline__ void pf_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
 
@@ -139,19 +159,20 @@ struct PfLayout {
   static constexpr int SLABS = D / 64;
   static constexpr int Q_BYTES = PF_ROWS * 128 * SLABS;
   static constexpr int KB_BYTES = PF_BLK * 128 * SLABS;     // one K block (= one V block)
-  static constexpr int P_BYTES = PF_ROWS * PF_BLK * 2;       // bf16 P tile, 128B rows
   static constexpr int OFF_Q = 0;
   static constexpr int OFF_K = OFF_Q + Q_BYTES;
   static constexpr int OFF_V = OFF_K + PF_STAGES * KB_BYTES;
-  static constexpr int OFF_P = OFF_V + PF_STAGES * KB_BYTES;
-  static constexpr int OFF_X = OFF_P + 2 * P_BYTES;          // [128 rows] (m, l) of the odd group
+  static constexpr int OFF_X = OFF_V + PF_STAGES * KB_BYTES;  // [128 rows] (m, l) of the odd group
   static constexpr int OFF_BAR = OFF_X + PF_ROWS * 8;
   // full[S], empty[S], sfull[2], sempty[2], pfull[2], odone[2], qfull
   static constexpr int NBAR = 2 * PF_STAGES + 9;
   static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
   static constexpr int S_COLS = PF_BLK;                       // per S slot
   static constexpr int O_COL = 2 * PF_BLK;                    // O_even, O_odd after the two S slots
-  static constexpr int TMEM_COLS = 2 * PF_BLK + 2 * D <= 256 ? 256 : 512;
+  static constexpr int P_COL = O_COL + 2 * D;                  // P_even, P_odd: bf16 pairs, PF_BLK / 2 columns each
+  static constexpr int TMEM_COLS = P_COL + PF_BLK <= 256 ? 256 : 512;
+  static_assert(P_COL + PF_BLK <= 512, "TMEM columns");
+  static_assert(SMEM <= 227 * 1024, "prefill shared memory exceeds the 227 KB per-CTA limit");
 };
 
 // the tile's block list: committed blocks from the selection, then the diagonal
@@ -281,14 +302,14 @@ __global__ void __launch_bounds__(PF_THREADS, 1) prefill_tc_kernel(const __grid_
         const int stage = j % PF_STAGES;
         pf_wait(&pfull[g], (j >> 1) & 1);
         pf_fence_after();
-        const uint64_t ad = pf_desc_k(smem + L::OFF_P + g * L::P_BYTES);
+        const uint32_t a_tmem = tmem + L::P_COL + g * (PF_BLK / 2);  // P_j as the A operand, from TMEM
         // V block [64 keys][D] as an MN-major B operand: MN atoms (64 d) are
         // the slabs (LBO), K groups of 8 keys are 1024 B apart (SBO)
         const uint64_t bd = pf_desc_mn(smem + L::OFF_V + stage * L::KB_BYTES, PF_BLK * 128, 1024);
 #pragma unroll
         for (int k = 0; k < PF_BLK / 16; ++k)
-          pf_mma(tmem + L::O_COL + g * D, ad + 2 * k, bd + (uint64_t)((16 * 128) >> 4) * k, id_o,
-                 (j >= 2 || k != 0) ? 1u : 0u);
+          pf_mma_ts(tmem + L::O_COL + g * D, a_tmem + 8 * k, bd + (uint64_t)((16 * 128) >> 4) * k, id_o,
+                    (j >= 2 || k != 0) ? 1u : 0u);
         pf_commit(&empty[stage]);  // K and V of this block no longer read
         pf_commit(&odone[g]);      // O_g holds the group's blocks up to j (frees P buffer g)
       }
@@ -373,14 +394,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1) prefill_tc_kernel(const __grid_
         }
       }
       m = m_new;
-      // K-major 128B-swizzled rows of the A operand
-      uint8_t* prow = smem + L::OFF_P + slot * L::P_BYTES + r * 128;
-#pragma unroll
-      for (int c8 = 0; c8 < PF_BLK / 8; ++c8)
-        *reinterpret_cast<uint4*>(prow + ((c8 ^ (r & 7)) * 16)) =
-            make_uint4(w[4 * c8], w[4 * c8 + 1], w[4 * c8 + 2], w[4 * c8 + 3]);
+      // the row's P into its TMEM lane (consecutive key pairs per column): the
+      // A operand of PV_j, no shared-memory round trip
+      pf_st32u(tmem + lane_off + L::P_COL + slot * (PF_BLK / 2), w);
+      pf_wait_st();
       l += rs;
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // P visible to the tensor core
       pf_fence_before();
       pf_arrive(&pfull[slot]);
     }
