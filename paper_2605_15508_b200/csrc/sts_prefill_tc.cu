@@ -8,7 +8,9 @@
 //   tile's two diagonal blocks under the causal mask.  Row t of tile T sees
 //   the selected committed keys and the diagonal keys <= t.
 //
-// CTA = (q-head, query tile), 128 rows = the 128 TMEM lanes.  Warp roles:
+// Persistent CTAs (one per SM) walk the work items (q-head, query tile) in
+// snake order, heavy tiles first; a tile's 128 rows = the 128 TMEM lanes.
+// Warp roles:
 //   warp 0   TMA producer: Q tile once, then K and V blocks of the list
 //            (128B swizzle; ring of STAGES (K, V) blocks)
 //   warps 1-2 MMA issuers, one per softmax group (even / odd key blocks):
@@ -30,7 +32,7 @@ namespace {
 
 constexpr int PF_ROWS = 128;   // query tile = MMA M = TMEM lanes
 constexpr int PF_BLK = 64;     // keys per block = MMA N of S, K of PV
-constexpr int PF_STAGES = 6;  // P lives in TMEM, so shared memory holds Q + 6 K/V stages
+constexpr int PF_STAGES = 5;  // P lives in TMEM: shared memory holds two Q tiles + 5 K/V stages
 constexpr int PF_THREADS = 352;  // TMA, two MMA issuers, two softmax warp groups (even / odd key blocks)
 constexpr float PF_RESCALE = 8.f;  // log2 growth of the row max that forces an O rescale
 
@@ -159,13 +161,13 @@ struct PfLayout {
   static constexpr int SLABS = D / 64;
   static constexpr int Q_BYTES = PF_ROWS * 128 * SLABS;
   static constexpr int KB_BYTES = PF_BLK * 128 * SLABS;     // one K block (= one V block)
-  static constexpr int OFF_Q = 0;
-  static constexpr int OFF_K = OFF_Q + Q_BYTES;
+  static constexpr int OFF_Q = 0;                            // two Q tiles (consecutive work items)
+  static constexpr int OFF_K = OFF_Q + 2 * Q_BYTES;
   static constexpr int OFF_V = OFF_K + PF_STAGES * KB_BYTES;
   static constexpr int OFF_X = OFF_V + PF_STAGES * KB_BYTES;  // [128 rows] (m, l) of the odd group
   static constexpr int OFF_BAR = OFF_X + PF_ROWS * 8;
-  // full[S], empty[S], sfull[2], sempty[2], pfull[2], odone[2], qfull
-  static constexpr int NBAR = 2 * PF_STAGES + 9;
+  // full[S], empty[S], sfull[2], sempty[2], pfull[2], odone[2], qfull[2], qempty[2], oempty
+  static constexpr int NBAR = 2 * PF_STAGES + 13;
   static constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
   static constexpr int S_COLS = PF_BLK;                       // per S slot
   static constexpr int O_COL = 2 * PF_BLK;                    // O_even, O_odd after the two S slots
@@ -193,6 +195,33 @@ __device__ __forceinline__ int pf_block(const PfParams& p, int kvh, int T, int n
   return p.idx[((int64_t)kvh * p.tiles + T) * p.idx_ld + (int64_t)j * PF_BLK] / PF_BLK;
 }
 
+// the n-th work item of this CTA: rounds of gridDim.x items in snake order
+// (CTA b takes item b of even rounds, item G-1-b of odd rounds), so with
+// heavy tiles first every CTA gets an even share of the work
+__device__ __forceinline__ int pf_item_index(int n, int n_items) {
+  const int G = gridDim.x, b = blockIdx.x;
+  const int i = n * G + ((n & 1) ? G - 1 - b : b);
+  return i < n_items ? i : n_items;
+}
+
+// work item i of the persistent grid: heavy (late) tiles first, heads inner
+struct PfItem {
+  int T, hq, kvh, ncommit, nb;
+};
+__device__ __forceinline__ PfItem pf_item(const PfParams& p, int i) {
+  PfItem it;
+  it.T = p.tiles - 1 - i / p.heads_q;
+  it.hq = i % p.heads_q;
+  it.kvh = it.hq / p.group;
+  it.nb = pf_nblocks(p, it.kvh, it.T, it.ncommit);
+  return it;
+}
+
+// Persistent: one CTA per SM walks the work items (tile, q-head) i = blockIdx.x,
+// blockIdx.x + gridDim.x, ... (heavy tiles first).  Every barrier phase is
+// counted across items, the K/V ring and the S slots flow from one item into
+// the next, and the Q tile is double-buffered, so an item's loads and first
+// scores overlap the previous item's last blocks and epilogue.
 template <int D>
 __global__ void __launch_bounds__(PF_THREADS, 1) prefill_tc_kernel(const __grid_constant__ CUtensorMap qmap,
                                                                    const __grid_constant__ CUtensorMap kmap,
@@ -207,17 +236,14 @@ __global__ void __launch_bounds__(PF_THREADS, 1) prefill_tc_kernel(const __grid_
   uint64_t* sfull = bars + 2 * PF_STAGES;
   uint64_t* sempty = sfull + 2;
   uint64_t* pfull = sempty + 2;
-  uint64_t* odone = pfull + 2;  // odone[j & 1]: PV_j landed in O (per buffer: waits stay one phase behind)
-  uint64_t* qfull = odone + 2;
+  uint64_t* odone = pfull + 2;   // odone[g]: group g's latest PV landed in O_g
+  uint64_t* qfull = odone + 2;   // qfull[b] / qempty[b]: Q buffer b loaded / no longer read
+  uint64_t* qempty = qfull + 2;
+  uint64_t* oempty = qempty + 2;  // the item's epilogue has read O_0 and O_1
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + L::NBAR);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // heavy (late) tiles first: tile index descending across the grid
-  const int T = p.tiles - 1 - (int)blockIdx.x;
-  const int hq = blockIdx.y;
-  const int kvh = hq / p.group;
-  int ncommit;
-  const int nb = pf_nblocks(p, kvh, T, ncommit);
+  const int n_items = p.tiles * p.heads_q;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < PF_STAGES; ++i) {
@@ -228,10 +254,11 @@ __global__ void __launch_bounds__(PF_THREADS, 1) prefill_tc_kernel(const __grid_
       pf_mbar_init(&sfull[i], 1);
       pf_mbar_init(&sempty[i], 128);
       pf_mbar_init(&pfull[i], 128);
+      pf_mbar_init(&odone[i], 1);
+      pf_mbar_init(&qfull[i], 1);
+      pf_mbar_init(&qempty[i], 2);  // both MMA issuers
     }
-    pf_mbar_init(&odone[0], 1);
-    pf_mbar_init(&odone[1], 1);
-    pf_mbar_init(qfull, 1);
+    pf_mbar_init(oempty, 128);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 1) {
@@ -246,26 +273,29 @@ __global__ void __launch_bounds__(PF_THREADS, 1) prefill_tc_kernel(const __grid_
 
   if (warp == 0) {
     if (lane == 0) {
-      pf_expect_tx(qfull, L::Q_BYTES);
+      uint32_t kv = 0;  // blocks loaded so far (ring position)
+      int n_it = 0;
+      for (int i = pf_item_index(0, n_items); i < n_items; i = pf_item_index(n_it + 1, n_items), ++n_it) {
+        const PfItem it = pf_item(p, i);
+        const int qb = n_it & 1;
+        if (n_it >= 2) pf_wait(&qempty[qb], ((n_it >> 1) - 1) & 1);  // item n_it - 2 done with this Q buffer
+        pf_expect_tx(&qfull[qb], L::Q_BYTES);
 #pragma unroll
-      for (int s = 0; s < L::SLABS; ++s)
-        pf_tma3(smem + L::OFF_Q + s * PF_ROWS * 128, &qmap, qfull, s * 64, T * PF_ROWS, hq);
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int j = 0; j < nb; ++j) {
-        const int b = pf_block(p, kvh, T, ncommit, j);
-        pf_wait(&empty[stage], phase ^ 1);
-        pf_expect_tx(&full[stage], 2 * L::KB_BYTES);
+        for (int s = 0; s < L::SLABS; ++s)
+          pf_tma3(smem + L::OFF_Q + qb * L::Q_BYTES + s * PF_ROWS * 128, &qmap, &qfull[qb], s * 64,
+                  it.T * PF_ROWS, it.hq);
+        for (int j = 0; j < it.nb; ++j, ++kv) {
+          const int b = pf_block(p, it.kvh, it.T, it.ncommit, j);
+          const int stage = kv % PF_STAGES;
+          pf_wait(&empty[stage], ((kv / PF_STAGES) & 1) ^ 1);
+          pf_expect_tx(&full[stage], 2 * L::KB_BYTES);
 #pragma unroll
-        for (int s = 0; s < L::SLABS; ++s) {
-          pf_tma3(smem + L::OFF_K + stage * L::KB_BYTES + s * PF_BLK * 128, &kmap, &full[stage], s * 64, b * PF_BLK,
-                  kvh);
-          pf_tma3(smem + L::OFF_V + stage * L::KB_BYTES + s * PF_BLK * 128, &vmap, &full[stage], s * 64, b * PF_BLK,
-                  kvh);
-        }
-        if (++stage == PF_STAGES) {
-          stage = 0;
-          phase ^= 1;
+          for (int s = 0; s < L::SLABS; ++s) {
+            pf_tma3(smem + L::OFF_K + stage * L::KB_BYTES + s * PF_BLK * 128, &kmap, &full[stage], s * 64,
+                    b * PF_BLK, it.kvh);
+            pf_tma3(smem + L::OFF_V + stage * L::KB_BYTES + s * PF_BLK * 128, &vmap, &full[stage], s * 64,
+                    b * PF_BLK, it.kvh);
+          }
         }
       }
     }
@@ -276,175 +306,202 @@ __global__ void __launch_bounds__(PF_THREADS, 1) prefill_tc_kernel(const __grid_
       const int g = warp - 1;
       constexpr uint32_t id_s = pf_idesc(PF_ROWS, PF_BLK, false);
       constexpr uint32_t id_o = pf_idesc(PF_ROWS, D, true);
-      pf_wait(qfull, 0);
-      pf_fence_after();
-      auto issue_s = [&](int j) {  // S_j into TMEM slot j & 1 (= g)
-        const int stage = j % PF_STAGES;
-        const uint32_t slot = j & 1;
-        pf_wait(&sempty[slot], ((j >> 1) & 1) ^ 1);  // the group has read S_{j-2}
-        pf_wait(&full[stage], (j / PF_STAGES) & 1);
+      uint32_t sc = 0, pc = 0;  // S / PV issued by this issuer (slot g uses)
+      uint32_t kv0 = 0;         // ring position of the item's block 0
+      int n_it = 0;
+      for (int i = pf_item_index(0, n_items); i < n_items; i = pf_item_index(n_it + 1, n_items), ++n_it) {
+        const PfItem it = pf_item(p, i);
+        const int nb = it.nb;
+        const int qb = n_it & 1;
+        pf_wait(&qfull[qb], (n_it >> 1) & 1);
         pf_fence_after();
-        const uint32_t d_tmem = tmem + slot * L::S_COLS;
+        auto issue_s = [&](int j) {  // S_j into TMEM slot g
+          const uint32_t kv = kv0 + j;
+          const int stage = kv % PF_STAGES;
+          pf_wait(&sempty[g], (sc & 1) ^ 1);  // the group has read its previous S
+          pf_wait(&full[stage], (kv / PF_STAGES) & 1);
+          pf_fence_after();
+          const uint32_t d_tmem = tmem + g * L::S_COLS;
 #pragma unroll
-        for (int s = 0; s < L::SLABS; ++s) {
-          const uint64_t ad = pf_desc_k(smem + L::OFF_Q + s * PF_ROWS * 128);
-          const uint64_t bd = pf_desc_k(smem + L::OFF_K + stage * L::KB_BYTES + s * PF_BLK * 128);
+          for (int s = 0; s < L::SLABS; ++s) {
+            const uint64_t ad = pf_desc_k(smem + L::OFF_Q + qb * L::Q_BYTES + s * PF_ROWS * 128);
+            const uint64_t bd = pf_desc_k(smem + L::OFF_K + stage * L::KB_BYTES + s * PF_BLK * 128);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) pf_mma(d_tmem, ad + 2 * k, bd + 2 * k, id_s, (s | k) != 0);
+            for (int k = 0; k < 4; ++k) pf_mma(d_tmem, ad + 2 * k, bd + 2 * k, id_s, (s | k) != 0);
+          }
+          pf_commit(&sfull[g]);
+          ++sc;
+        };
+        // S_{j+2} reuses S_j's slot: issued as soon as the group has read S_j
+        // (early in softmax j), so its next scores are ready when it finishes
+        if (g < nb) issue_s(g);
+        for (int j = g; j < nb; j += 2) {
+          if (j + 2 < nb) issue_s(j + 2);
+          const uint32_t kv = kv0 + j;
+          const int stage = kv % PF_STAGES;
+          pf_wait(&pfull[g], pc & 1);
+          if (j < 2 && n_it > 0) pf_wait(oempty, (n_it - 1) & 1);  // O_g drained by the last epilogue
+          pf_fence_after();
+          const uint32_t a_tmem = tmem + L::P_COL + g * (PF_BLK / 2);  // P_j as the A operand, from TMEM
+          // V block [64 keys][D] as an MN-major B operand: MN atoms (64 d) are
+          // the slabs (LBO), K groups of 8 keys are 1024 B apart (SBO)
+          const uint64_t bd = pf_desc_mn(smem + L::OFF_V + stage * L::KB_BYTES, PF_BLK * 128, 1024);
+#pragma unroll
+          for (int k = 0; k < PF_BLK / 16; ++k)
+            pf_mma_ts(tmem + L::O_COL + g * D, a_tmem + 8 * k, bd + (uint64_t)((16 * 128) >> 4) * k, id_o,
+                      (j >= 2 || k != 0) ? 1u : 0u);
+          pf_commit(&empty[stage]);  // K and V of this block no longer read
+          pf_commit(&odone[g]);      // O_g holds the group's blocks up to j (frees P buffer g)
+          ++pc;
         }
-        pf_commit(&sfull[slot]);
-      };
-      // S_{j+2} reuses S_j's slot: issued as soon as the group has read S_j
-      // (early in softmax j), so its next scores are ready when it finishes
-      if (g < nb) issue_s(g);
-      for (int j = g; j < nb; j += 2) {
-        if (j + 2 < nb) issue_s(j + 2);
-        const int stage = j % PF_STAGES;
-        pf_wait(&pfull[g], (j >> 1) & 1);
-        pf_fence_after();
-        const uint32_t a_tmem = tmem + L::P_COL + g * (PF_BLK / 2);  // P_j as the A operand, from TMEM
-        // V block [64 keys][D] as an MN-major B operand: MN atoms (64 d) are
-        // the slabs (LBO), K groups of 8 keys are 1024 B apart (SBO)
-        const uint64_t bd = pf_desc_mn(smem + L::OFF_V + stage * L::KB_BYTES, PF_BLK * 128, 1024);
-#pragma unroll
-        for (int k = 0; k < PF_BLK / 16; ++k)
-          pf_mma_ts(tmem + L::O_COL + g * D, a_tmem + 8 * k, bd + (uint64_t)((16 * 128) >> 4) * k, id_o,
-                    (j >= 2 || k != 0) ? 1u : 0u);
-        pf_commit(&empty[stage]);  // K and V of this block no longer read
-        pf_commit(&odone[g]);      // O_g holds the group's blocks up to j (frees P buffer g)
+        pf_commit(&qempty[qb]);  // this issuer's reads of Q buffer qb are done
+        kv0 += nb;
       }
     }
   } else {
     // ===== softmax: thread = query row; group g takes the blocks j = g mod 2 =====
     const int quad = warp & 3;
     const int grp = (warp - 3) >> 2;
-    const int r = quad * 32 + lane;       // row within the tile (TMEM lane)
-    const int row = T * PF_ROWS + r;      // query position
+    const int r = quad * 32 + lane;  // row within the tile (TMEM lane)
     const uint32_t lane_off = (uint32_t)(quad * 32) << 16;
     const uint32_t o_col = L::O_COL + grp * D;
     const float sl2 = p.scale * LOG2E;
-    float m = -INFINITY, l = 0.f;
-    for (int j = grp; j < nb; j += 2) {
-      const uint32_t slot = grp;  // S_j sits in slot j & 1
-      const int b = pf_block(p, kvh, T, ncommit, j);
-      pf_wait(&sfull[slot], (j >> 1) & 1);
-      pf_fence_after();
-      float s[PF_BLK];
-      pf_ld32(tmem + lane_off + slot * L::S_COLS, s);
-      pf_ld32(tmem + lane_off + slot * L::S_COLS + 32, s + 32);
-      pf_wait_ld();
-      pf_fence_before();
-      pf_arrive(&sempty[slot]);
-      // row max of the raw scores (the scale is folded into the exponent's FFMA)
-      float mx = -INFINITY;
-      if (j >= ncommit) {  // diagonal block: causal mask (and the ragged end of the prompt)
-#pragma unroll
-        for (int c = 0; c < PF_BLK; ++c) {
-          const int key = b * PF_BLK + c;
-          s[c] = (key <= row && key < p.n) ? s[c] : -INFINITY;
-          mx = fmaxf(mx, s[c]);
-        }
-      } else {
-#pragma unroll
-        for (int c = 0; c < PF_BLK; ++c) mx = fmaxf(mx, s[c]);
-      }
-      mx *= sl2;
-      // lazy rescale, warp-uniform (tcgen05.ld/st are warp-collective): rows
-      // whose max grew by > 2^8 rescale their O row
-      const bool need = mx > m + PF_RESCALE;
-      const bool any = __any_sync(0xffffffffu, need);
-      float m_new = m, f = 1.f;
-      if (any) {
-        if (j < 2) {
-          m_new = mx;  // the group's first block: its PV overwrites O_grp
-        } else if (need) {
-          f = fast_exp2(m - mx);
-          m_new = mx;
-        }
-      }
-      const float mb = m_new == -INFINITY ? 0.f : m_new;  // a row with no key yet: P = 0, not NaN
-      // P = 2^(s - m) in bf16 (before waiting for the group's previous PV)
-      uint32_t w[PF_BLK / 2];
-      float rs = 0.f;
-#pragma unroll
-      for (int e = 0; e < PF_BLK / 2; ++e) {
-        const float a0 = fast_exp2(fmaf(s[2 * e], sl2, -mb)), a1 = fast_exp2(fmaf(s[2 * e + 1], sl2, -mb));
-        rs += a0 + a1;
-        const __nv_bfloat162 h = __floats2bfloat162_rn(a0, a1);
-        w[e] = *reinterpret_cast<const uint32_t*>(&h);
-      }
-      // this group's previous PV (j - 2) read P buffer j&1 and wrote O_grp
-      if (j >= 2) pf_wait(&odone[slot], ((j - 2) >> 1) & 1);
-      if (any) {
-        if (j < 2) {
-          l = 0.f;
-        } else {
-          pf_fence_after();
-#pragma unroll
-          for (int c0 = 0; c0 < D; c0 += 32) {
-            float o[32];
-            pf_ld32(tmem + lane_off + o_col + c0, o);
-            pf_wait_ld();
-#pragma unroll
-            for (int c = 0; c < 32; ++c) o[c] *= f;
-            pf_st32(tmem + lane_off + o_col + c0, o);
-          }
-          pf_wait_st();
-          l *= f;
-        }
-      }
-      m = m_new;
-      // the row's P into its TMEM lane (consecutive key pairs per column): the
-      // A operand of PV_j, no shared-memory round trip
-      pf_st32u(tmem + lane_off + L::P_COL + slot * (PF_BLK / 2), w);
-      pf_wait_st();
-      l += rs;
-      pf_fence_before();
-      pf_arrive(&pfull[slot]);
-    }
-    // epilogue: the odd group hands its (m, l) to the even group, which merges
-    // O_even and O_odd (both in its TMEM lanes) and writes O / l
     float2* xch = reinterpret_cast<float2*>(smem + L::OFF_X);
-    if (grp == 1) xch[r] = make_float2(m, l);
-    asm volatile("bar.sync 1, 256;\n" ::: "memory");
-    if (grp == 0) {
-      const int last0 = ((nb - 1) & 1) == 0 ? nb - 1 : nb - 2;  // last even / odd block
-      const int last1 = ((nb - 1) & 1) == 1 ? nb - 1 : nb - 2;
-      if (last0 >= 0) pf_wait(&odone[0], (last0 >> 1) & 1);
-      if (last1 >= 1) pf_wait(&odone[1], (last1 >> 1) & 1);
-      pf_fence_after();
-      const float2 x1 = xch[r];
-      const bool has1 = last1 >= 1;
-      const float m1 = has1 ? x1.x : -INFINITY, l1 = has1 ? x1.y : 0.f;
-      const float mm = fmaxf(m, m1);
-      const float a0 = (m == -INFINITY) ? 0.f : fast_exp2(m - mm);
-      const float a1 = (m1 == -INFINITY) ? 0.f : fast_exp2(m1 - mm);
-      const float L = l * a0 + l1 * a1;
-      const float inv = L > 0.f ? 1.f / L : 0.f;
-      const float w0 = a0 * inv, w1 = a1 * inv;
-      __nv_bfloat16* orow = p.out + ((int64_t)hq * p.n + row) * D;
-#pragma unroll
-      for (int c0 = 0; c0 < D; c0 += 32) {
-        float o[32], o1[32];
-        pf_ld32(tmem + lane_off + L::O_COL + c0, o);  // warp-collective: every row loads
-        pf_ld32(tmem + lane_off + L::O_COL + D + c0, o1);
+    uint32_t u0 = 0, u1 = 0;  // blocks processed so far by group 0 / group 1 (barrier phases)
+    int n_it = 0;
+    for (int i = pf_item_index(0, n_items); i < n_items; i = pf_item_index(n_it + 1, n_items), ++n_it) {
+      const PfItem it = pf_item(p, i);
+      const int nb = it.nb;
+      const int row = it.T * PF_ROWS + r;  // query position
+      uint32_t& u = grp ? u1 : u0;
+      float m = -INFINITY, l = 0.f;
+      for (int j = grp; j < nb; j += 2, ++u) {
+        const int b = pf_block(p, it.kvh, it.T, it.ncommit, j);
+        pf_wait(&sfull[grp], u & 1);
+        pf_fence_after();
+        float s[PF_BLK];
+        pf_ld32(tmem + lane_off + grp * L::S_COLS, s);
+        pf_ld32(tmem + lane_off + grp * L::S_COLS + 32, s + 32);
         pf_wait_ld();
-        if (row < p.n) {
+        pf_fence_before();
+        pf_arrive(&sempty[grp]);
+        // row max of the raw scores (the scale is folded into the exponent's FFMA)
+        float mx = -INFINITY;
+        if (j >= it.ncommit) {  // diagonal block: causal mask (and the ragged end of the prompt)
 #pragma unroll
-          for (int c = 0; c < 32; c += 8) {
-            uint4 w;
-            w.x = pack_bf16(o[c] * w0 + (has1 ? o1[c] * w1 : 0.f), o[c + 1] * w0 + (has1 ? o1[c + 1] * w1 : 0.f));
-            w.y = pack_bf16(o[c + 2] * w0 + (has1 ? o1[c + 2] * w1 : 0.f),
-                            o[c + 3] * w0 + (has1 ? o1[c + 3] * w1 : 0.f));
-            w.z = pack_bf16(o[c + 4] * w0 + (has1 ? o1[c + 4] * w1 : 0.f),
-                            o[c + 5] * w0 + (has1 ? o1[c + 5] * w1 : 0.f));
-            w.w = pack_bf16(o[c + 6] * w0 + (has1 ? o1[c + 6] * w1 : 0.f),
-                            o[c + 7] * w0 + (has1 ? o1[c + 7] * w1 : 0.f));
-            *reinterpret_cast<uint4*>(orow + c0 + c) = w;
+          for (int c = 0; c < PF_BLK; ++c) {
+            const int key = b * PF_BLK + c;
+            s[c] = (key <= row && key < p.n) ? s[c] : -INFINITY;
+            mx = fmaxf(mx, s[c]);
+          }
+        } else {
+#pragma unroll
+          for (int c = 0; c < PF_BLK; ++c) mx = fmaxf(mx, s[c]);
+        }
+        mx *= sl2;
+        // lazy rescale, warp-uniform (tcgen05.ld/st are warp-collective): rows
+        // whose max grew by > 2^8 rescale their O row
+        const bool need = mx > m + PF_RESCALE;
+        const bool any = __any_sync(0xffffffffu, need);
+        float m_new = m, f = 1.f;
+        if (any) {
+          if (j < 2) {
+            m_new = mx;  // the group's first block of the item: its PV overwrites O_grp
+          } else if (need) {
+            f = fast_exp2(m - mx);
+            m_new = mx;
           }
         }
+        const float mb = m_new == -INFINITY ? 0.f : m_new;  // a row with no key yet: P = 0, not NaN
+        // P = 2^(s - m) in bf16 (before waiting for the group's previous PV)
+        uint32_t w[PF_BLK / 2];
+        float rs = 0.f;
+#pragma unroll
+        for (int e = 0; e < PF_BLK / 2; ++e) {
+          const float a0 = fast_exp2(fmaf(s[2 * e], sl2, -mb)), a1 = fast_exp2(fmaf(s[2 * e + 1], sl2, -mb));
+          rs += a0 + a1;
+          const __nv_bfloat162 h = __floats2bfloat162_rn(a0, a1);
+          w[e] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+        // the group's previous PV (maybe the last item's) read P buffer grp and wrote O_grp
+        if (u > 0) pf_wait(&odone[grp], (u - 1) & 1);
+        if (any) {
+          if (j < 2) {
+            l = 0.f;
+          } else {
+            pf_fence_after();
+#pragma unroll
+            for (int c0 = 0; c0 < D; c0 += 32) {
+              float o[32];
+              pf_ld32(tmem + lane_off + o_col + c0, o);
+              pf_wait_ld();
+#pragma unroll
+              for (int c = 0; c < 32; ++c) o[c] *= f;
+              pf_st32(tmem + lane_off + o_col + c0, o);
+            }
+            pf_wait_st();
+            l *= f;
+          }
+        }
+        m = m_new;
+        // the row's P into its TMEM lane: the A operand of PV_j
+        pf_st32u(tmem + lane_off + L::P_COL + grp * (PF_BLK / 2), w);
+        pf_wait_st();
+        l += rs;
+        pf_fence_before();
+        pf_arrive(&pfull[grp]);
       }
-      if (row < p.n && !(L > 0.f)) set_status(p.status, STS_DEV_EMPTY_ROW);
+      // both groups track both counts: the other group's blocks of this item
+      if (grp == 1) u0 += (nb + 1) / 2;
+      else u1 += nb / 2;
+      // epilogue: the odd group hands its (m, l) to the even group, which
+      // merges O_even and O_odd (both in its TMEM lanes) and writes O / l
+      if (grp == 1) {
+        if (n_it > 0) asm volatile("bar.sync 2, 256;\n" ::: "memory");  // group 0 has read the last (m, l)
+        xch[r] = make_float2(m, l);
+      }
+      asm volatile("bar.sync 1, 256;\n" ::: "memory");
+      if (grp == 0) {
+        const bool has1 = nb >= 2;
+        // the last PVs of both groups in this item (group 0: u0 - 1, group 1: u1 - 1)
+        pf_wait(&odone[0], (u0 - 1) & 1);
+        if (has1) pf_wait(&odone[1], (u1 - 1) & 1);
+        pf_fence_after();
+        const float2 x1 = xch[r];
+        if (pf_item_index(n_it + 1, n_items) < n_items) asm volatile("bar.arrive 2, 256;\n" ::: "memory");
+        const float m1 = has1 ? x1.x : -INFINITY, l1 = has1 ? x1.y : 0.f;
+        const float mm = fmaxf(m, m1);
+        const float a0 = (m == -INFINITY) ? 0.f : fast_exp2(m - mm);
+        const float a1 = (m1 == -INFINITY) ? 0.f : fast_exp2(m1 - mm);
+        const float Lsum = l * a0 + l1 * a1;
+        const float inv = Lsum > 0.f ? 1.f / Lsum : 0.f;
+        const float w0 = a0 * inv, w1 = a1 * inv;
+        __nv_bfloat16* orow = p.out + ((int64_t)it.hq * p.n + row) * D;
+#pragma unroll
+        for (int c0 = 0; c0 < D; c0 += 32) {
+          float o[32], o1[32];
+          pf_ld32(tmem + lane_off + L::O_COL + c0, o);  // warp-collective: every row loads
+          pf_ld32(tmem + lane_off + L::O_COL + D + c0, o1);
+          pf_wait_ld();
+          if (row < p.n) {
+#pragma unroll
+            for (int c = 0; c < 32; c += 8) {
+              uint4 wv;
+              wv.x = pack_bf16(o[c] * w0 + (has1 ? o1[c] * w1 : 0.f), o[c + 1] * w0 + (has1 ? o1[c + 1] * w1 : 0.f));
+              wv.y = pack_bf16(o[c + 2] * w0 + (has1 ? o1[c + 2] * w1 : 0.f),
+                               o[c + 3] * w0 + (has1 ? o1[c + 3] * w1 : 0.f));
+              wv.z = pack_bf16(o[c + 4] * w0 + (has1 ? o1[c + 4] * w1 : 0.f),
+                               o[c + 5] * w0 + (has1 ? o1[c + 5] * w1 : 0.f));
+              wv.w = pack_bf16(o[c + 6] * w0 + (has1 ? o1[c + 6] * w1 : 0.f),
+                               o[c + 7] * w0 + (has1 ? o1[c + 7] * w1 : 0.f));
+              *reinterpret_cast<uint4*>(orow + c0 + c) = wv;
+            }
+          }
+        }
+        if (row < p.n && !(Lsum > 0.f)) set_status(p.status, STS_DEV_EMPTY_ROW);
+        pf_fence_before();
+        pf_arrive(oempty);  // the next item's first PVs may overwrite O_0 / O_1
+      }
     }
   }
   pf_fence_before();
@@ -517,7 +574,9 @@ extern "C" int sts_prefill_blocksparse(const void* q_dev, const void* k_dev, con
   if (rc == STS_OK) rc = pf_map(&vm, v_dev, heads_kv, n, d, kv_head_stride, row_stride, PF_BLK);
   if (rc != STS_OK) return rc;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  dim3 grid((unsigned)p.tiles, (unsigned)heads_q);
+  const int64_t items = (int64_t)p.tiles * heads_q;
+  STS_REQUIRE(items <= 0x7fffffffLL, STS_ERR_CONTRACT, "too many prefill tiles");
+  const unsigned grid = (unsigned)(items < num_sms() ? items : num_sms());  // persistent: one CTA per SM
   if (d == 128) {
     STS_CUDA_CHECK(cudaFuncSetAttribute(prefill_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         PfLayout<128>::SMEM));
