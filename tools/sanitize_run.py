@@ -80,15 +80,17 @@ if "union" in which:
     cnt = torch.full((8,), 60, dtype=torch.int32, device=dev)
     kernels.row_union(idx, cnt, torch.arange(8, dtype=torch.int32, device=dev).reshape(2, 4), M=4, n_max=500)
 if "prefill_tc" in which:
-    n, hq, hkv, d = 300, 2, 1, 128
-    q = torch.randn((hq, n, d), generator=g, device=dev).bfloat16()
-    kk = torch.randn((hkv, n, d), generator=g, device=dev).bfloat16()
-    vv = torch.randn((hkv, n, d), generator=g, device=dev).bfloat16()
-    tiles = -(-n // 128)
-    sc = torch.rand((hkv * tiles, -(-n // 4) * 4), generator=g, device=dev)
-    idx, cnt = kernels.prefill_tile_select(sc, budget=0.3, n=n)
-    kernels.prefill_blocksparse(q, kk, vv, idx=idx, cnt=cnt)
-    kernels.prefill_blocksparse(q, kk, vv)
+    # 300 tokens: one item per CTA; 2600 tokens x 8 heads = 168 items > the SMs,
+    # so persistent CTAs also run items back to back
+    for n, hq, hkv, d in ((300, 2, 1, 128), (2600, 8, 2, 128)):
+        q = torch.randn((hq, n, d), generator=g, device=dev).bfloat16()
+        kk = torch.randn((hkv, n, d), generator=g, device=dev).bfloat16()
+        vv = torch.randn((hkv, n, d), generator=g, device=dev).bfloat16()
+        tiles = -(-n // 128)
+        sc = torch.rand((hkv * tiles, -(-n // 4) * 4), generator=g, device=dev)
+        idx, cnt = kernels.prefill_tile_select(sc, budget=0.3, n=n)
+        kernels.prefill_blocksparse(q, kk, vv, idx=idx, cnt=cnt)
+        kernels.prefill_blocksparse(q, kk, vv)
 if "offload" in which:
     from paper_2605_15508_b200.offload import PagedKVOffload
 
