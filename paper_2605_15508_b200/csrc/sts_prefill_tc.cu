@@ -395,8 +395,12 @@ __global__ void __launch_bounds__(PF_THREADS, 1) prefill_tc_kernel(const __grid_
             mx = fmaxf(mx, s[c]);
           }
         } else {
+          float m8[8];  // 8 independent chains: the max is not a 64-long dependency
 #pragma unroll
-          for (int c = 0; c < PF_BLK; ++c) mx = fmaxf(mx, s[c]);
+          for (int c = 0; c < 8; ++c) m8[c] = s[c];
+#pragma unroll
+          for (int c = 8; c < PF_BLK; ++c) m8[c & 7] = fmaxf(m8[c & 7], s[c]);
+          mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
         }
         mx *= sl2;
         // lazy rescale, warp-uniform (tcgen05.ld/st are warp-collective): rows
@@ -415,14 +419,15 @@ __global__ void __launch_bounds__(PF_THREADS, 1) prefill_tc_kernel(const __grid_
         const float mb = m_new == -INFINITY ? 0.f : m_new;  // a row with no key yet: P = 0, not NaN
         // P = 2^(s - m) in bf16 (before waiting for the group's previous PV)
         uint32_t w[PF_BLK / 2];
-        float rs = 0.f;
+        float rs4[4] = {0.f, 0.f, 0.f, 0.f};  // 4 independent sum chains
 #pragma unroll
         for (int e = 0; e < PF_BLK / 2; ++e) {
           const float a0 = fast_exp2(fmaf(s[2 * e], sl2, -mb)), a1 = fast_exp2(fmaf(s[2 * e + 1], sl2, -mb));
-          rs += a0 + a1;
+          rs4[e & 3] += a0 + a1;
           const __nv_bfloat162 h = __floats2bfloat162_rn(a0, a1);
           w[e] = *reinterpret_cast<const uint32_t*>(&h);
         }
+        const float rs = (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
         // the group's previous PV (maybe the last item's) read P buffer grp and wrote O_grp
         if (u > 0) pf_wait(&odone[grp], (u - 1) & 1);
         if (any) {
