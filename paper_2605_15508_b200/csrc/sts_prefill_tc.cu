@@ -272,30 +272,40 @@ __global__ void __launch_bounds__(PF_THREADS, 1) prefill_tc_kernel(const __grid_
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0) {
-      uint32_t kv = 0;  // blocks loaded so far (ring position)
-      int n_it = 0;
-      for (int i = pf_item_index(0, n_items); i < n_items; i = pf_item_index(n_it + 1, n_items), ++n_it) {
-        const PfItem it = pf_item(p, i);
-        const int qb = n_it & 1;
+    // the whole warp walks the items: the block ids of 32 blocks at a time
+    // come in one load across the lanes (a selection's list is a dependent
+    // read, one per block would serialise the producer), lane 0 issues
+    uint32_t kv = 0;  // blocks loaded so far (ring position)
+    int n_it = 0;
+    for (int i = pf_item_index(0, n_items); i < n_items; i = pf_item_index(n_it + 1, n_items), ++n_it) {
+      const PfItem it = pf_item(p, i);
+      const int qb = n_it & 1;
+      if (lane == 0) {
         if (n_it >= 2) pf_wait(&qempty[qb], ((n_it >> 1) - 1) & 1);  // item n_it - 2 done with this Q buffer
         pf_expect_tx(&qfull[qb], L::Q_BYTES);
 #pragma unroll
         for (int s = 0; s < L::SLABS; ++s)
           pf_tma3(smem + L::OFF_Q + qb * L::Q_BYTES + s * PF_ROWS * 128, &qmap, &qfull[qb], s * 64,
                   it.T * PF_ROWS, it.hq);
-        for (int j = 0; j < it.nb; ++j, ++kv) {
-          const int b = pf_block(p, it.kvh, it.T, it.ncommit, j);
-          const int stage = kv % PF_STAGES;
-          pf_wait(&empty[stage], ((kv / PF_STAGES) & 1) ^ 1);
-          pf_expect_tx(&full[stage], 2 * L::KB_BYTES);
+      }
+      for (int j0 = 0; j0 < it.nb; j0 += 32) {
+        const int bid = j0 + lane < it.nb ? pf_block(p, it.kvh, it.T, it.ncommit, j0 + lane) : 0;
+        const int cnt32 = min(32, it.nb - j0);
+        for (int jl = 0; jl < cnt32; ++jl, ++kv) {
+          const int b = __shfl_sync(0xffffffffu, bid, jl);
+          if (lane == 0) {
+            const int stage = kv % PF_STAGES;
+            pf_wait(&empty[stage], ((kv / PF_STAGES) & 1) ^ 1);
+            pf_expect_tx(&full[stage], 2 * L::KB_BYTES);
 #pragma unroll
-          for (int s = 0; s < L::SLABS; ++s) {
-            pf_tma3(smem + L::OFF_K + stage * L::KB_BYTES + s * PF_BLK * 128, &kmap, &full[stage], s * 64,
-                    b * PF_BLK, it.kvh);
-            pf_tma3(smem + L::OFF_V + stage * L::KB_BYTES + s * PF_BLK * 128, &vmap, &full[stage], s * 64,
-                    b * PF_BLK, it.kvh);
+            for (int s = 0; s < L::SLABS; ++s) {
+              pf_tma3(smem + L::OFF_K + stage * L::KB_BYTES + s * PF_BLK * 128, &kmap, &full[stage], s * 64,
+                      b * PF_BLK, it.kvh);
+              pf_tma3(smem + L::OFF_V + stage * L::KB_BYTES + s * PF_BLK * 128, &vmap, &full[stage], s * 64,
+                      b * PF_BLK, it.kvh);
+            }
           }
+          __syncwarp();
         }
       }
     }
@@ -376,7 +386,7 @@ __global__ void __launch_bounds__(PF_THREADS, 1) prefill_tc_kernel(const __grid_
       uint32_t& u = grp ? u1 : u0;
       float m = -INFINITY, l = 0.f;
       for (int j = grp; j < nb; j += 2, ++u) {
-        const int b = pf_block(p, it.kvh, it.T, it.ncommit, j);
+        const int b = 2 * it.T + (j - it.ncommit);  // (used for the diagonal blocks only)
         pf_wait(&sfull[grp], u & 1);
         pf_fence_after();
         float s[PF_BLK];
