@@ -24,6 +24,8 @@
 // a per-CTA slot of the global workspace (persistent grid over rows).
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "sts_common.cuh"
 
 namespace sts {
@@ -728,18 +730,18 @@ __device__ __forceinline__ int block_scan_nw(int v, int* warp_tot, int& total) {
 
 // Lane-exclusive prefixes and warp totals of per-g nibble popcounts, packed
 // 4 groups per word in 8-bit fields (a lane count is <= 4, a warp's <= 128).
-template <int G>
+template <int G, typename M>
 struct NibbleScan {
   static constexpr int W = (G + 3) / 4;
   uint32_t excl[W], tot[W];
-  __device__ __forceinline__ NibbleScan(uint32_t bits) {
+  __device__ __forceinline__ NibbleScan(M bits) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
       uint32_t v = 0u;
 #pragma unroll
       for (int q = 0; q < 4; ++q)
-        if (4 * w + q < G) v |= (uint32_t)__popc((bits >> (4 * (4 * w + q))) & 15u) << (8 * q);
+        if (4 * w + q < G) v |= (uint32_t)__popc((uint32_t)(bits >> (4 * (4 * w + q))) & 15u) << (8 * q);
       uint32_t x = v;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -754,15 +756,18 @@ struct NibbleScan {
   __device__ __forceinline__ int total(int g) const { return (int)((tot[g >> 2] >> (8 * (g & 3))) & 255u); }
 };
 
+__device__ __forceinline__ int popc_m(uint32_t x) { return __popc(x); }
+__device__ __forceinline__ int popc_m(unsigned long long x) { return __popcll(x); }
+
 // one histogram pass over the register keys; FULL: every key of the thread is
 // in the row, FIRST: every valid key matches the prefix (common bits)
-template <int KPT, bool FULL, bool FIRST>
-__device__ __forceinline__ void hist_pass(const uint32_t (&key)[KPT], uint32_t valid, uint32_t pmask,
+template <int KPT, bool FULL, bool FIRST, typename M>
+__device__ __forceinline__ void hist_pass(const uint32_t (&key)[KPT], M valid, uint32_t pmask,
                                           uint32_t prefix, int s, uint32_t bmask, uint32_t* hist) {
 #pragma unroll
   for (int i = 0; i < KPT; ++i) {
     bool m = FIRST ? true : (key[i] & pmask) == prefix;
-    if (!FULL) m = m && ((valid >> i) & 1u);
+    if (!FULL) m = m && ((valid >> i) & 1);
     if (m) atomicAdd(&hist[(key[i] >> s) & bmask], 1u);
   }
 }
@@ -771,7 +776,9 @@ template <int KPT, int NSRC>
 __global__ void __launch_bounds__(SEL_THREADS, 1) select_reg_kernel(SelectParams p) {
   constexpr int NT = SEL_THREADS, NW = SEL_WARPS, G = KPT / 4;
   constexpr int BPT = NBINS / NT;  // histogram bins per thread in the scan
-  static_assert(KPT % 4 == 0 && KPT <= 32 && NW == 32 && BPT * NT == NBINS, "layout");
+  static_assert(KPT % 4 == 0 && KPT <= 64 && NW == 32 && BPT * NT == NBINS, "layout");
+  using M = typename std::conditional<(KPT > 32), unsigned long long, uint32_t>::type;  // one bit per key slot
+  constexpr M ONE = 1;
   __shared__ uint32_t hist[NBINS];
   __shared__ int scan_a[NW], scan_b[NW];
   __shared__ int bc[3];
@@ -834,11 +841,11 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) select_reg_kernel(SelectParams
           key[i] = f32_key(a);
         }
       }
-      uint32_t valid = 0xffffffffu;
+      M valid = ~(M)0;
       if (!full) {
-        valid = 0u;
+        valid = 0;
 #pragma unroll
-        for (int i = 0; i < KPT; ++i) valid |= (jl + 128 * (i >> 2) + (i & 3) < n ? 1u : 0u) << i;
+        for (int i = 0; i < KPT; ++i) valid |= (jl + 128 * (i >> 2) + (i & 3) < n ? ONE : (M)0) << i;
       }
       uint32_t k_or = 0u, k_and = 0xffffffffu;
       if (full) {
@@ -850,7 +857,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) select_reg_kernel(SelectParams
       } else {
 #pragma unroll
         for (int i = 0; i < KPT; ++i)
-          if ((valid >> i) & 1u) {
+          if ((valid >> i) & 1) {
             k_or |= key[i];
             k_and &= key[i];
           }
@@ -885,11 +892,11 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) select_reg_kernel(SelectParams
           __syncthreads();
           const uint32_t bmask = (uint32_t)(nb - 1);
           if (first) {
-            if (full) hist_pass<KPT, true, true>(key, valid, pmask, prefix, s, bmask, h);
-            else hist_pass<KPT, false, true>(key, valid, pmask, prefix, s, bmask, h);
+            if (full) hist_pass<KPT, true, true, M>(key, valid, pmask, prefix, s, bmask, h);
+            else hist_pass<KPT, false, true, M>(key, valid, pmask, prefix, s, bmask, h);
           } else {
-            if (full) hist_pass<KPT, true, false>(key, valid, pmask, prefix, s, bmask, h);
-            else hist_pass<KPT, false, false>(key, valid, pmask, prefix, s, bmask, h);
+            if (full) hist_pass<KPT, true, false, M>(key, valid, pmask, prefix, s, bmask, h);
+            else hist_pass<KPT, false, false, M>(key, valid, pmask, prefix, s, bmask, h);
           }
           __syncthreads();
           int local[BPT], lsum = 0;
@@ -927,16 +934,16 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) select_reg_kernel(SelectParams
       }
 
       // emit ascending: above-threshold keys, the first `need` of the class, extras
-      uint32_t gt = 0u, eq = 0u;
+      M gt = 0, eq = 0;
 #pragma unroll
       for (int i = 0; i < KPT; ++i) {
         const uint32_t hk = key[i] & pmask;
-        gt |= (hk > prefix ? 1u : 0u) << i;
-        eq |= (hk == prefix ? 1u : 0u) << i;
+        gt |= (hk > prefix ? ONE : (M)0) << i;
+        eq |= (hk == prefix ? ONE : (M)0) << i;
       }
       gt &= valid;
       eq &= valid;
-      uint32_t sel = gt;
+      M sel = gt;
       const int lo_extra = p.recent_window > 0 ? n - p.recent_window : n;
       const bool cur = (p.flags & STS_SEL_CURRENT) != 0, sink = (p.flags & STS_SEL_SINK) != 0;
       const int whi = wbase + 32 * KPT - 1;
@@ -944,34 +951,34 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) select_reg_kernel(SelectParams
 #pragma unroll
         for (int i = 0; i < KPT; ++i) {
           const int j = jl + 128 * (i >> 2) + (i & 3);
-          if (j < n && (j >= lo_extra || (sink && j == 0) || (cur && j == n - 1))) sel |= 1u << i;
+          if (j < n && (j >= lo_extra || (sink && j == 0) || (cur && j == n - 1))) sel |= ONE << i;
         }
       }
       if (need == ties) {
         sel |= eq;
       } else {
         int tot;
-        int rank = warp_excl_scan_of_warps<NW>(__reduce_add_sync(0xffffffffu, (uint32_t)__popc(eq)), scan_b, tot);
-        const NibbleScan<G> ns(eq);
+        int rank = warp_excl_scan_of_warps<NW>(__reduce_add_sync(0xffffffffu, (uint32_t)popc_m(eq)), scan_b, tot);
+        const NibbleScan<G, M> ns(eq);
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           int rr = rank + ns.before(g);
 #pragma unroll
           for (int e = 0; e < 4; ++e)
-            if ((eq >> (4 * g + e)) & 1u) {
-              if (rr < need) sel |= 1u << (4 * g + e);
+            if ((eq >> (4 * g + e)) & 1) {
+              if (rr < need) sel |= ONE << (4 * g + e);
               ++rr;
             }
           rank += ns.total(g);
         }
       }
-      int pos = warp_excl_scan_of_warps<NW>(__reduce_add_sync(0xffffffffu, (uint32_t)__popc(sel)), scan_a, count);
-      const NibbleScan<G> ns(sel);
+      int pos = warp_excl_scan_of_warps<NW>(__reduce_add_sync(0xffffffffu, (uint32_t)popc_m(sel)), scan_a, count);
+      const NibbleScan<G, M> ns(sel);
       const bool fits = count <= p.idx_ld;
 #pragma unroll
       for (int g = 0; g < G; ++g) {
         int q = pos + ns.before(g);
-        uint32_t nib = (sel >> (4 * g)) & 15u;
+        uint32_t nib = (uint32_t)(sel >> (4 * g)) & 15u;
         while (nib) {  // set bits only (a tenth of the keys at 90% sparsity)
           const int e = __ffs(nib) - 1;
           if (fits) out[q] = jl + 128 * g + e;
@@ -1077,16 +1084,21 @@ extern "C" int sts_select_topk(const float* scores_dev, int64_t ld, const int32_
   p.status = status_dev;
   p.buf_bytes = key_buf_bytes(max_len, page_size);
 
-  // token rows that fit in registers (<= 32K keys): select_reg_kernel
+  // token rows that fit in registers (<= 36K keys): select_reg_kernel
   // (c2: 44 us vs 63 us for select_kernel, profiles/r02/select/)
-  if (page_size == 1 && max_len <= 32 * 32 * SEL_WARPS) {
+  if (page_size == 1 && max_len <= 36 * 32 * SEL_WARPS) {
     const int64_t grid = rows < ((int64_t)1 << 30) ? rows : ((int64_t)1 << 30);
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (max_len <= 8 * 32 * SEL_WARPS) return launch_reg<8, 0>(p, grid, st);
     if (max_len <= 16 * 32 * SEL_WARPS) return launch_reg<16, 0>(p, grid, st);
-    if (nsrc == 1) return launch_reg<32, 1>(p, grid, st);
-    if (nsrc == 4) return launch_reg<32, 4>(p, grid, st);
-    return launch_reg<32, 0>(p, grid, st);
+    if (max_len <= 32 * 32 * SEL_WARPS) {
+      if (nsrc == 1) return launch_reg<32, 1>(p, grid, st);
+      if (nsrc == 4) return launch_reg<32, 4>(p, grid, st);
+      return launch_reg<32, 0>(p, grid, st);
+    }
+    // just past 32K (mode-R rows: the committed context plus their in-block prefix)
+    if (nsrc == 1) return launch_reg<36, 1>(p, grid, st);
+    return launch_reg<36, 0>(p, grid, st);
   }
   const size_t sh_bytes = (sizeof(SelShared) + 15) & ~size_t(15);
   size_t smem = sh_bytes;

@@ -186,10 +186,10 @@ def test_capacity_status_flag(cuda_ok):
     assert status.item() & 0x1
 
 
-@pytest.mark.parametrize("n", [8192, 8193, 16384, 16385, 32767, 32768, 32769])
+@pytest.mark.parametrize("n", [8192, 8193, 16384, 16385, 32767, 32768, 32769, 36864, 36865])
 def test_register_select_boundaries(cuda_ok, n):
-    """Token rows around the register kernel's capacity steps (8K / 16K / 32K
-    keys per CTA; 32769 falls back to select_kernel): every row kind, ties
+    """Token rows around the register kernel's capacity steps (8K / 16K / 32K /
+    36K keys per CTA; 36865 falls back to select_kernel): every row kind, ties
     spanning many warps (coarse rows), extras — bit-exact vs the oracle."""
     from paper_2605_15508_b200 import SparsityConfig
     from paper_2605_15508_b200.sparsity import select_rows
