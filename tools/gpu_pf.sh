@@ -9,7 +9,7 @@ python -c "
 import json
 for l in open('$OUT/bench.log'):
     if l.startswith('{'):
-        d=json.loads(l); print(d['workload'][60:80], 'sparse', d['sparse_prefill_us'], 'dense', d['dense_same_kernel_us'], 'TF/s', d['dense_same_kernel_TFLOPs'], 'fa', d['dense_flash_attn_us'])
+        d=json.loads(l); print(d['workload'][60:80], 'sel', d['tile_select_us'], 'selg', d.get('tile_select_graph_us'), 'sparse', d['sparse_prefill_us'], 'dense', d['dense_same_kernel_us'], 'TF/s', d['dense_same_kernel_TFLOPs'], 'fa', d['dense_flash_attn_us'])
 " || tail -3 $OUT/bench.log
 if [ -z "$NO_NCU" ]; then
 timeout 600 ncu --set full --import-source on --clock-control none -k regex:prefill_tc -s 4 -c 1 -o $OUT/pf -f python tools/bench_prefill_tc.py --n 16384 --iters 1 > $OUT/ncu.log 2>&1
