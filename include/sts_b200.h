@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define STS_ABI_VERSION 6
+#define STS_ABI_VERSION 7
 
 #define STS_OK 0
 #define STS_ERR_INPUT 1
@@ -299,7 +299,19 @@ STS_API int sts_block_attention_f64(const float* q_dev, const float* k_cache_dev
  *   from K/V in pinned, device-mapped host memory ([unit][row][d], strides in
  *   elements) into the pool ([unit][pages_ld * P][d]), with `ctas` CTAs (one
  *   warp per page, 16-byte loads over the host link) so it runs beside the
- *   attention of units already resident.
+ *   attention of units already resident.  slots_dev (NULL: page w of a
+ *   unit's list goes to pool rank w) gives each listed page its pool slot.
+ * sts_page_cache_plan — the "prefetch" strategy's residency across steps
+ *   (src/offloadsim.py:173-209, per unit with a capacity of `slots` pages):
+ *   slot_page / slot_last ([units][slots_ld], persistent, -1 = empty) hold
+ *   each pool slot's page and the step that last used it.  The step's
+ *   committed pages already resident keep their slots; the missing ones
+ *   (ascending) are listed in copy_pages / copy_slots (ncopy per unit) and
+ *   take free slots in the reference's LRU eviction order (empty first,
+ *   then by (last use, page)); the key list is re-expressed in pool rows as
+ *   in sts_page_plan (tail pages at fixed ranks >= tail_rank0 >= slots).
+ *   A step needing more than `slots` committed pages sets
+ *   STS_DEV_IDX_CAPACITY.
  * ---------------------------------------------------------------------- */
 STS_API int sts_page_plan(const int32_t* idx_dev, int64_t idx_ld, const int32_t* cnt_dev, int64_t units,
                           int32_t page_size, int32_t tail_page0, int32_t tail_rank0, int32_t* pages_dev,
@@ -308,8 +320,14 @@ STS_API int sts_page_plan(const int32_t* idx_dev, int64_t idx_ld, const int32_t*
 STS_API int sts_page_copy(const void* host_k, const void* host_v, int64_t host_unit_stride,
                           int64_t host_row_stride, int32_t n_rows_host, void* pool_k, void* pool_v,
                           int64_t pool_unit_stride, int32_t d, int32_t elem_bytes, const int32_t* pages_dev,
-                          int64_t pages_ld, const int32_t* npages_dev, int64_t unit_begin, int64_t unit_end,
-                          int32_t page_size, int32_t tail_page0, int32_t tail_rank0, int32_t ctas, void* stream);
+                          int64_t pages_ld, const int32_t* npages_dev, const int32_t* slots_dev,
+                          int64_t unit_begin, int64_t unit_end, int32_t page_size, int32_t tail_page0,
+                          int32_t tail_rank0, int32_t ctas, void* stream);
+STS_API int sts_page_cache_plan(const int32_t* idx_dev, int64_t idx_ld, const int32_t* cnt_dev, int64_t units,
+                                int32_t page_size, int32_t tail_page0, int32_t tail_rank0, int32_t* slot_page_dev,
+                                int32_t* slot_last_dev, int64_t slots_ld, int32_t slots, int32_t step,
+                                int32_t* copy_pages_dev, int32_t* copy_slots_dev, int32_t* ncopy_dev,
+                                int32_t* idx_pool_dev, int32_t* status_dev, void* stream);
 
 /* ------------------------------------------------------------------------
  * sts_prefill_blocksparse — block-sparse prefill attention on tcgen05

@@ -515,6 +515,32 @@ def find_head_mapping(samples, draft_heads, target_heads, k: int) -> dict:
 # ---------------------------------------------------------------------------
 
 
+def lru_prefetch_steps(traces, capacity: int):
+    """The "prefetch" strategy's residency for one layer
+    (src/offloadsim.py:173-209 with _lru_insert / _lru_touch :135-150): per
+    step, the pages not resident (in trace order) are inserted FIFO, evicting
+    the first non-pinned page in LRU-dict order while the tier is full; then
+    every page of the step is touched in trace order.  Returns per step the
+    list of missing pages (what the device tier copies)."""
+    resident: dict = {}
+    out = []
+    for pages in traces:
+        pinned = set(pages)
+        if len(pinned) > capacity:
+            raise ValueError("step needs more pages than the tier holds")
+        missing = [p for p in pages if p not in resident]
+        for key in missing:
+            while len(resident) >= capacity:
+                victim = next(k for k in resident if k not in pinned)
+                resident.pop(victim)
+            resident[key] = True
+        for key in pages:
+            resident.pop(key)
+            resident[key] = True
+        out.append(missing)
+    return out
+
+
 @dataclass(frozen=True)
 class OracleModelConfig:
     """Fields of src/toymodel.py:38-57 ``ModelConfig``."""

@@ -25,7 +25,7 @@ STS_DEV_EMPTY_ROW = 0x2
 STS_DEV_BAD_INDEX = 0x4
 STS_DEV_SELECT_INCONSISTENT = 0x8
 STS_BLOCK_INCLUDE_SELF = 0x1
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 _i32, _i64, _u32, _f32, _f64 = C.c_int32, C.c_int64, C.c_uint32, C.c_float, C.c_double
 _p, _sz = C.c_void_p, C.c_size_t
@@ -61,8 +61,10 @@ SIGNATURES = {
     "sts_block_attention_f64": (C.c_int, [_p, _p, _p, _i64, _i64, _i32, _i32, _i32, _i32, _f64, _p, _i64, _p, _p,
                                           _i32, _p, _i64, _p, _p, _i64, _p, _p]),
     "sts_page_plan": (C.c_int, [_p, _i64, _p, _i64, _i32, _i32, _i32, _p, _i64, _p, _p, _p, _p]),
-    "sts_page_copy": (C.c_int, [_p, _p, _i64, _i64, _i32, _p, _p, _i64, _i32, _i32, _p, _i64, _p, _i64, _i64, _i32,
-                                _i32, _i32, _i32, _p]),
+    "sts_page_copy": (C.c_int, [_p, _p, _i64, _i64, _i32, _p, _p, _i64, _i32, _i32, _p, _i64, _p, _p, _i64, _i64,
+                                _i32, _i32, _i32, _i32, _p]),
+    "sts_page_cache_plan": (C.c_int, [_p, _i64, _p, _i64, _i32, _i32, _i32, _p, _p, _i64, _i32, _i32, _p, _p, _p, _p,
+                                      _p, _p]),
     "sts_prefill_blocksparse": (C.c_int, [_p, _p, _p, _i32, _i32, _i32, _i32, _i64, _i64, _i64, _f32, _p, _i64, _p,
                                           _p, _p, _p]),
     "sts_dist_select_rounds": (_i32, [_i32]),

@@ -222,3 +222,18 @@ def test_lse_merge_equals_union_attention():
         outs.append(o[None]); lses.append(np.array([l]))
     merged, _ = O.lse_merge(outs, lses)
     np.testing.assert_allclose(merged[0], want, rtol=1e-5, atol=1e-6)
+
+
+def test_lru_prefetch_matches_reference_simulator():
+    """The resident-pool restatement reproduces the reference simulator's
+    per-step transfers (specsparse.offloadsim.simulate('prefetch'), recorded
+    by tests/golden/make_offload_golden.py)."""
+    import json
+    from pathlib import Path
+
+    from oracle import sts_oracle as O
+
+    g = json.loads((Path(__file__).resolve().parent / "golden" / "offload_lru.json").read_text())
+    for case in g["cases"]:
+        missing = O.lru_prefetch_steps(case["traces"], case["capacity"])
+        assert [len(m) for m in missing] == case["missing_per_step"]
