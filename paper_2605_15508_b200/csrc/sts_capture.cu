@@ -217,8 +217,10 @@ struct StepIter {
 };
 
 // RT: rows per head at compile time (5 = gamma 4, the configured depth), 0 = runtime p.R;
-// MODE: CAP_MODE_LSE or CAP_MODE_PROBS (p.mode is ignored)
-template <int D, int NCOL, int RT, int MODE>
+// MODE: CAP_MODE_LSE or CAP_MODE_PROBS (p.mode is ignored);
+// MC: the unit's stacked rows G*R at compile time (0 = runtime p.M): the
+// per-score loops then skip the MMA's padding columns (c2: 20 of 32, c3: 35 of 48)
+template <int D, int NCOL, int RT, int MODE, int MC = 0>
 __global__ void __launch_bounds__(cap_threads(NCOL, MODE), 1)
     capture_kernel(const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap qmap, CapParams p) {
   using L = CapLayout<D, NCOL, MODE>;
@@ -350,7 +352,8 @@ __global__ void __launch_bounds__(cap_threads(NCOL, MODE), 1)
     const int key_in_tile = quad * 32 + lane;
     const int ew = warp - 2;    // epilogue warp index
     const int grp = ew >> 2;    // steps with index % GROUPS == grp
-    const int M = p.M, R = p.R;
+    const int M = MC > 0 ? MC : p.M, R = p.R;
+    constexpr int MR = MC > 0 ? MC : NCOL;  // columns the per-score loops visit
     const int lim = p.causal_base - p.pos_offset;  // row r sees local keys j <= lim + r % R
     const float sl2 = p.scale * LOG2E;
     int slot = 0, stage = 0;
@@ -404,14 +407,14 @@ __global__ void __launch_bounds__(cap_threads(NCOL, MODE), 1)
             // steady state: x = s*scale*log2e - m (one FFMA), 2^x (MUFU), sum (FADD)
             bool need = false;
 #pragma unroll
-            for (int r = 0; r < NCOL; ++r) {
+            for (int r = 0; r < MR; ++r) {
               const float x = fmaf(s[r], sl2, -mx[r]);
               s[r] = x;
               need |= x > 32.f;
             }
             if (__any_sync(0xffffffffu, need)) {  // warp-uniform and rare: a jump of 2^32 moves the reference
 #pragma unroll
-              for (int r = 0; r < NCOL; ++r) {
+              for (int r = 0; r < MR; ++r) {
                 const float real = s[r] + mx[r];
                 const float mn = fmaxf(mx[r], real);
                 ls[r] *= fast_exp2(mx[r] - mn);
@@ -420,7 +423,7 @@ __global__ void __launch_bounds__(cap_threads(NCOL, MODE), 1)
               }
             }
 #pragma unroll
-            for (int r = 0; r < NCOL; ++r)
+            for (int r = 0; r < MR; ++r)
               if (r < M) ls[r] += fast_exp2(s[r]);
             continue;
           }
@@ -428,10 +431,10 @@ __global__ void __launch_bounds__(cap_threads(NCOL, MODE), 1)
             // probabilities: 2^(s*scale*log2e - lse2) in one FFMA + MUFU
             if (in_range && p.probs_mode != 2) {
 #pragma unroll
-              for (int r = 0; r < NCOL; ++r) s[r] = fast_exp2(fmaf(s[r], sl2, -mx[r]));
+              for (int r = 0; r < MR; ++r) s[r] = fast_exp2(fmaf(s[r], sl2, -mx[r]));
             } else {
 #pragma unroll
-              for (int r = 0; r < NCOL; ++r) s[r] *= p.scale;
+              for (int r = 0; r < MR; ++r) s[r] *= p.scale;
             }
           } else {
             // masked tile (a unit's causal tail / past the last key) or the
@@ -625,12 +628,12 @@ int make_map(CUtensorMap* map, const void* base, int64_t units, int64_t rows, in
   return STS_OK;
 }
 
-template <int D, int NCOL, int RT, int MODE>
+template <int D, int NCOL, int RT, int MODE, int MC>
 int launch_m(const CUtensorMap& km, const CUtensorMap& qm, const CapParams& p, cudaStream_t st) {
   using L = CapLayout<D, NCOL, MODE>;
   static_assert(L::SMEM <= 227 * 1024, "capture shared memory");
-  STS_CUDA_CHECK(
-      cudaFuncSetAttribute(capture_kernel<D, NCOL, RT, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM));
+  STS_CUDA_CHECK(cudaFuncSetAttribute(capture_kernel<D, NCOL, RT, MODE, MC>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM));
   const int64_t grid = p.tiles < num_sms() ? p.tiles : num_sms();
   cudaLaunchConfig_t cfg;
   memset(&cfg, 0, sizeof(cfg));
@@ -643,20 +646,28 @@ int launch_m(const CUtensorMap& km, const CUtensorMap& qm, const CapParams& p, c
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = MODE == CAP_MODE_PROBS ? 1 : 0;  // the probability pass overlaps the LSE pass's tail
-  STS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, capture_kernel<D, NCOL, RT, MODE>, km, qm, p));
+  STS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, capture_kernel<D, NCOL, RT, MODE, MC>, km, qm, p));
   count_launch();
   return STS_OK;
 }
 
-template <int D, int NCOL, int RT>
+template <int D, int NCOL, int RT, int MC = 0>
 int launch_t(const CUtensorMap& km, const CUtensorMap& qm, const CapParams& p, cudaStream_t st) {
-  return p.mode == CAP_MODE_LSE ? launch_m<D, NCOL, RT, CAP_MODE_LSE>(km, qm, p, st)
-                                : launch_m<D, NCOL, RT, CAP_MODE_PROBS>(km, qm, p, st);
+  return p.mode == CAP_MODE_LSE ? launch_m<D, NCOL, RT, CAP_MODE_LSE, MC>(km, qm, p, st)
+                                : launch_m<D, NCOL, RT, CAP_MODE_PROBS, MC>(km, qm, p, st);
 }
 
 template <int D, int NCOL>
 int launch_r(const CUtensorMap& km, const CUtensorMap& qm, const CapParams& p, cudaStream_t st) {
-  return p.R == 5 ? launch_t<D, NCOL, 5>(km, qm, p, st) : launch_t<D, NCOL, 0>(km, qm, p, st);
+  if (p.R != 5) return launch_t<D, NCOL, 0>(km, qm, p, st);
+  // the measured shapes' stacked rows at compile time (4 or 7 q-heads per kv-head, gamma 4)
+  if constexpr (D == 64 && NCOL == 32) {
+    if (p.M == 20) return launch_t<D, NCOL, 5, 20>(km, qm, p, st);
+  }
+  if constexpr (D == 64 && NCOL == 48) {
+    if (p.M == 35) return launch_t<D, NCOL, 5, 35>(km, qm, p, st);
+  }
+  return launch_t<D, NCOL, 5>(km, qm, p, st);
 }
 
 }  // namespace
