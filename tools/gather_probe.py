@@ -26,8 +26,15 @@ from paper_2605_15508_b200.verify_step import (STSVerifyStep, algorithmic_bytes,
 
 lib = ctypes.CDLL(str(SO))
 lib.gather_probe.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_longlong] * 2 + [ctypes.c_int] * 6 + [ctypes.c_void_p] * 2
-s = config_shape("c2")
-step = STSVerifyStep(s, SparsityConfig(budget=0.1), random_mapping_table(s, 5), mode="S", device="cuda")
+import argparse  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2")
+ap.add_argument("--sparsity", type=float, default=0.9)
+a = ap.parse_args([x for x in sys.argv[1:] if x != "--build"])
+s = config_shape(a.config)
+step = STSVerifyStep(s, SparsityConfig(budget=round(1 - a.sparsity, 6)), random_mapping_table(s, 5), mode="S",
+                     device="cuda")
 dq, dk, tq, tk, tv = synthetic_inputs(s, "cuda", seed=0)
 q, k, v = step.target_views(tq, tk, tv)
 dqv, dkv = step.draft_views(dq, dk)
@@ -62,7 +69,8 @@ def timed(fn, iters=20):
 
 
 keys = float(step.cnt.sum().item())
-res = {"workload": "c2 mode S 90%", "selected_keys": int(keys), "peak_copy_gbs": 6549.4}
+res = {"workload": f"{a.config} mode S {a.sparsity:g}", "rows_per_unit": int(step.M), "selected_keys": int(keys),
+       "peak_copy_gbs": 6549.4}
 def probe(splits, unroll, dense_n=0, key_stride=1):
     return timed(lambda: lib.gather_probe(k.data_ptr(), v.data_ptr(), step.idx.data_ptr(), step.cnt.data_ptr(),
                                           step.idx.stride(0), k.stride(0) * 2 // 16, row_vecs, U, splits, dense_n,
