@@ -146,3 +146,27 @@ def test_resident_pool_across_steps_matches_hbm(cuda_ok):
         moved.append(off.bytes_moved())
     assert int(step.status.item()) == 0
     assert moved[1] < moved[0] and moved[2] < moved[0]  # later steps copy only what changed
+
+
+def test_page_cache_capacity_flag(cuda_ok):
+    """A step needing more committed pages than the pool's slots sets
+    STS_DEV_IDX_CAPACITY (the reference raises ConfigError for the same trace,
+    src/offloadsim.py:122-126)."""
+    import torch
+
+    from paper_2605_15508_b200._lib import call, ptr
+
+    P, C, NP = 4, 3, 32
+    toks = torch.tensor([[p * P for p in (1, 5, 9, 13, 17)]], dtype=torch.int32, device="cuda")
+    cnt = torch.tensor([5], dtype=torch.int32, device="cuda")
+    sp = torch.full((1, C + 1), -1, dtype=torch.int32, device="cuda")
+    sl = torch.full((1, C + 1), -1, dtype=torch.int32, device="cuda")
+    cp, cs = torch.empty_like(sp), torch.empty_like(sp)
+    nc = torch.empty((1,), dtype=torch.int32, device="cuda")
+    ip = torch.empty_like(toks)
+    status = torch.zeros((1,), dtype=torch.int32, device="cuda")
+    call("sts_page_cache_plan", ptr(toks), 5, ptr(cnt), 1, P, NP, C, ptr(sp), ptr(sl), C + 1, C, 0, ptr(cp), ptr(cs),
+         ptr(nc), ptr(ip), ptr(status), None)
+    torch.cuda.synchronize()
+    assert int(status.item()) & 0x1
+    assert int(nc.item()) == C
