@@ -127,6 +127,28 @@ def ncu_traffic(key):
     return d.get("dram_bytes"), d.get("source")
 
 
+def gather_floor(config, mode, sparsity):
+    """The measured pure-gather floor of this workload's selection (K and V
+    rows of every selected key, no math; tools/gather_probe.py), from the
+    committed probe runs; None if not measured."""
+    if mode != "S":
+        return None
+    for f in sorted((ROOT / "profiles").glob("r*/**/gather_probe*.json"), reverse=True):
+        try:
+            for line in f.read_text().splitlines():
+                if not line.startswith("{"):
+                    continue
+                d = json.loads(line)
+                w = d.get("workload", "")
+                if w.split()[0] == config and abs(float(w.split()[-1].rstrip("%")) / (100 if w.endswith("%") else 1)
+                                                  - sparsity) < 1e-6:
+                    best = min(v for k, v in d.items() if k.startswith("gather_us"))
+                    return {"us": best, "source": f"tools/gather_probe.py ({f.relative_to(ROOT)})"}
+        except Exception:
+            continue
+    return None
+
+
 class L2Flush:
     """Evict L2 (126 MB) between timed stages with a 256 MB buffer.
 
@@ -608,7 +630,10 @@ def run_single_gpu(args):
                      "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
                      "kernel": "sts_sparse_decode: verify_decode_kernel (gathered flash-decode, cluster/DSMEM or "
                                "stream-K + piece merge)",
-                     "algorithmic_bytes_per_launch": int(nbytes), "peak_source": peak_src},
+                     "algorithmic_bytes_per_launch": int(nbytes), "peak_source": peak_src,
+                     **({"gather_floor_us": gf["us"], "frac_of_gather_floor": round(gf["us"] / att, 4),
+                         "gather_floor_source": gf["source"]} if (gf := gather_floor(args.config, args.mode,
+                                                                                     args.sparsity)) else {})},
         "parity": par,
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e, 2), "unit": "us", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
