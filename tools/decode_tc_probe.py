@@ -17,7 +17,8 @@ import sys
 from pathlib import Path
 
 HERE = Path(__file__).resolve().parent
-SO = HERE / "_build" / "decode_tc.so"
+import os
+SO = Path(os.environ.get("DECODE_TC_SO", str(HERE / "_build" / "decode_tc.so")))
 if "--build" in sys.argv:
     SO.parent.mkdir(exist_ok=True)
     subprocess.run(["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17", "-shared", "-Xcompiler",
