@@ -6,7 +6,7 @@ OUT=${OUT:-gpurun_out/selab}
 mkdir -p $OUT
 timeout 900 python -m pytest tests/test_gpu_select.py tests/test_gpu_pipeline.py tests/test_gpu_measured.py -x -q -p no:cacheprovider > $OUT/pytest.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest.log
 tail -3 $OUT/pytest.log
-for v in ${VARS:-STS_SELECT_SMEM=1 STS_SELECT_CL=1 STS_SELECT_CL=2}; do
+for v in ${VARS:-STS_NONE=0}; do
  env $v timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-extras --parity-units 0 ${BENCH} > $OUT/b_$v.log 2>&1
  python -c "
 import json
