@@ -20,7 +20,7 @@ namespace {
 using sts::fast_exp2;
 using sts::pack_bf16;
 
-constexpr int D = 128, NC = 48, KT = 128, STAGES = 2;
+constexpr int D = 128, NC = 48, KT = 128, KS = 3, VS = 2;  // K ring freed after S, V ring after PV
 constexpr int THREADS = 224;                   // 2 producer warps, 1 MMA warp, 4 softmax warps (<= 2 per SMSP)
 constexpr int Q_SLAB = NC * 128;               // 6 KB per 64-d slab of Q (48 rows x 128 B)
 constexpr int KV_SLAB = KT * 128;              // 16 KB per slab of a K or V tile
@@ -28,11 +28,11 @@ constexpr int KV_TILE = 2 * KV_SLAB;           // 32 KB
 constexpr int P_TILE = KT * 128;               // [key][64 rows] bf16, 16 KB
 constexpr int OFF_Q = 0;
 constexpr int OFF_K = OFF_Q + 2 * Q_SLAB;      // 12 KB (1024-aligned)
-constexpr int OFF_V = OFF_K + STAGES * KV_TILE;
-constexpr int OFF_P = OFF_V + STAGES * KV_TILE;
+constexpr int OFF_V = OFF_K + KS * KV_TILE;
+constexpr int OFF_P = OFF_V + VS * KV_TILE;
 constexpr int OFF_RED = OFF_P + 2 * P_TILE;    // [4 warps][48] floats + flags
 constexpr int OFF_BAR = OFF_RED + 5 * NC * 4 + 64;  // + the row references [48]
-constexpr int NBAR = 2 * STAGES + 2 + 2 + 2 + 2 + 2 + 2;
+constexpr int NBAR = 2 * KS + 2 * VS + 2 + 2 + 2 + 2 + 2 + 2;
 constexpr int SMEM = OFF_BAR + NBAR * 8 + 16 + 1024;
 constexpr int S_COL = 0, O_COL = 128;          // TMEM: S slots at 0 / 48, O^T at 128
 constexpr float JUMP = 16.f;
@@ -46,6 +46,7 @@ struct P {
   float sl2;
   __nv_bfloat16* out;
   float* lse;
+  long long* dbg;  // (optional) per-role wait / busy cycle counters of CTA 0
 };
 
 __device__ __forceinline__ uint32_t su(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -134,9 +135,11 @@ __global__ void __launch_bounds__(THREADS, 1) decode_tc_kernel(P p) {
   extern __shared__ uint8_t raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + OFF_BAR);
-  uint64_t* kvfull = bars;
-  uint64_t* kvempty = bars + STAGES;
-  uint64_t* sfull = bars + 2 * STAGES;
+  uint64_t* kfull = bars;
+  uint64_t* kempty = kfull + KS;
+  uint64_t* vfull = kempty + KS;
+  uint64_t* vempty = vfull + VS;
+  uint64_t* sfull = vempty + VS;
   uint64_t* sempty = sfull + 2;
   uint64_t* pfull = sempty + 2;
   uint64_t* pempty = pfull + 2;
@@ -151,9 +154,13 @@ __global__ void __launch_bounds__(THREADS, 1) decode_tc_kernel(P p) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < STAGES; ++i) {
-      minit(&kvfull[i], 32);  // the stage's producer warp
-      minit(&kvempty[i], 1);
+    for (int i = 0; i < KS; ++i) {
+      minit(&kfull[i], 32);  // producer warp 0
+      minit(&kempty[i], 1);
+    }
+    for (int i = 0; i < VS; ++i) {
+      minit(&vfull[i], 32);  // producer warp 1
+      minit(&vempty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
       minit(&sfull[i], 1);
@@ -198,14 +205,20 @@ __global__ void __launch_bounds__(THREADS, 1) decode_tc_kernel(P p) {
       const int32_t* il = p.idx + u * p.idx_ld;
       const __nv_bfloat16* kb = p.k + u * p.kv_stride;
       const __nv_bfloat16* vb = p.v + u * p.kv_stride;
-      // producer warp w owns ring stage w: it loads the tiles g with g % 2 == w
-      // (4 keys per lane), publishes each as soon as its copies landed
+      // warp 0 streams the K tiles (ring of KS, freed by S), warp 1 the V tiles
+      // (ring of VS, freed by PV); each keeps two tiles in flight and publishes a
+      // tile once the next one is issued (and at the unit's end)
+      const bool isK = warp == 0;
+      const int NS = isK ? KS : VS;
+      uint64_t* fullb = isK ? kfull : vfull;
+      uint64_t* emptyb = isK ? kempty : vempty;
+      const __nv_bfloat16* src = isK ? kb : vb;
+      const uint32_t base = su(sm + (isK ? OFF_K : OFF_V));
       for (int j = 0; j < nt; ++j) {
         const uint32_t g = gj + j;
-        if ((int)(g & 1) != warp) continue;
-        const int st = g & 1;
-        mwait(&kvempty[st], ((g >> 1) & 1) ^ 1);
-        const uint32_t kd = su(sm + OFF_K + st * KV_TILE), vd = su(sm + OFF_V + st * KV_TILE);
+        const int st = g % NS;
+        mwait(&emptyb[st], ((g / NS) & 1) ^ 1);
+        const uint32_t dst = base + st * KV_TILE;
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
           const int key = lane + 32 * h;
@@ -215,14 +228,20 @@ __global__ void __launch_bounds__(THREADS, 1) decode_tc_kernel(P p) {
 #pragma unroll
           for (int c = 0; c < 16; ++c) {
             const uint32_t off = (c >> 3) * KV_SLAB + key * 128 + (((c & 7) ^ (key & 7)) * 16);
-            cpa16(kd + off, kb + (int64_t)pos * D + c * 8, ok);
-            cpa16(vd + off, vb + (int64_t)pos * D + c * 8, ok);
+            cpa16(dst + off, src + (int64_t)pos * D + c * 8, ok);
           }
         }
         asm volatile("cp.async.commit_group;\n" ::: "memory");
+        if (j > 0) {
+          asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+          proxy();
+          marrive(&fullb[(g - 1) % NS]);
+        }
+      }
+      if (nt > 0) {
         asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         proxy();
-        marrive(&kvfull[st]);
+        marrive(&fullb[(gj + nt - 1) % NS]);
       }
       gj += nt;
     }
@@ -239,9 +258,15 @@ __global__ void __launch_bounds__(THREADS, 1) decode_tc_kernel(P p) {
         mwait(qfull, n_u & 1);
         fa();
         auto issue_s = [&](uint32_t g) {  // S of ring tile g into slot g & 1
-          const int st = g % STAGES;
+          const int st = g % KS;
+          long long a0_ = clock64();
           mwait(&sempty[g & 1], ((g >> 1) & 1) ^ 1);
-          mwait(&kvfull[st], (g / STAGES) & 1);
+          long long a1_ = clock64();
+          mwait(&kfull[st], (g / KS) & 1);
+          if (p.dbg && blockIdx.x == 0) {
+            p.dbg[4] += a1_ - a0_;          // MMA: waiting for the S slot
+            p.dbg[5] += clock64() - a1_;    // MMA: waiting for K
+          }
           fa();
 #pragma unroll
           for (int s = 0; s < 2; ++s) {
@@ -251,16 +276,27 @@ __global__ void __launch_bounds__(THREADS, 1) decode_tc_kernel(P p) {
             for (int k = 0; k < 4; ++k) mma(tmem + S_COL + (g & 1) * NC, a + 2 * k, b + 2 * k, id_s, (s | k) != 0);
           }
           commit(&sfull[g & 1]);
+          commit(&kempty[st]);  // the K stage is free once S is done
         };
         if (nt > 0) issue_s(gj);
         for (int j = 0; j < nt; ++j) {
           const uint32_t g = gj + j;
           if (j + 1 < nt) issue_s(g + 1);
           if (j + 1 == nt) commit(qempty);  // every S of the unit issued: Q may be replaced
+          long long b0_ = clock64();
           mwait(&pfull[g & 1], (g >> 1) & 1);
+          long long b1_ = clock64();
           if (j == 0 && n_u > 0) mwait(oempty, (n_u - 1) & 1);  // O^T drained by the last unit's epilogue
+          if (p.dbg && blockIdx.x == 0) {
+            p.dbg[6] += b1_ - b0_;          // MMA: waiting for P
+            p.dbg[7] += clock64() - b1_;    // MMA: waiting for O drained
+          }
           fa();
-          const int st = g % STAGES;
+          const int st = g % VS;
+          long long v0_ = clock64();
+          mwait(&vfull[st], (g / VS) & 1);
+          if (p.dbg && blockIdx.x == 0) p.dbg[8] += clock64() - v0_;  // MMA: waiting for V
+          fa();
           // O^T += V^T . P: A = V tile (MN-major: 64-d atoms 16 KB apart, 8-key groups 1 KB apart),
           // B = P (MN-major: rows 0..47 of a 64-wide atom, 8-key groups 1 KB apart); K = 16 keys per MMA
           const uint64_t a = dmn(sm + OFF_V + st * KV_TILE, KV_SLAB, 1024);
@@ -268,7 +304,7 @@ __global__ void __launch_bounds__(THREADS, 1) decode_tc_kernel(P p) {
 #pragma unroll
           for (int k = 0; k < KT / 16; ++k)
             mma(tmem + O_COL, a + (uint64_t)(2048 >> 4) * k, b + (uint64_t)(2048 >> 4) * k, id_o, (j > 0 || k > 0) ? 1u : 0u);
-          commit(&kvempty[st]);
+          commit(&vempty[st]);
           commit(&pempty[g & 1]);
         }
         if (nt == 0) commit(qempty);
@@ -297,7 +333,9 @@ __global__ void __launch_bounds__(THREADS, 1) decode_tc_kernel(P p) {
         const int kk = j * KT + t;
         const bool ok = kk < n;
         const int pos = ok ? il[kk] : 0;
+        long long c0_ = clock64();
         mwait(&sfull[g & 1], (g >> 1) & 1);
+        long long c1_ = clock64();
         fa();
         float x[NC];
         ld16(tmem + loff + S_COL + (g & 1) * NC, x);
@@ -306,9 +344,12 @@ __global__ void __launch_bounds__(THREADS, 1) decode_tc_kernel(P p) {
         wld();
         fb();
         marrive(&sempty[g & 1]);
+        // committed keys are seen by every row; an in-block key by the rows of
+        // each head at or after its offset (gamma + 1 = 5 rows per head, compiled in)
+        const int toff = pos - p.base;  // < 0: committed
 #pragma unroll
         for (int r = 0; r < NC; ++r) {
-          const bool vis = ok && r < M && pos <= p.base + (r % p.R);
+          const bool vis = ok && r < M && toff <= (r % 5);
           x[r] = vis ? x[r] * p.sl2 : -INFINITY;
         }
         bool need = j == 0;
@@ -365,7 +406,15 @@ __global__ void __launch_bounds__(THREADS, 1) decode_tc_kernel(P p) {
           lt[2 * e + 1] += a1;
           w[e] = pack_bf16(a0, a1);
         }
+        long long c2_ = clock64();
         mwait(&pempty[g & 1], ((g >> 1) & 1) ^ 1);  // PV two tiles back has read this P buffer
+        long long c3_ = clock64();
+        if (p.dbg && blockIdx.x == 0 && t == 0) {
+          p.dbg[0] += c1_ - c0_;  // softmax: waiting for S
+          p.dbg[1] += c2_ - c1_;  // softmax: compute
+          p.dbg[2] += c3_ - c2_;  // softmax: waiting for the P buffer
+          p.dbg[3] += 1;
+        }
         uint8_t* prow = sm + OFF_P + (g & 1) * P_TILE + t * 128;
 #pragma unroll
         for (int c = 0; c < NC / 8; ++c)
@@ -430,8 +479,8 @@ __global__ void __launch_bounds__(THREADS, 1) decode_tc_kernel(P p) {
 
 extern "C" int decode_tc(const void* q, const void* k, const void* v, long long kv_stride, long long units, int M,
                          int R, int base, const int* idx, long long idx_ld, const int* cnt, float scale, void* out,
-                         float* lse, int sms, void* stream) {
-  if (M > NC) return 2;
+                         float* lse, int sms, void* stream, long long* dbg) {
+  if (M > NC || R != 5) return 2;
   P p;
   p.q = (const __nv_bfloat16*)q;
   p.k = (const __nv_bfloat16*)k;
@@ -447,6 +496,7 @@ extern "C" int decode_tc(const void* q, const void* k, const void* v, long long 
   p.sl2 = scale * 1.4426950408889634f;
   p.out = (__nv_bfloat16*)out;
   p.lse = lse;
+  p.dbg = dbg;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(decode_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);

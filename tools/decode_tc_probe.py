@@ -41,7 +41,7 @@ a = ap.parse_args()
 lib = ctypes.CDLL(str(SO))
 lib.decode_tc.argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_longlong] * 2 + [ctypes.c_int] * 3 + \
     [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_void_p, ctypes.c_float, ctypes.c_void_p, ctypes.c_void_p,
-     ctypes.c_int, ctypes.c_void_p]
+     ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p]
 if a.config == "small":
     s = VerifyShape(batch=2, context=5000, gamma=4, target_layers=3, target_q_heads=14, target_kv_heads=2,
                     head_dim=128, draft_layers=2, draft_q_heads=8, draft_kv_heads=2, draft_head_dim=64)
@@ -63,10 +63,13 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 acc = torch.empty((), dtype=torch.int64, device="cuda")
 
 
-def run_tc():
+dbg = torch.zeros(16, dtype=torch.int64, device="cuda")
+
+
+def run_tc(d=None):
     rc = lib.decode_tc(q.data_ptr(), k.data_ptr(), v.data_ptr(), k.stride(0), U, M, s.rows, s.context,
                        step.idx.data_ptr(), step.idx.stride(0), step.cnt.data_ptr(), 1.0 / math.sqrt(s.head_dim),
-                       out_tc.data_ptr(), lse_tc.data_ptr(), sms, st)
+                       out_tc.data_ptr(), lse_tc.data_ptr(), sms, st, d.data_ptr() if d is not None else None)
     assert rc == 0, rc
 
 
@@ -86,8 +89,13 @@ def timed(fn, iters=20):
 
 
 step.attend(q, k, v)
-run_tc()
+run_tc(dbg)
 torch.cuda.synchronize()
+cyc = dbg.cpu().tolist()
+tiles = max(1, cyc[3])
+cycles = {"tiles_cta0": cyc[3]} | {name: round(cyc[i] / tiles) for i, name in enumerate(
+    ["sm_wait_S", "sm_compute", "sm_wait_Pbuf", None, "mma_wait_Sslot", "mma_wait_K", "mma_wait_P", "mma_wait_O",
+     "mma_wait_V"]) if name}
 diff = (out_tc.float() - step.out.float()).abs().max().item()
 lse_diff = (lse_tc - step.lse).abs().max().item()
 g = torch.cuda.CUDAGraph()
@@ -98,4 +106,4 @@ t_tc = timed(run_tc)
 print(json.dumps({"config": a.config, "sparsity": a.sparsity, "rows_per_unit": M, "units": U,
                   "keys_per_unit": round(step.cnt.float().mean().item(), 1),
                   "mma_sync_us": round(t_mma, 1), "tcgen05_prototype_us": round(t_tc, 1),
-                  "max_abs_diff_out": diff, "max_abs_diff_lse": lse_diff}))
+                  "max_abs_diff_out": diff, "max_abs_diff_lse": lse_diff, "cycles_per_tile_cta0": cycles}))
