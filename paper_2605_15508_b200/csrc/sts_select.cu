@@ -1,8 +1,8 @@
 // sts_select.cu — sparsity-mask construction on sm_100a.
 //
 // Two kernels, one CTA (1024 threads) per logical row:
-//   select_reg_kernel  token mode, rows <= 32K keys: the row lives in
-//                      registers (32 keys per thread), see below;
+//   select_reg_kernel  token mode, rows <= 36K keys: the row lives in
+//                      registers (up to 36 keys per thread), see below;
 //   select_kernel      page mode and longer rows: keys in shared memory or a
 //                      global slot.
 // Both give identical results (same keys, same radix rule, same emit order).
@@ -17,11 +17,13 @@
 // out sorted without a sort.
 //
 // Page mode (page_size > 1) reproduces src/sparsity.py:94-101: fp64 page sums
-// in numpy add.reduceat order (x0 + pairwise(x[1:]), see pairwise_sum), a
-// 64-bit-key radix select over pages, then page expansion.
+// in numpy add.reduceat order (x0 + pairwise(x[1:]), see pairwise_sum; by
+// lane octets for 9-129-token pages, page_key_lanes), all-pairs ranks for rows
+// of <= 256 pages or a 64-bit-key radix select over pages, then expansion by
+// selected page (or a scan over positions when extras are requested).
 //
-// Keys live in shared memory when the row fits (<= SEL_SMEM_MAX_LEN), else in
-// a per-CTA slot of the global workspace (persistent grid over rows).
+// select_kernel's keys live in shared memory when the row fits, else in a
+// per-CTA slot of the global workspace (persistent grid over rows).
 #include <stdlib.h>
 
 #include <type_traits>
@@ -670,7 +672,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) select_kernel(SelectParams p) 
 }
 
 // ---------------------------------------------------------------------------
-// Token mode with the row in registers (rows <= 32 * KPT * 32 keys).
+// Token mode with the row in registers (rows <= 32 * KPT * 32 keys, KPT <= 36).
 //
 // One 1024-thread CTA per row.  Warp w owns the contiguous slice
 // [w*32*KPT, (w+1)*32*KPT) of the row; lane l holds positions
