@@ -638,13 +638,14 @@ def run_single_gpu(args):
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e, 2), "unit": "us", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "what": "public API STSVerifyStep.attend_host: H2D of the target Q from pinned host memory, sparse "
-                        "target attention, D2H of the output; one CUDA graph, units in step.host_chunks groups so "
-                        "the copies of one group overlap the attention of the other",
-                "host_chunks": step.host_chunks},
+                        "target attention writing its output straight into the pinned host buffer (device-mapped; "
+                        "the output crosses the host link inside the kernel); one CUDA graph",
+                "output": "direct"},
         "e2e_step": {"value": round(e2e_step, 2), "unit": "us", "h2d_bytes_per_step": int(h2d_step),
                      "d2h_bytes_per_step": int(d2h),
-                     "what": "public API STSVerifyStep.step_host: H2D target+draft Q, draft capture, mask select, "
-                             "sparse attention (one CUDA graph), D2H output"},
+                     "what": "public API STSVerifyStep.step_host: H2D target+draft Q (target Q under capture + "
+                             "select), draft capture, mask select, sparse attention writing the pinned host output "
+                             "(one CUDA graph)"},
         "gpu_launches": int(launches),
         "launches_per_stage": stage_launches,
         "clocks": clocks.summary(),

@@ -240,19 +240,22 @@ class STSVerifyStep:
         return self.attend(target_q, target_k, target_v, stream)
 
     # -- host-buffer API (queries in from pinned host memory, output back out) --
-    def _graph(self, key, fn):
-        """CUDA graph of ``fn`` (captured once per key; replays launch no Python)."""
+    def _graph(self, key, fn, keep=()):
+        """CUDA graph of ``fn`` (captured once per key; replays launch no Python).
+        ``keep``: host tensors the graph reads or writes by address (the key
+        holds their pointers): held as long as the graph, so no other tensor
+        can take their memory while a replay may still touch it."""
         if not hasattr(self, "_graphs"):
             self._graphs = {}
-        g = self._graphs.get(key)
-        if g is None:
+        ent = self._graphs.get(key)
+        if ent is None:
             fn()  # warm-up outside capture (workspace allocations happen here)
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 fn()
-            self._graphs[key] = g
-        return g
+            ent = self._graphs[key] = (g, tuple(t for t in keep if t is not None))
+        return ent[0]
 
     def _host_buffers(self, h_dq, h_tq):
         """Device staging buffers for host queries (allocated once per shape)."""
@@ -262,21 +265,40 @@ class STSVerifyStep:
             self._d_dq = torch.empty(h_dq.shape, dtype=h_dq.dtype, device=self.device)
         return getattr(self, "_d_dq", None), self._d_tq
 
-    def attend_host(self, h_tq, target_k, target_v, h_out, chunks=None):
+    def attend_host(self, h_tq, target_k, target_v, h_out, chunks=None, direct_out=None):
         """Target attention with host queries: H2D copy of Q [B, L, Hq, R, d]
         (pinned), the attention, D2H copy of the output into ``h_out`` (pinned,
         shaped like ``self.out``).  The masks are the ones the last
         ``build_masks`` produced.
 
-        ``chunks`` > 1 pipelines the copies with the kernel: the units are cut
-        into ``chunks`` contiguous groups and, inside one CUDA graph, the H2D of
-        group c+1 and the D2H of group c-1 run on side streams while group c
-        attends, so the link time hides behind the HBM-bound kernel.
+        ``direct_out`` (default: when ``h_out`` is pinned): the attention
+        kernel writes the output straight into ``h_out`` over the host link
+        (pinned memory is device-mapped), so no D2H copy trails the kernel and
+        the result is bit-identical to the device-resident ``attend`` (one
+        launch).  Measured at c2: 138-142 µs vs 149-152 µs for the best
+        copy-engine form (``tools/e2e_direct_probe.py``).
+
+        Otherwise ``chunks`` > 1 pipelines the copies with the kernel: the units
+        are cut into ``chunks`` contiguous groups and, inside one CUDA graph,
+        the H2D of group c+1 and the D2H of group c-1 run on side streams while
+        group c attends, so the link time hides behind the HBM-bound kernel.
         """
-        chunks = self.host_chunks if chunks is None else int(chunks)
+        direct_out = h_out.is_pinned() if direct_out is None else bool(direct_out)
+        if direct_out:
+            chunks = 1 if chunks is None else int(chunks)
+        else:
+            chunks = self.host_chunks if chunks is None else int(chunks)
         _, d_tq = self._host_buffers(None, h_tq)
         q, k, v = self.target_views(d_tq, target_k, target_v)
         idx_ptr = self.idx.data_ptr() if self.idx is not None else 0
+        if direct_out:
+            if not h_out.is_pinned() or h_out.shape != self.out.shape or h_out.dtype != self.out.dtype:
+                raise ValueError("direct_out needs a pinned h_out shaped like step.out")
+            key = ("attend_host_direct", chunks, h_tq.data_ptr(), h_out.data_ptr(), target_k.data_ptr(),
+                   target_v.data_ptr(), idx_ptr)
+            self._graph(key, lambda: self._attend_pipelined(h_tq, d_tq, q, k, v, h_out, max(1, chunks),
+                                                            direct_out=True), keep=(h_tq, h_out)).replay()
+            return h_out
         if chunks <= 1:
             d_tq.copy_(h_tq, non_blocking=True)
             key = ("attend", target_k.data_ptr(), target_v.data_ptr(), idx_ptr)
@@ -285,10 +307,11 @@ class STSVerifyStep:
             return h_out
         key = ("attend_host", chunks, h_tq.data_ptr(), h_out.data_ptr(), target_k.data_ptr(), target_v.data_ptr(),
                idx_ptr)
-        self._graph(key, lambda: self._attend_pipelined(h_tq, d_tq, q, k, v, h_out, chunks)).replay()
+        self._graph(key, lambda: self._attend_pipelined(h_tq, d_tq, q, k, v, h_out, chunks),
+                    keep=(h_tq, h_out)).replay()
         return h_out
 
-    def _attend_pipelined(self, h_tq, d_tq, q, k, v, h_out, chunks):
+    def _attend_pipelined(self, h_tq, d_tq, q, k, v, h_out, chunks, direct_out=False):
         s = self.shape
         U = s.target_units
         C = max(1, min(chunks, U))
@@ -309,26 +332,32 @@ class STSVerifyStep:
             member = self.member[u0:u1] if self.member is not None else None
             kernels.sparse_decode(q[u0:u1], k[u0:u1], v[u0:u1], idx=self.idx[u0:u1], cnt=self.cnt[u0:u1],
                                   member=member, causal_base=causal, rows_per_head=s.rows, schedule=self.schedule,
-                                  out=self.out[u0:u1], lse=self.lse[u0:u1], status=self.status,
-                                  workspace=self.ws_dec, stream=main)
+                                  out=h_out[u0:u1] if direct_out else self.out[u0:u1], lse=self.lse[u0:u1],
+                                  status=self.status, workspace=self.ws_dec, stream=main)
+            if direct_out:
+                continue
             s_out.wait_stream(main)
             with torch.cuda.stream(s_out):
                 ho[u0:u1].copy_(self.out[u0:u1].view(u1 - u0, -1), non_blocking=True)
         main.wait_stream(s_out)
 
-    def step_host(self, h_dq, draft_k, h_tq, target_k, target_v, h_out, chunks=None):
+    def step_host(self, h_dq, draft_k, h_tq, target_k, target_v, h_out, chunks=None, direct_out=None):
         """The whole verify step with host queries (draft Q [B, Ld, Hqd, R, dd]
         and target Q), replayed as one CUDA graph; output copied to ``h_out``.
 
         With ``chunks`` > 1 (default ``host_chunks``) the copies ride inside the
         graph: the target-Q H2D runs on a side stream under the capture and
         select stages, and the output D2H of each unit group overlaps the
-        attention of the next."""
-        chunks = self.host_chunks if chunks is None else int(chunks)
+        attention of the next.  With a pinned ``h_out`` the attention writes the
+        output there directly (see ``attend_host``)."""
+        direct_out = h_out.is_pinned() if direct_out is None else bool(direct_out)
+        if direct_out and (h_out.shape != self.out.shape or h_out.dtype != self.out.dtype):
+            raise ValueError("h_out must be shaped like step.out")
+        chunks = 1 if direct_out else (self.host_chunks if chunks is None else int(chunks))
         d_dq, d_tq = self._host_buffers(h_dq, h_tq)
         dq, dk = self.draft_views(d_dq, draft_k)
         q, k, v = self.target_views(d_tq, target_k, target_v)
-        if chunks <= 1:
+        if chunks <= 1 and not direct_out:
             d_dq.copy_(h_dq, non_blocking=True)
             d_tq.copy_(h_tq, non_blocking=True)
             key = ("step", draft_k.data_ptr(), target_k.data_ptr(), target_v.data_ptr())
@@ -348,11 +377,11 @@ class STSVerifyStep:
             self.capture(dq, dk)
             self.build_masks()
             main.wait_stream(s_in)
-            self._attend_pipelined(None, d_tq, q, k, v, h_out, chunks)
+            self._attend_pipelined(None, d_tq, q, k, v, h_out, chunks, direct_out=direct_out)
 
-        key = ("step_host", chunks, h_dq.data_ptr(), h_tq.data_ptr(), h_out.data_ptr(), draft_k.data_ptr(),
+        key = ("step_host", chunks, direct_out, h_dq.data_ptr(), h_tq.data_ptr(), h_out.data_ptr(), draft_k.data_ptr(),
                target_k.data_ptr(), target_v.data_ptr())
-        self._graph(key, body).replay()
+        self._graph(key, body, keep=(h_dq, h_tq, h_out)).replay()
         return h_out
 
     def _streams(self):

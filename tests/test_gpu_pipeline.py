@@ -176,33 +176,45 @@ def test_host_buffer_api_matches_device_path(cuda_ok):
         step.step_host(dq.cpu().pin_memory(), dk, tq.cpu().pin_memory(), tk, tv, h_out, chunks=1)
         torch.cuda.synchronize()
         assert torch.equal(h_out, want.cpu())
-    h_out.zero_()
-    step.attend_host(tq.cpu().pin_memory(), tk, tv, h_out, chunks=1)
-    torch.cuda.synchronize()
-    assert torch.equal(h_out, want.cpu())
-    # pipelined copies (units in C groups; per-group work splits differ, so
-    # the fp32 merge order may differ from the one-launch run: tolerance)
+    # default: the kernel writes the pinned output directly (one launch); and
+    # the copy-engine form (D2H after the kernel)
+    for kw in ({}, {"direct_out": False, "chunks": 1}):
+        for _ in range(2):
+            h_out.zero_()
+            step.attend_host(tq.cpu().pin_memory(), tk, tv, h_out, **kw)
+            torch.cuda.synchronize()
+            assert torch.equal(h_out, want.cpu()), kw
+    # units in C groups (pipelined copies or direct writes; per-group work
+    # splits differ, so the fp32 merge order may differ from the one-launch
+    # run: tolerance)
     h_tq = tq.cpu().pin_memory()
     for C in (2, 3):
-        got = []
-        for _ in range(2):  # capture, then replay: deterministic
-            h_out.zero_()
-            step.attend_host(h_tq, tk, tv, h_out, chunks=C)
-            torch.cuda.synchronize()
-            got.append(h_out.clone())
-        assert torch.equal(got[0], got[1])
-        torch.testing.assert_close(got[0].float(), want.cpu().float(), rtol=2e-2, atol=2e-2)
+        for direct in (False, True):
+            got = []
+            for _ in range(2):  # capture, then replay: deterministic
+                h_out.zero_()
+                step.attend_host(h_tq, tk, tv, h_out, chunks=C, direct_out=direct)
+                torch.cuda.synchronize()
+                got.append(h_out.clone())
+            assert torch.equal(got[0], got[1])
+            torch.testing.assert_close(got[0].float(), want.cpu().float(), rtol=2e-2, atol=2e-2)
     # the whole step with in-graph copies (target-Q H2D under capture + select,
     # D2H per unit group): same masks, attention within tolerance, deterministic
     h_dq = dq.cpu().pin_memory()
     got = []
     for _ in range(2):
         h_out.zero_()
-        step.step_host(h_dq, dk, h_tq, tk, tv, h_out, chunks=2)
+        step.step_host(h_dq, dk, h_tq, tk, tv, h_out, chunks=2, direct_out=False)
         torch.cuda.synchronize()
         got.append(h_out.clone())
     assert torch.equal(got[0], got[1])
     torch.testing.assert_close(got[0].float(), want.cpu().float(), rtol=2e-2, atol=2e-2)
+    # default with a pinned output: in-graph target-Q H2D, the kernel writes
+    # the output directly (one attention launch: bit-exact)
+    h_out.zero_()
+    step.step_host(h_dq, dk, h_tq, tk, tv, h_out)
+    torch.cuda.synchronize()
+    assert torch.equal(h_out, want.cpu())
 
 
 def test_mask_agreement_with_fp64_reference_rows(cuda_ok):
