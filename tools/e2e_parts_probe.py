@@ -1,7 +1,7 @@
-import json, sys, os
 """Components of the host-buffer e2e at c2, each as its own CUDA graph with the
 bench's L2 flush: device attention, attention writing the pinned host output,
 H2D of the target Q, D2H of the output."""
+import json, sys, os
 sys.path.insert(0, os.getcwd())
 import torch
 from paper_2605_15508_b200 import SparsityConfig
