@@ -271,7 +271,7 @@ class STSVerifyStep:
         shaped like ``self.out``).  The masks are the ones the last
         ``build_masks`` produced.
 
-        ``direct_out`` (default: when ``h_out`` is pinned): the attention
+        ``direct_out`` (default: when ``h_out`` is pinned and contiguous): the attention
         kernel writes the output straight into ``h_out`` over the host link
         (pinned memory is device-mapped), so no D2H copy trails the kernel and
         the result is bit-identical to the device-resident ``attend`` (one
@@ -283,7 +283,7 @@ class STSVerifyStep:
         the H2D of group c+1 and the D2H of group c-1 run on side streams while
         group c attends, so the link time hides behind the HBM-bound kernel.
         """
-        direct_out = h_out.is_pinned() if direct_out is None else bool(direct_out)
+        direct_out, h_dst = self._direct_view(h_out, direct_out)
         if direct_out:
             chunks = 1 if chunks is None else int(chunks)
         else:
@@ -292,11 +292,9 @@ class STSVerifyStep:
         q, k, v = self.target_views(d_tq, target_k, target_v)
         idx_ptr = self.idx.data_ptr() if self.idx is not None else 0
         if direct_out:
-            if not h_out.is_pinned() or h_out.shape != self.out.shape or h_out.dtype != self.out.dtype:
-                raise ValueError("direct_out needs a pinned h_out shaped like step.out")
             key = ("attend_host_direct", chunks, h_tq.data_ptr(), h_out.data_ptr(), target_k.data_ptr(),
                    target_v.data_ptr(), idx_ptr)
-            self._graph(key, lambda: self._attend_pipelined(h_tq, d_tq, q, k, v, h_out, max(1, chunks),
+            self._graph(key, lambda: self._attend_pipelined(h_tq, d_tq, q, k, v, h_dst, max(1, chunks),
                                                             direct_out=True), keep=(h_tq, h_out)).replay()
             return h_out
         if chunks <= 1:
@@ -310,6 +308,18 @@ class STSVerifyStep:
         self._graph(key, lambda: self._attend_pipelined(h_tq, d_tq, q, k, v, h_out, chunks),
                     keep=(h_tq, h_out)).replay()
         return h_out
+
+    def _direct_view(self, h_out, direct_out):
+        """Whether the kernel writes ``h_out`` itself, and ``h_out`` viewed as
+        ``step.out`` for that: by default when h_out is pinned, contiguous and
+        holds step.out's elements in its dtype; ``direct_out=True`` requires it."""
+        ok = (h_out.is_pinned() and h_out.is_contiguous() and h_out.numel() == self.out.numel()
+              and h_out.dtype == self.out.dtype)
+        if direct_out is None:
+            direct_out = ok
+        elif direct_out and not ok:
+            raise ValueError("direct_out needs a pinned, contiguous h_out with step.out's size and dtype")
+        return bool(direct_out), (h_out.view(self.out.shape) if direct_out else h_out)
 
     def _attend_pipelined(self, h_tq, d_tq, q, k, v, h_out, chunks, direct_out=False):
         s = self.shape
@@ -350,9 +360,7 @@ class STSVerifyStep:
         select stages, and the output D2H of each unit group overlaps the
         attention of the next.  With a pinned ``h_out`` the attention writes the
         output there directly (see ``attend_host``)."""
-        direct_out = h_out.is_pinned() if direct_out is None else bool(direct_out)
-        if direct_out and (h_out.shape != self.out.shape or h_out.dtype != self.out.dtype):
-            raise ValueError("h_out must be shaped like step.out")
+        direct_out, h_dst = self._direct_view(h_out, direct_out)
         chunks = 1 if direct_out else (self.host_chunks if chunks is None else int(chunks))
         d_dq, d_tq = self._host_buffers(h_dq, h_tq)
         dq, dk = self.draft_views(d_dq, draft_k)
@@ -377,7 +385,7 @@ class STSVerifyStep:
             self.capture(dq, dk)
             self.build_masks()
             main.wait_stream(s_in)
-            self._attend_pipelined(None, d_tq, q, k, v, h_out, chunks, direct_out=direct_out)
+            self._attend_pipelined(None, d_tq, q, k, v, h_dst, chunks, direct_out=direct_out)
 
         key = ("step_host", chunks, direct_out, h_dq.data_ptr(), h_tq.data_ptr(), h_out.data_ptr(), draft_k.data_ptr(),
                target_k.data_ptr(), target_v.data_ptr())

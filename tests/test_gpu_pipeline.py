@@ -184,6 +184,11 @@ def test_host_buffer_api_matches_device_path(cuda_ok):
             step.attend_host(tq.cpu().pin_memory(), tk, tv, h_out, **kw)
             torch.cuda.synchronize()
             assert torch.equal(h_out, want.cpu()), kw
+    # a pinned output of another shape with the same elements (flat): direct
+    h_flat = torch.empty(want.numel(), dtype=want.dtype).pin_memory()
+    step.attend_host(tq.cpu().pin_memory(), tk, tv, h_flat)
+    torch.cuda.synchronize()
+    assert torch.equal(h_flat.view(want.shape), want.cpu())
     # units in C groups (pipelined copies or direct writes; per-group work
     # splits differ, so the fp32 merge order may differ from the one-launch
     # run: tolerance)
