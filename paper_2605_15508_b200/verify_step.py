@@ -240,6 +240,8 @@ class STSVerifyStep:
         return self.attend(target_q, target_k, target_v, stream)
 
     # -- host-buffer API (queries in from pinned host memory, output back out) --
+    _GRAPH_CACHE = 32
+
     def _graph(self, key, fn, keep=()):
         """CUDA graph of ``fn`` (captured once per key; replays launch no Python).
         ``keep``: host tensors the graph reads or writes by address (the key
@@ -249,6 +251,12 @@ class STSVerifyStep:
             self._graphs = {}
         ent = self._graphs.get(key)
         if ent is None:
+            if len(self._graphs) >= self._GRAPH_CACHE:
+                # bounded: callers passing fresh host buffers every call would
+                # otherwise grow the cache (and the buffers it holds) forever;
+                # evict the oldest once no replay of it can still be running
+                torch.cuda.synchronize(self.device)
+                self._graphs.pop(next(iter(self._graphs)))
             fn()  # warm-up outside capture (workspace allocations happen here)
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()

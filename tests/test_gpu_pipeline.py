@@ -238,3 +238,25 @@ def test_mask_agreement_with_fp64_reference_rows(cuda_ok):
     torch.cuda.synchronize()
     agree = parity.mask_agreement(step, dq, dk, list(range(s.target_units)))
     assert agree["recall"] >= 0.99 and agree["min_recall"] >= 0.97, agree
+
+
+def test_host_api_graph_cache_bounded(cuda_ok):
+    """Fresh host buffers on every call: each call captures a graph that holds
+    its buffers; the cache stays bounded and every result is right."""
+    import torch
+
+    from paper_2605_15508_b200 import SparsityConfig
+    from paper_2605_15508_b200.verify_step import STSVerifyStep, random_mapping_table, synthetic_inputs
+
+    s = _small_shape()
+    step = STSVerifyStep(s, SparsityConfig(budget=0.1), random_mapping_table(s, seed=2), mode="S")
+    dq, dk, tq, tk, tv = synthetic_inputs(s, "cuda", seed=3)
+    q, k, v = step.target_views(tq, tk, tv)
+    out, _ = step.step(*step.draft_views(dq, dk), q, k, v)
+    want = out.cpu()
+    for _ in range(step._GRAPH_CACHE + 8):
+        h_out = torch.empty(want.shape, dtype=want.dtype).pin_memory()
+        step.attend_host(tq.cpu().pin_memory(), tk, tv, h_out)
+        torch.cuda.synchronize()
+        assert torch.equal(h_out, want)
+    assert len(step._graphs) <= step._GRAPH_CACHE
