@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define STS_ABI_VERSION 7
+#define STS_ABI_VERSION 8
 
 #define STS_OK 0
 #define STS_ERR_INPUT 1
@@ -328,6 +328,16 @@ STS_API int sts_page_cache_plan(const int32_t* idx_dev, int64_t idx_ld, const in
                                 int32_t* slot_last_dev, int64_t slots_ld, int32_t slots, int32_t step,
                                 int32_t* copy_pages_dev, int32_t* copy_slots_dev, int32_t* ncopy_dev,
                                 int32_t* idx_pool_dev, int32_t* status_dev, void* stream);
+
+/* sts_kv_prefetch_l2 — L2 prefetch of selected K/V rows (no result depends
+ * on it): for each unit, the rows of the first keys_per_part keys of each of
+ * `parts` contiguous shares of its idx list (cnt keys; idx null = keys
+ * 0..cnt-1). Used by the host-buffer verify step to pull the attention's
+ * first rows into L2 while the queries are still crossing the host link. */
+STS_API int sts_kv_prefetch_l2(const void* k_cache_dev, const void* v_cache_dev, int64_t kv_unit_stride,
+                               int64_t kv_row_stride, int64_t units, int32_t d, int32_t elem_bytes,
+                               const int32_t* idx_dev, int64_t idx_ld, const int32_t* cnt_dev, int32_t parts,
+                               int32_t keys_per_part, void* stream);
 
 /* ------------------------------------------------------------------------
  * sts_prefill_blocksparse — block-sparse prefill attention on tcgen05

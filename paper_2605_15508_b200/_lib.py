@@ -25,7 +25,7 @@ STS_DEV_EMPTY_ROW = 0x2
 STS_DEV_BAD_INDEX = 0x4
 STS_DEV_SELECT_INCONSISTENT = 0x8
 STS_BLOCK_INCLUDE_SELF = 0x1
-ABI_VERSION = 7
+ABI_VERSION = 8
 
 _i32, _i64, _u32, _f32, _f64 = C.c_int32, C.c_int64, C.c_uint32, C.c_float, C.c_double
 _p, _sz = C.c_void_p, C.c_size_t
@@ -51,6 +51,7 @@ SIGNATURES = {
                                 _p, _p, _sz, _p]),
     "sts_draft_probs": (C.c_int, [_i32, _p, _p, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _i32, _f32,
                                   _p, _i32, _p, _i64, _p]),
+    "sts_kv_prefetch_l2": (C.c_int, [_p, _p, _i64, _i64, _i64, _i32, _i32, _p, _i64, _p, _i32, _i32, _p]),
     "sts_draft_scores": (C.c_int, [_i32, _p, _p, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _i32, _f32,
                                    _p, _i64, _p]),
     "sts_lse_merge": (C.c_int, [_p, _p, _i32, _i64, _i32, _i32, _p, _p, _p]),

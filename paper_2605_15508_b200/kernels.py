@@ -190,6 +190,20 @@ def sparse_decode(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor,
     return out, lse
 
 
+def kv_prefetch_l2(k_cache: torch.Tensor, v_cache: torch.Tensor, *, idx=None, cnt, parts: int = 1,
+                   keys_per_part: int, stream=None):
+    """Prefetch into L2 the K/V rows of the first ``keys_per_part`` keys of
+    each of ``parts`` contiguous shares of every unit's key list
+    (sts_kv_prefetch_l2). No output; nothing depends on it for correctness."""
+    _require_cuda(k_cache, v_cache, idx, cnt)
+    U, _, d = k_cache.shape
+    if k_cache.stride(-1) != 1 or v_cache.stride() != k_cache.stride():
+        raise ValueError("k_cache/v_cache must be [U, N, d] views with unit inner stride and equal strides")
+    call("sts_kv_prefetch_l2", ptr(k_cache), ptr(v_cache), k_cache.stride(0), k_cache.stride(1), U, d,
+         k_cache.element_size(), ptr(idx), idx.stride(0) if idx is not None else 0, ptr(cnt), int(parts),
+         int(keys_per_part), stream_handle(stream))
+
+
 def sparse_prefill(q: torch.Tensor, k_cache: torch.Tensor, v_cache: torch.Tensor, *, idx, cnt, scale=None,
                    out=None, lse=None, out_dtype=None, status=None, workspace: Workspace | None = None, stream=None):
     """Sparse prefill attention (STS-PD): every query row has its own key list.

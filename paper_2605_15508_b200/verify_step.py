@@ -33,7 +33,7 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-from . import kernels
+from . import _lib, kernels
 from .kernels import Workspace
 from .sparsity import SparsityConfig
 
@@ -171,6 +171,8 @@ class STSVerifyStep:
         # unit groups of the host-buffer attention pipeline (see attend_host)
         # (2 measured best at c2: 157 vs 200 µs for 1, 200 for 3 — tools/gpu_e2e_chunks.sh)
         self.host_chunks = int(os.environ.get("STS_HOST_CHUNKS", "2"))
+        # host-buffer attention: K/V bytes pulled into L2 while Q is copied in
+        self.l2_prefetch_bytes = 32 << 20  # 24-48 MB: 134 vs 140 us at c2 (tools/e2e_direct_probe.py)
 
     # -- the four stages ----------------------------------------------------------
     def capture(self, draft_q, draft_k, stream=None):
@@ -300,8 +302,8 @@ class STSVerifyStep:
         q, k, v = self.target_views(d_tq, target_k, target_v)
         idx_ptr = self.idx.data_ptr() if self.idx is not None else 0
         if direct_out:
-            key = ("attend_host_direct", chunks, h_tq.data_ptr(), h_out.data_ptr(), target_k.data_ptr(),
-                   target_v.data_ptr(), idx_ptr)
+            key = ("attend_host_direct", chunks, self.l2_prefetch_bytes, h_tq.data_ptr(), h_out.data_ptr(),
+                   target_k.data_ptr(), target_v.data_ptr(), idx_ptr)
             self._graph(key, lambda: self._attend_pipelined(h_tq, d_tq, q, k, v, h_dst, max(1, chunks),
                                                             direct_out=True), keep=(h_tq, h_out)).replay()
             return h_out
@@ -311,11 +313,27 @@ class STSVerifyStep:
             self._graph(key, lambda: self.attend(q, k, v)).replay()
             h_out.copy_(self.out, non_blocking=True)
             return h_out
-        key = ("attend_host", chunks, h_tq.data_ptr(), h_out.data_ptr(), target_k.data_ptr(), target_v.data_ptr(),
-               idx_ptr)
+        key = ("attend_host", chunks, self.l2_prefetch_bytes, h_tq.data_ptr(), h_out.data_ptr(), target_k.data_ptr(),
+               target_v.data_ptr(), idx_ptr)
         self._graph(key, lambda: self._attend_pipelined(h_tq, d_tq, q, k, v, h_out, chunks),
                     keep=(h_tq, h_out)).replay()
         return h_out
+
+    def _prefetch_first_rows(self, k, v, u0, u1, stream):
+        """While the first queries cross the host link: the K/V rows each CTA
+        of the attention reads first, into L2 (``l2_prefetch_bytes`` in all;
+        0 disables). The shares follow the schedule the decode will use."""
+        if not self.l2_prefetch_bytes or self.idx is None:
+            return
+        s = self.shape
+        nu = u1 - u0
+        sched = int(_lib.load().sts_sparse_decode_schedule(nu, self.M, s.head_dim, self.idx_ld, self.schedule))
+        parts = sched if sched >= 2 else 1
+        row = 2 * s.head_dim * k.element_size()  # K and V
+        kpp = int(self.l2_prefetch_bytes // (nu * parts * row))
+        if kpp > 0:
+            kernels.kv_prefetch_l2(k, v, idx=self.idx[u0:u1], cnt=self.cnt[u0:u1], parts=parts, keys_per_part=kpp,
+                                   stream=stream)
 
     def _direct_view(self, h_out, direct_out):
         """Whether the kernel writes ``h_out`` itself, and ``h_out`` viewed as
@@ -346,6 +364,8 @@ class STSVerifyStep:
             if hq is not None:
                 with torch.cuda.stream(s_in):
                     dq_[u0:u1].copy_(hq[u0:u1], non_blocking=True)
+                if c == 0:
+                    self._prefetch_first_rows(k[u0:u1], v[u0:u1], u0, u1, main)
                 main.wait_stream(s_in)
             member = self.member[u0:u1] if self.member is not None else None
             kernels.sparse_decode(q[u0:u1], k[u0:u1], v[u0:u1], idx=self.idx[u0:u1], cnt=self.cnt[u0:u1],

@@ -29,7 +29,7 @@ def test_library_builds_and_exports_header_symbols():
     nm = subprocess.run(["nm", "-D", "--defined-only", str(lib_path)], capture_output=True, text=True).stdout
     exported = set(re.findall(r" T (sts_\w+)", nm))
     assert declared <= exported, f"missing exports: {declared - exported}"
-    assert lib.sts_abi_version() == _lib.ABI_VERSION == 7
+    assert lib.sts_abi_version() == _lib.ABI_VERSION == 8
     assert lib.sts_dist_select_bins() == _lib.STS_DIST_BINS
 
 

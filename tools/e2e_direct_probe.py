@@ -1,7 +1,8 @@
 #!/usr/bin/env python
 """attend_host with the output copied back by the copy engine (D2H after
 each unit group) vs written by the attention kernel straight into the pinned
-host buffer (direct_out): time per call as bench.py's e2e measures it, and
+host buffer (direct_out), and the L2 prefetch of the first K/V rows beside
+the Q copy (step.l2_prefetch_bytes, MB in the key): time per call as bench.py's e2e measures it, and
 equality of the host output with the device-resident attention.
 
     python tools/e2e_direct_probe.py [c2]
@@ -33,8 +34,9 @@ flush = L2Flush(torch.device("cuda"), "clean")
 h_tq = tq.cpu().pin_memory()
 res = {"config": cfg_name, "out_bytes": ref.numel() * ref.element_size()}
 st = torch.cuda.current_stream()
-for direct, chunks, busy in ((False, 2, 0), (False, 1, 0), (True, 1, 0), (True, 2, 0), (True, 3, 0),
-                             (False, 2, 1), (True, 1, 1), (True, 2, 1)):
+for direct, chunks, busy, pf_mb in ((False, 2, 0, 0), (True, 1, 0, 0), (True, 1, 0, 16), (True, 1, 0, 32),
+                                    (True, 1, 0, 48), (True, 1, 1, 32)):
+    step.l2_prefetch_bytes = pf_mb << 20
     if True:
         h_out = torch.zeros(step.out.shape, dtype=step.out.dtype).pin_memory()
         ts = []
@@ -50,7 +52,9 @@ for direct, chunks, busy in ((False, 2, 0), (False, 1, 0), (True, 1, 0), (True, 
             if i >= 5:
                 ts.append(a.elapsed_time(b) * 1e3)
         ts.sort()
-        key = f"{'direct' if direct else 'copy'}_c{chunks}" + ("_busy" if busy else "")
+        key = f"{'direct' if direct else 'copy'}_c{chunks}" + ("_busy" if busy else "") + f"_pf{pf_mb}"
+        if key + "_us_median" in res:
+            key += "_again"
         res[key + "_us_median"] = round(ts[len(ts) // 2], 1)
         res[key + "_us_mean"] = round(sum(ts) / len(ts), 1)
         res[key + "_equal"] = bool(torch.equal(h_out, ref.cpu()))
