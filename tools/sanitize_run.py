@@ -70,6 +70,8 @@ if "prefill" in which:
         idx[r, : m.size] = torch.from_numpy(m.astype(np.int32))
         cnt[r] = m.size
     kernels.sparse_prefill(q, kk, vv, idx=idx, cnt=cnt)
+    # L2 prefetch of K/V rows (the host-buffer verify step): idx / cnt reads
+    kernels.kv_prefetch_l2(kk, vv, idx=idx[::n].contiguous(), cnt=cnt[::n].contiguous(), parts=3, keys_per_part=8)
 if "block" in which:
     H, m, d, start = 3, 4, 16, 40
     kk = torch.randn((H, start + m, d), generator=g, device=dev)
